@@ -1,0 +1,256 @@
+"""Seeded synthetic Loghub-shaped workloads in the token-id domain.
+
+This module is the ONLY code shared by the CUDA path's callers (tests, bench) and the
+oracle's callers. It holds input generation only: no similarity, no top-k, no PAIR,
+no hashing, no attention. Nothing here is the method's arithmetic.
+
+Recipe:
+  * templates: length U[4,20]; each position constant w.p. 0.75 else a ``<*>`` slot (>=1
+    slot); constants drawn Zipf(1.0) over a 2,000-id dataset vocabulary, so templates
+    share words and similarity is non-trivial.  Template tokens = constants + PH.
+  * popularity: Zipf(s) over templates (template 0 hottest) — the hotspot structure of
+    PAPER.md P:256-257 (fig:hotspot).
+  * logs: each slot of each template owns a value pool of U[1,1000] values; a value is a
+    run of U[1, w] tokens (w ~ U[1,8] per slot) drawn from a per-slot alphabet of U[4,40]
+    fresh ids — numbers, IPs and block ids are several BPE tokens long and share digit
+    chunks — so logs of one template differ in length and in partial overlap.  A
+    log is its template with each slot replaced by a value drawn uniformly from the slot's
+    pool (exact repeats happen).
+  * pool: seeded uniform sample of M logs without replacement ("samples 200 logs
+    from each log dataset"), kept in dataset-row order.
+  * queries: every log in dataset order, cycled; batch b = next B queries
+    (closed-loop concurrency B).
+  * instruction: I fixed tokens from a separate id range ("Common Instruction").
+  * Q/K/V: a counter-based generator of (seed, token, absolute position, head, dim),
+    SURVEY §8(c) Z28, so a cached page equals recomputation (cache transparency).
+
+Token ids: 0 PAD, 1 SEP, 2 TPL, 3 PH (the ``<*>`` placeholder), 4..15 spare; real >= 16.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+import numpy as np
+
+PAD, SEP, TPL, PH = 0, 1, 2, 3
+VOCAB_BASE = 16          # dataset vocabulary ids live in [16, 16 + vocab)
+INSTR_BASE = 1 << 20     # instruction ids
+VALUE_BASE = 1 << 22     # slot-value ids (numbers, IPs, block ids ...)
+
+# The 16 Loghub-2k systems named in PAPER.md P:599-614, with approximate public template
+# counts (NOT given in PAPER.md: tunable knobs).
+LOGHUB16 = [
+    ("Android", 166), ("Apache", 6), ("BGL", 120), ("Hadoop", 114), ("HDFS", 14),
+    ("HealthApp", 75), ("HPC", 46), ("Linux", 118), ("Mac", 341), ("OpenSSH", 27),
+    ("OpenStack", 43), ("Proxifier", 8), ("Spark", 36), ("Thunderbird", 149),
+    ("Windows", 50), ("Zookeeper", 50),
+]
+
+
+@dataclass
+class Dataset:
+    name: str
+    templates: list            # list[np.ndarray uint32] template tokens (PH at slots)
+    log_off: np.ndarray        # [n+1] uint32 CSR offsets
+    log_tok: np.ndarray        # [sum] uint32
+    log_tpl: np.ndarray        # [n] uint32 template id of each log
+
+    @property
+    def n(self) -> int:
+        return len(self.log_tpl)
+
+    def log(self, r: int) -> np.ndarray:
+        return self.log_tok[self.log_off[r]:self.log_off[r + 1]]
+
+
+@dataclass
+class Pool:
+    """The candidate set: per-demo log tokens, template tokens, template id, row."""
+    log_off: np.ndarray
+    log_tok: np.ndarray
+    tpl_off: np.ndarray
+    tpl_tok: np.ndarray
+    template_id: np.ndarray
+    src_index: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return len(self.template_id)
+
+
+@dataclass
+class Batch:
+    q_off: np.ndarray   # [B+1] uint32
+    q_tok: np.ndarray   # [sum] uint32
+    q_src: np.ndarray   # [B] uint32 dataset row of each query
+
+    @property
+    def B(self) -> int:
+        return len(self.q_src)
+
+
+def _zipf_probs(n: int, s: float) -> np.ndarray:
+    w = 1.0 / np.arange(1, n + 1, dtype=np.float64) ** s
+    return w / w.sum()
+
+
+def make_dataset(name: str, n_logs: int, n_templates: int, zipf_s: float, seed: int,
+                 vocab: int = 2000, len_range=(4, 20), p_const: float = 0.75,
+                 value_pool_range=(1, 1000), value_base: int = VALUE_BASE,
+                 max_value_len: int = 8) -> Dataset:
+    rng = np.random.default_rng(seed)
+    word_p = _zipf_probs(vocab, 1.0)
+    templates, slot_pools, seen = [], [], set()
+    next_value = value_base
+    while len(templates) < n_templates:
+        ell = int(rng.integers(len_range[0], len_range[1] + 1))
+        is_slot = rng.random(ell) >= p_const
+        if not is_slot.any():
+            is_slot[int(rng.integers(ell))] = True
+        words = VOCAB_BASE + rng.choice(vocab, size=ell, p=word_p)
+        tpl = np.where(is_slot, PH, words).astype(np.uint32)
+        key = tpl.tobytes()
+        if key in seen:            # template_id is a pure function of template text
+            continue
+        seen.add(key)
+        pools = []
+        for pos in np.flatnonzero(is_slot):
+            sz = int(rng.integers(value_pool_range[0], value_pool_range[1] + 1))
+            w = int(rng.integers(1, max_value_len + 1))
+            alpha = int(rng.integers(4, 41))
+            vlen = rng.integers(1, w + 1, size=sz)
+            vals = [(next_value + rng.integers(0, alpha, size=vlen[v])).astype(np.uint32)
+                    for v in range(sz)]
+            pools.append((int(pos), vals))
+            next_value += alpha
+        templates.append(tpl)
+        slot_pools.append(pools)
+    pop = _zipf_probs(n_templates, zipf_s)
+    log_tpl = rng.choice(n_templates, size=n_logs, p=pop).astype(np.uint32)
+    rows = []
+    for t in log_tpl:
+        parts, prev = [], 0
+        for pos, vals in slot_pools[t]:
+            parts.append(templates[t][prev:pos])
+            parts.append(vals[int(rng.integers(len(vals)))])
+            prev = pos + 1
+        parts.append(templates[t][prev:])
+        rows.append(np.concatenate(parts).astype(np.uint32))
+    log_off = np.zeros(n_logs + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in rows], out=log_off[1:])
+    log_tok = np.concatenate(rows).astype(np.uint32)
+    return Dataset(name, templates, log_off.astype(np.uint32), log_tok, log_tpl)
+
+
+def sample_pool(ds: Dataset, M: int, seed: int) -> Pool:
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(ds.n, size=M, replace=False)).astype(np.uint32)
+    log_lens = np.array([ds.log_off[r + 1] - ds.log_off[r] for r in rows], dtype=np.int64)
+    tpls = [ds.templates[ds.log_tpl[r]] for r in rows]
+    log_off = np.zeros(M + 1, dtype=np.int64); np.cumsum(log_lens, out=log_off[1:])
+    tpl_off = np.zeros(M + 1, dtype=np.int64); np.cumsum([len(t) for t in tpls], out=tpl_off[1:])
+    log_tok = np.concatenate([ds.log(int(r)) for r in rows]).astype(np.uint32)
+    tpl_tok = np.concatenate(tpls).astype(np.uint32)
+    return Pool(log_off.astype(np.uint32), log_tok, tpl_off.astype(np.uint32), tpl_tok,
+                ds.log_tpl[rows].astype(np.uint32), rows)
+
+
+def instruction(n_instr: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return (INSTR_BASE + rng.integers(0, 1 << 16, size=n_instr)).astype(np.uint32)
+
+
+def make_batch(ds: Dataset, start: int, B: int) -> Batch:
+    """Queries start..start+B-1 in dataset order, cycled."""
+    rows = (np.arange(start, start + B, dtype=np.int64) % ds.n).astype(np.uint32)
+    lens = (ds.log_off[rows + 1].astype(np.int64) - ds.log_off[rows].astype(np.int64))
+    q_off = np.zeros(B + 1, dtype=np.int64); np.cumsum(lens, out=q_off[1:])
+    q_tok = np.concatenate([ds.log(int(r)) for r in rows]) if B else np.zeros(0, np.uint32)
+    return Batch(q_off.astype(np.uint32), q_tok.astype(np.uint32), rows)
+
+
+# ----------------------------------------------------------------------------------------
+# Workload configurations (BASELINE.json configs)
+# ----------------------------------------------------------------------------------------
+@dataclass
+class Config:
+    name: str
+    datasets: list            # list of (name, n_logs, n_templates, zipf_s, seed)
+    M: int
+    k: int
+    B: int
+    n_instr: int
+    T: int
+    C: int
+    Hq: int
+    Hkv: int
+    d: int
+    pool_seed: int
+    qkv_seed: int = 3000
+    instr_seed: int = 77
+    max_prompt_tokens: int = 1024
+    extra: dict = field(default_factory=dict)
+
+
+def config(n: int) -> Config:
+    if n == 1:
+        return Config("c1-tiny-hdfs", [("HDFS", 2000, 14, 1.3, 1004)], M=200, k=3, B=100,
+                      n_instr=128, T=512, C=4096, Hq=4, Hkv=4, d=64, pool_seed=2004,
+                      max_prompt_tokens=512)
+    if n == 2:
+        return Config("c2-loghub16", [(nm, 2000, nt, 1.1, 1000 + j)
+                                      for j, (nm, nt) in enumerate(LOGHUB16)],
+                      M=200, k=5, B=256, n_instr=128, T=4096, C=73728, Hq=32, Hkv=8, d=128,
+                      pool_seed=2000, max_prompt_tokens=1024)
+    if n == 3:
+        return Config("c3-2k-prompts", [("C3", 32768, 300, 1.1, 4000)], M=200, k=5, B=1024,
+                      n_instr=1836, T=4096, C=73728, Hq=32, Hkv=8, d=128, pool_seed=4001,
+                      max_prompt_tokens=2560)
+    if n == 4:
+        return Config("c4-qwen14b-skewed", [("C4", 102400, 1000, 1.3, 5000)], M=10000, k=8,
+                      B=1024, n_instr=128, T=2048, C=45056, Hq=40, Hkv=8, d=128,
+                      pool_seed=5001, max_prompt_tokens=1536)
+    raise ValueError(f"unknown config {n}")
+
+
+# ----------------------------------------------------------------------------------------
+# Q/K/V counter-based generator.  A pure function of
+# (seed, token, absolute position, head, dim): the GPU helper il_synth_qkv implements the
+# same generator independently.
+# ----------------------------------------------------------------------------------------
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint64, copy=True)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(30); x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(27); x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+    return x
+
+
+QKV_TENSOR_SALT = {"q": 0x51, "k": 0x4B, "v": 0x56}
+
+
+def tensor_seed(seed: int, which: str) -> int:
+    return int(_mix(np.array([(seed << 8) ^ QKV_TENSOR_SALT[which]], dtype=np.uint64))[0])
+
+
+def synth_bf16_bits(seed: int, which: str, tokens: np.ndarray, positions: np.ndarray,
+                    n_heads: int, d: int, scale: float = 1.0) -> np.ndarray:
+    """[n][n_heads][d] uint16 bf16 bit patterns: x = (i32(u>>40) - 2^23)/2^23 * scale, RNE."""
+    s = np.uint64(tensor_seed(seed, which))
+    t = tokens.astype(np.uint64)[:, None, None]
+    p = positions.astype(np.uint64)[:, None, None]
+    hd = (np.arange(n_heads, dtype=np.uint64)[None, :, None] * np.uint64(256)
+          + np.arange(d, dtype=np.uint64)[None, None, :])
+    u = _mix(_mix(_mix(s ^ t) ^ p) ^ hd)
+    x = ((u >> np.uint64(40)).astype(np.int64) - (1 << 23)).astype(np.float32)
+    x = x * np.float32(scale / float(1 << 23))
+    b = x.view(np.uint32).astype(np.uint64)
+    rnd = ((b >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)
+    return ((b + rnd) >> np.uint64(16)).astype(np.uint16)
+
+
+def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
+    return (bits.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
