@@ -1,0 +1,202 @@
+/* il.h — C ABI of libinferlog_b200.so: the InferLog hot path on B200 (sm_100a).
+ *
+ * The path (§3.2, on top of prefix caching P:192-198):
+ *   il_refine_batch  kNN demo selection + PAIR matching / modifying /
+ *                    reordering against the ICL Table + prompt render
+ *   il_prefix_match  chained 16-token KV-block hashes + longest cached prefix (P:195-198,
+ *                    fig:prefixcache) + LRU pin / evict / page allocation
+ *   il_prefill_attn  only the uncached suffix runs: append its K/V to pages, then causal
+ *                    attention over the paged cached prefix + the suffix
+ *   il_commit        after the batch: insert the new blocks into the prefix index and apply
+ *                    the ICL Table update rules
+ *
+ * Conventions
+ *  - Pointers are DEVICE pointers unless the name ends in _h (host).  Every buffer is owned
+ *    by the caller (PyTorch allocates them); the workspace is handed over once at create and
+ *    the library never allocates device memory.
+ *  - All calls are asynchronous on the caller's stream and never synchronize, except
+ *    il_status_sync / il_stats_sync.  Device-computed sizes (sum of suffix lengths, pages
+ *    needed) stay on the device.
+ *  - Errors: host-detectable errors return immediately (IL_ERR_ARG / IL_ERR_STATE).  Errors
+ *    the device detects (capacity, an over-long prompt) latch into a device status word and
+ *    surface from il_status_sync(); after a latched error the context's cache state is
+ *    unspecified and it must be reloaded with il_pool_load.  il_last_error() returns the
+ *    calling thread's last message.
+ *  - Threading: one context per GPU; calls on a context must be serialized in admission
+ *    order (single writer).
+ *  - Determinism: integer outputs (top-k, final DS, PMC, rule, chain hashes, hit counts,
+ *    evicted set, table and index contents) are bit-exact functions of (config, inputs,
+ *    history) and equal the CPU oracle's (tests/test_parity_*.py).  Physical page numbers
+ *    are NOT part of that contract.
+ *
+ * Batch semantics (reading Z1): every request of a batch matches against the
+ * table and index as they were after the previous commit ("snapshot"), and the commit
+ * applies the batch's updates in admission order.  B = 1 reproduces the sequential
+ * semantics of the paper's OrderedDict ICL Table exactly.
+ */
+#ifndef INFERLOG_IL_H
+#define INFERLOG_IL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct il_ctx il_ctx;
+typedef struct CUstream_st* il_stream;   /* == cudaStream_t; NULL = legacy default stream */
+typedef uint16_t il_bf16;                /* bfloat16 bit pattern */
+
+typedef enum {
+  IL_OK = 0,
+  IL_ERR_ARG = 1,       /* bad size / flag; k > eligible demos ("argument error");
+                           a rendered prompt longer than max_prompt_tokens (latched) */
+  IL_ERR_CAPACITY = 2,  /* batch needs more KV pages than free + evictable, or
+                           more suffix rows than max_suffix_tokens (latched) */
+  IL_ERR_STATE = 3,     /* call out of order: refine before pool_load, commit before match */
+  IL_ERR_INTERNAL = 4,  /* device invariant broken ("internal error") */
+  IL_ERR_CUDA = 5       /* a CUDA runtime call failed (message in il_last_error) */
+} il_status;
+
+typedef enum { IL_SIM_COSINE = 0, IL_SIM_JACCARD = 1 } il_sim;
+
+enum {
+  IL_F_PAIR = 1u << 0,         /* PAIR on; off = naive prefix caching (paper baseline "PC") */
+  IL_F_GUARD = 1u << 1,        /* never-worse guard (Z25; not in the paper) */
+  IL_F_EXCLUDE_SELF = 1u << 2, /* a query never selects its own dataset row */
+  IL_F_VERIFY = 1u << 3        /* a hit also requires equal block tokens + parent hash (Z19) */
+};
+
+typedef struct {
+  uint32_t k;                  /* demonstrations per prompt (N in P:357), 1..8 */
+  uint32_t table_capacity;     /* T: ICL Table entries, <= 8192 */
+  uint32_t kv_pages;           /* C: 16-token KV pages in the caller's page tensors */
+  uint32_t max_batch;          /* B per call, <= 8192 */
+  uint32_t max_prompt_tokens;  /* prompt row stride; longer prompts latch IL_ERR_ARG */
+  uint32_t max_pool;           /* M: demos in the pool */
+  uint32_t max_pool_tokens;    /* sum over demos of (log + template) tokens */
+  uint32_t max_log_tokens;     /* longest log (demo or query), <= 256 */
+  uint32_t max_suffix_tokens;  /* rows of q / k_new / v_new / out the caller allocated */
+  uint32_t n_q_heads, n_kv_heads, head_dim;   /* Hq % Hkv == 0; head_dim 64 or 128 */
+  uint32_t metric;             /* il_sim */
+  uint32_t flags;              /* IL_F_* */
+  uint64_t hash_seed;          /* chain-hash root (Z17) */
+} il_config;
+
+/* Per-request refinement outcome (SPEC S:190-193 RefinementResult). */
+typedef struct {
+  uint64_t target_stamp;       /* recency stamp of DS_target, (batch << 32 | admission index); 0 = none */
+  int32_t target_slot;         /* device table slot of DS_target; -1 = none */
+  uint8_t pmc;                 /* prefix-matching count of DS_target; 0 = none */
+  uint8_t rule;                /* 1, 2 or 3 */
+  uint8_t reverted;            /* the guard kept DS_current (Z25) */
+  uint8_t matched;             /* a target with PMC >= 1 was found */
+} il_refine_info;
+
+typedef struct {               /* counters of the last committed batch (il_stats_sync) */
+  uint64_t batch;              /* b of the last commit (1-based) */
+  uint32_t resident_blocks;    /* |prefix index| */
+  uint32_t free_pages;
+  uint32_t table_entries;
+  uint32_t evicted_blocks;     /* evicted by the last il_prefix_match */
+  uint32_t need_pages;         /* pages the last il_prefix_match allocated */
+  uint32_t suffix_tokens;      /* sum of suffix lengths of the last il_prefix_match */
+  uint32_t index_rebuilds;     /* tombstone compactions so far */
+  uint32_t status;             /* latched il_status */
+} il_stats;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+il_status il_workspace_bytes(const il_config* cfg_h, size_t* bytes_h);
+il_status il_create(const il_config* cfg_h, void* workspace, size_t bytes, il_stream s, il_ctx** out_h);
+il_status il_destroy(il_ctx* ctx);
+il_status il_status_sync(il_ctx* ctx, il_stream s);      /* sync s, return + clear latched status */
+il_status il_stats_sync(il_ctx* ctx, il_stream s, il_stats* out_h);
+const char* il_last_error(void);                          /* thread-local */
+
+/* ---- il_pool_load: the candidate set ("samples 200 logs ... to construct the
+ * candidate set").  CSR device arrays of n_demos demos: log tokens, template tokens,
+ * interned template ids, dataset row (for IL_F_EXCLUDE_SELF), and the common
+ * instruction.  Builds the per-demo token sets (a1) and rendered demos (a5), and
+ * resets the ICL Table and the prefix index (demo ids change meaning).  The input buffers
+ * may be freed once the stream reaches this call. */
+il_status il_pool_load(il_ctx* ctx, uint32_t n_demos,
+                       const uint32_t* log_off, const uint32_t* log_tok,
+                       const uint32_t* tpl_off, const uint32_t* tpl_tok,
+                       const uint32_t* template_id, const uint32_t* src_index,
+                       const uint32_t* instr_tok, uint32_t n_instr, il_stream s);
+
+/* ---- il_refine_batch: for each of B query logs (CSR q_off[B+1] / q_tok), in admission
+ * order i = 0..B-1:
+ *   topk[i][0..k)      the k most similar demos (exact cosine over token counts or Jaccard
+ *                      over token sets), emitted ascending by similarity, ties by demo index
+ *                      (Z4-Z8)
+ *   final_ds[i][0..k)  after PAIR against the table snapshot: rule 1 uses the
+ *                      target verbatim, rule 2 keeps DS_current, rule 3 modifies + reorders
+ *   info[i]            see il_refine_info
+ *   prompt_tok[i][..]  instruction ++ render(d_1..d_k) ++ query, render(m) = log ++ [TPL] ++
+ *                      template ++ [SEP] (Z9); row stride = cfg.max_prompt_tokens
+ *   prompt_len[i]
+ * q_src[i] is the query's dataset row (only read with IL_F_EXCLUDE_SELF; may be NULL). */
+il_status il_refine_batch(il_ctx* ctx, uint32_t B,
+                          const uint32_t* q_off, const uint32_t* q_tok, const uint32_t* q_src,
+                          uint32_t* topk, uint32_t* final_ds, il_refine_info* info,
+                          uint32_t* prompt_tok, uint32_t* prompt_len, il_stream s);
+
+/* ---- il_prefix_match: for each prompt (row stride cfg.max_prompt_tokens):
+ *   block_hash[i][j]   chain hash of full block j (Z17), j < floor(L_i/16); row stride = max_blocks
+ *   hit_blocks[i]      leading blocks resident (and verified) in the index snapshot, capped at
+ *                      floor((L_i-1)/16) so the last token is always computed (Z19, Z20)
+ *   block_table[i][j]  page of block j: hit pages, then freshly allocated pages; row stride =
+ *                      max_blocks = ceil(cfg.max_prompt_tokens / 16)
+ *   prefix_len[i]      16 * hit_blocks[i];  cu_q[B+1] cumulative suffix lengths
+ * Hit pages are pinned; if the batch needs more pages than are free, the least recently used
+ * unpinned blocks are evicted in (stamp asc, depth desc) order (Z21).  prompt_tok,
+ * prompt_len, block_hash, hit_blocks and block_table must stay valid until il_commit. */
+il_status il_prefix_match(il_ctx* ctx, uint32_t B,
+                          const uint32_t* prompt_tok, const uint32_t* prompt_len,
+                          uint64_t* block_hash, uint32_t* hit_blocks,
+                          int32_t* block_table, int32_t* prefix_len, int32_t* cu_q, il_stream s);
+
+/* ---- il_prefill_attn: rows r in [cu_q[i], cu_q[i+1]) are the suffix tokens of request i at
+ * absolute positions p = prefix_len[i] + (r - cu_q[i]).  First writes k_new/v_new rows into
+ * the request's pages, then for every q-head h:
+ *   out[r][h] = sum_{j <= p} softmax_j(q[r][h] . K_j * scale) V_j,  kv-head = h / (Hq/Hkv)
+ * with K_j, V_j read from the pages (cached prefix and the just-written suffix alike).
+ *   q, out        [max_suffix_tokens][Hq][d]  bf16;  lse [..][Hq] f32 natural log, or NULL
+ *   k_new, v_new  [max_suffix_tokens][Hkv][d] bf16
+ *   k_pages, v_pages  [C][Hkv][16][d] bf16, caller-owned, persistent across batches
+ * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27). */
+il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
+                          const int32_t* block_table,
+                          const il_bf16* q, const il_bf16* k_new, const il_bf16* v_new,
+                          il_bf16* k_pages, il_bf16* v_pages, il_bf16* out, float* lse,
+                          float softmax_scale, il_stream s);
+
+/* ---- il_commit: end of batch ("update the elements in the ICL Table after processing
+ * the request").  Inserts the batch's new full blocks into the prefix index (first request in
+ * admission order owns the page; duplicates and partial-block pages are freed, Z22-Z23) and
+ * applies the ICL Table records in admission order (rule 1 refreshes the target; rules 2/3
+ * upsert the final DS; the target of rule 3 keeps its position), then keeps the T most recent
+ * entries (Z2, Z3, Z14). */
+il_status il_commit(il_ctx* ctx, il_stream s);
+
+/* ---- bench / test helper (not part of the method): deterministic bf16 Q, K, V for the
+ * suffix rows from (seed, token, absolute position, head, dim) — the counter-based
+ * generator of DESIGN.md Z28, so cached pages equal recomputation.  q_scale scales Q. */
+il_status il_synth_qkv(il_ctx* ctx, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
+                       const int32_t* prefix_len, uint64_t seed, float q_scale,
+                       il_bf16* q, il_bf16* k_new, il_bf16* v_new, il_stream s);
+
+/* ---- debug / parity helpers: copy the resident index (hash, stamp, depth, parent hash;
+ * unordered) and the ICL Table (ds [T][k], stamp [T]; empty slots have stamp 0) to host. */
+il_status il_index_dump(il_ctx* ctx, il_stream s, uint64_t* hash_h, uint64_t* stamp_h,
+                        uint32_t* depth_h, uint64_t* parent_h, uint32_t* n_h);
+il_status il_table_dump(il_ctx* ctx, il_stream s, uint32_t* ds_h, uint64_t* stamp_h);
+/* evicted block hashes of the last il_prefix_match (unordered) */
+il_status il_evicted_dump(il_ctx* ctx, il_stream s, uint64_t* hash_h, uint32_t* n_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

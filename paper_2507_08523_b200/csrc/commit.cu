@@ -1,0 +1,371 @@
+// commit.cu — il_commit (K8): prefix-index insert in admission order (first request owns the
+// page, duplicates and partial pages are freed; Z22, Z23) + tombstone compaction, and the
+// ICL-Table commit (keyed upsert in admission order, keep the T most recent; Z2, Z3, Z14).
+#include <cooperative_groups.h>
+
+#include "il_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace il {
+
+constexpr uint32_t OCC_FREE = 0xFFFFFFFEu;   // the request's page is a duplicate: free it
+constexpr uint32_t OCC_CAND = 0xFFFFFFFDu;   // not resident: insert candidate
+
+__device__ __forceinline__ void push_free(const Ctx& c, uint32_t page) {
+  const uint32_t f = atomicAdd(&c.sc->n_free, 1u);
+  c.free_list[f] = page;
+}
+
+// Phase A: blocks j in [h_i, F_i) that are resident now (only the Z20-capped block can be)
+// get their stamp refreshed and the request's page freed; the rest become insert candidates.
+__global__ void __launch_bounds__(256) k_commit_probe(Ctx c, uint32_t B, uint64_t b_cur) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t L = c.prompt_len[i], h = c.hit[i], F = L / BS;
+  const uint64_t st = stamp_of(b_cur, i);
+  for (uint32_t j = h + lane; j < F; j += 32) {
+    const uint64_t H = c.block_hash[(size_t)i * c.max_blocks + j];
+    const uint32_t page = index_find(c.slot_key, c.slot_page, c.slot_mask, H, nullptr);
+    if (page != NONE32) {
+      atomicMax((unsigned long long*)&c.pg_stamp[page], (unsigned long long)st);
+      c.occ[(size_t)i * c.max_blocks + j] = OCC_FREE;
+    } else {
+      c.occ[(size_t)i * c.max_blocks + j] = OCC_CAND;
+    }
+  }
+}
+
+// Phase B: lock-free insert-or-find of every candidate key (CAS into EMPTY slots, linear
+// probing past tombstones), then claim = min admission index, cstamp = max stamp over the
+// requests presenting the key (order-independent, hence deterministic).
+__global__ void __launch_bounds__(256) k_commit_insert(Ctx c, uint32_t B, uint64_t b_cur) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t L = c.prompt_len[i], h = c.hit[i], F = L / BS;
+  const uint64_t st = stamp_of(b_cur, i);
+  uint32_t inserted = 0;
+  for (uint32_t j = h + lane; j < F; j += 32) {
+    uint32_t* occ = c.occ + (size_t)i * c.max_blocks + j;
+    if (*occ != OCC_CAND) continue;
+    const uint64_t H = c.block_hash[(size_t)i * c.max_blocks + j];
+    uint32_t s = (uint32_t)(H ^ (H >> 32)) & c.slot_mask;
+    while (true) {
+      const uint64_t k = c.slot_key[s];
+      if (k == H) break;
+      if (k == KEY_EMPTY) {
+        const uint64_t old = atomicCAS((unsigned long long*)&c.slot_key[s], (unsigned long long)KEY_EMPTY,
+                                       (unsigned long long)H);
+        if (old == KEY_EMPTY) { ++inserted; break; }
+        if (old == H) break;
+      }
+      s = (s + 1) & c.slot_mask;
+    }
+    atomicMin(&c.claim[s], i);
+    atomicMax((unsigned long long*)&c.cstamp[s], (unsigned long long)st);
+    *occ = s;
+  }
+  for (int o = 16; o; o >>= 1) inserted += __shfl_xor_sync(~0u, inserted, o);
+  if (lane == 0 && inserted) atomicAdd(&c.sc->used_slots, inserted);
+}
+
+// Phase C: the claimant owns the block: its page becomes resident with the block's hash,
+// parent hash, tokens, depth and the max stamp.  Every other page of the batch that is not
+// resident now (duplicates, the capped block, the partial trailing block) is freed.
+__global__ void __launch_bounds__(256) k_commit_own(Ctx c, uint32_t B) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t L = c.prompt_len[i], h = c.hit[i], F = L / BS;
+  const int32_t* bt = c.block_table + (size_t)i * c.max_blocks;
+  const uint64_t* bh = c.block_hash + (size_t)i * c.max_blocks;
+  const uint32_t* row = c.prompt_tok + (size_t)i * c.cfg.max_prompt_tokens;
+  uint32_t owned = 0;
+  for (uint32_t j = h + lane; j < F; j += 32) {
+    const uint32_t o = c.occ[(size_t)i * c.max_blocks + j];
+    const uint32_t page = (uint32_t)bt[j];
+    if (o == OCC_FREE) { push_free(c, page); continue; }
+    if (c.claim[o] != i) { push_free(c, page); continue; }
+    c.slot_page[o] = page;
+    c.pg_hash[page] = bh[j];
+    c.pg_parent[page] = j ? bh[j - 1] : root_hash(c.cfg.hash_seed);
+    const uint4* src = reinterpret_cast<const uint4*>(row + (size_t)BS * j);
+    uint4* dst = reinterpret_cast<uint4*>(c.pg_tok + (size_t)page * BS);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = src[q];
+    c.pg_depth[page] = j;
+    c.pg_stamp[page] = c.cstamp[o];
+    c.pg_slot[page] = o;
+    c.pg_state[page] = 1;
+    c.claim[o] = NONE32;
+    c.cstamp[o] = 0;
+    ++owned;
+  }
+  if (lane == 0 && (L % BS)) push_free(c, (uint32_t)bt[F]);       // partial block (Z23)
+  for (int o = 16; o; o >>= 1) owned += __shfl_xor_sync(~0u, owned, o);
+  if (lane == 0 && owned) atomicAdd(&c.sc->resident, owned);
+}
+
+// Tombstone compaction: when live + tombstones exceed 3/4 of the slots, rebuild the table
+// from the resident pages (one cooperative grid).
+__global__ void __launch_bounds__(512) k_rebuild(Ctx c) {
+  cg::grid_group grid = cg::this_grid();
+  DevScalars* sc = c.sc;
+  if ((uint64_t)sc->used_slots * 4 <= (uint64_t)c.n_slots * 3) return;   // uniform
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (uint32_t s = gtid; s < c.n_slots; s += gs) { c.slot_key[s] = KEY_EMPTY; c.slot_page[s] = NONE32; }
+  grid.sync();
+  for (uint32_t p = gtid; p < c.cfg.kv_pages; p += gs) {
+    if (c.pg_state[p] != 1) continue;
+    const uint64_t H = c.pg_hash[p];
+    uint32_t s = (uint32_t)(H ^ (H >> 32)) & c.slot_mask;
+    while (atomicCAS((unsigned long long*)&c.slot_key[s], (unsigned long long)KEY_EMPTY, (unsigned long long)H) !=
+           KEY_EMPTY)
+      s = (s + 1) & c.slot_mask;
+    c.slot_page[s] = p;
+    c.pg_slot[p] = s;
+  }
+  grid.sync();
+  if (gtid == 0) { sc->used_slots = sc->resident; sc->rebuilds += 1; }
+}
+
+// ---------------------------------------------------------------------------------------
+// ICL Table commit.
+// ---------------------------------------------------------------------------------------
+// k_tab_find: one warp per request: the slot already holding final_ds (or -1) and whether
+// this request is the last of the batch presenting that key.
+__global__ void __launch_bounds__(256) k_tab_find(Ctx c, uint32_t B) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t k = c.cfg.k;
+  uint32_t key[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; ++j) key[j] = (uint32_t)j < k ? c.final_ds[(size_t)i * k + j] : 0;
+  int32_t found = -1;
+  for (uint32_t s = lane; s < c.cfg.table_capacity; s += 32) {
+    if (c.tab_stamp[s] == 0) continue;
+    bool eq = true;
+    for (uint32_t j = 0; j < k; ++j) eq &= c.tab_ds[(size_t)s * k + j] == key[j];
+    if (eq) found = (int32_t)s;
+  }
+  bool later = false;
+  for (uint32_t i2 = i + 1 + lane; i2 < B; i2 += 32) {
+    bool eq = true;
+    for (uint32_t j = 0; j < k; ++j) eq &= c.final_ds[(size_t)i2 * k + j] == key[j];
+    later |= eq;
+  }
+  for (int o = 16; o; o >>= 1) found = max(found, __shfl_xor_sync(~0u, found, o));
+  later = __any_sync(~0u, later);
+  if (lane == 0) { c.tab_find[i] = found; c.tab_last[i] = !later; }
+}
+
+// block-wide exclusive scan of one value per thread (1024 threads)
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32_t* total) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(~0u, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = s_w[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(~0u, t, o);
+      if (lane >= (uint32_t)o) t += y;
+    }
+    s_w[lane] = t;
+  }
+  __syncthreads();
+  const uint32_t before = (w ? s_w[w - 1] : 0) + x - v;
+  *total = s_w[31];
+  __syncthreads();
+  return before;
+}
+
+// k_tab_commit (one CTA of 1024 threads, T <= 8192 slots, B <= 8192 requests).
+// The recency order after the batch is: untouched old entries (stamps of earlier batches),
+// then the batch's keys ordered by their last request.  Keep the T most recent.
+__global__ void __launch_bounds__(1024) k_tab_commit(Ctx c, uint32_t B, uint64_t b_cur) {
+  extern __shared__ uint64_t s_old[];                  // old stamps, compacted [n_old]
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint64_t s_pref;
+  __shared__ uint32_t s_rem;
+  const uint32_t tid = threadIdx.x, T = c.cfg.table_capacity, k = c.cfg.k;
+  const uint32_t perB = cdiv(B, 1024), perT = cdiv(T, 1024);
+  // 1. refresh keys that exist (rule 1 targets and re-appended keys)
+  for (uint32_t i = tid; i < B; i += 1024)
+    if (c.tab_last[i] && c.tab_find[i] >= 0) c.tab_stamp[c.tab_find[i]] = stamp_of(b_cur, i);
+  __syncthreads();
+  // 2. counts: old (stamp of an earlier batch), live, new keys, last requests
+  uint32_t my_old = 0;
+  for (uint32_t s = tid * perT; s < min(T, (tid + 1) * perT); ++s) {
+    const uint64_t st = c.tab_stamp[s];
+    my_old += st != 0 && (st >> 32) < b_cur;
+  }
+  uint32_t n_old;
+  const uint32_t old_off = block_scan(my_old, s_w, &n_old);
+  {
+    uint32_t o = old_off;
+    for (uint32_t s = tid * perT; s < min(T, (tid + 1) * perT); ++s) {
+      const uint64_t st = c.tab_stamp[s];
+      if (st != 0 && (st >> 32) < b_cur) s_old[o++] = st;
+    }
+  }
+  uint32_t my_last = 0, my_new = 0;
+  for (uint32_t i = tid * perB; i < min(B, (tid + 1) * perB); ++i) {
+    my_last += c.tab_last[i];
+    my_new += c.tab_last[i] && c.tab_find[i] < 0;
+  }
+  uint32_t n_last, n_new;
+  const uint32_t last_off = block_scan(my_last, s_w, &n_last);
+  const uint32_t new_off = block_scan(my_new, s_w, &n_new);
+  const uint32_t total = n_old + n_last;                 // live entries after the batch
+  const uint32_t d = total > T ? total - T : 0;          // entries to drop
+  // 3. drop: the d smallest old stamps, or all old + the first (d - n_old) batch keys
+  uint64_t tau = 0;                                      // drop old entries with stamp <= tau
+  if (d > 0 && d <= n_old) {
+    // radix select (8-bit digits, MSB first) of the d-th smallest old stamp
+    if (tid == 0) { s_pref = 0; s_rem = d; }
+    __syncthreads();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (uint32_t x = tid; x < 256; x += 1024) s_hist[x] = 0;
+      __syncthreads();
+      const uint64_t pref = s_pref;
+      for (uint32_t x = tid; x < n_old; x += 1024) {
+        const uint64_t v = s_old[x];
+        const uint64_t hi = shift + 8 >= 64 ? 0 : v >> (shift + 8);
+        if (hi == pref) atomicAdd(&s_hist[(v >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t acc = 0, bin = 0;
+        for (bin = 0; bin < 256; ++bin) {
+          if (acc + s_hist[bin] >= s_rem) break;
+          acc += s_hist[bin];
+        }
+        s_pref = (pref << 8) | bin;
+        s_rem -= acc;
+      }
+      __syncthreads();
+    }
+    tau = s_pref;
+  } else if (d > n_old) {
+    tau = ~0ull;                                         // every old entry goes
+  }
+  const uint32_t d_batch = d > n_old ? d - n_old : 0;   // batch keys dropped (earliest last-requests)
+  if (d > 0) {
+    for (uint32_t s = tid; s < T; s += 1024) {
+      const uint64_t st = c.tab_stamp[s];
+      if (st != 0 && (st >> 32) < b_cur && st <= tau) c.tab_stamp[s] = 0;
+    }
+  }
+  __syncthreads();
+  // batch keys: request i with last[i] has rank r among last requests; it survives iff r >= d_batch
+  {
+    uint32_t r = last_off;
+    for (uint32_t i = tid * perB; i < min(B, (tid + 1) * perB); ++i) {
+      if (!c.tab_last[i]) continue;
+      if (r < d_batch && c.tab_find[i] >= 0) c.tab_stamp[c.tab_find[i]] = 0;
+      ++r;
+    }
+  }
+  __syncthreads();
+  // 4. free slots (stamp 0) in slot order receive the surviving new keys in admission order
+  uint32_t my_free = 0;
+  for (uint32_t s = tid * perT; s < min(T, (tid + 1) * perT); ++s) my_free += c.tab_stamp[s] == 0;
+  uint32_t n_free;
+  const uint32_t free_off = block_scan(my_free, s_w, &n_free);
+  // surviving new keys: new requests whose last-rank >= d_batch; their order = new rank minus
+  // the number of dropped new keys before them.  Dropped batch keys are a prefix (by i) of
+  // the last requests, so the surviving new keys are a suffix of the new requests.
+  uint32_t my_dnew = 0;
+  {
+    uint32_t r = last_off;
+    for (uint32_t i = tid * perB; i < min(B, (tid + 1) * perB); ++i) {
+      if (!c.tab_last[i]) continue;
+      if (r < d_batch && c.tab_find[i] < 0) ++my_dnew;
+      ++r;
+    }
+  }
+  uint32_t n_dnew;
+  block_scan(my_dnew, s_w, &n_dnew);
+  // map: j-th free slot (slot order) -> stored in s_old reuse as u32 list
+  uint32_t* s_free = reinterpret_cast<uint32_t*>(s_old);
+  __syncthreads();
+  {
+    uint32_t o = free_off;
+    for (uint32_t s = tid * perT; s < min(T, (tid + 1) * perT); ++s)
+      if (c.tab_stamp[s] == 0) s_free[o++] = s;
+  }
+  __syncthreads();
+  {
+    uint32_t rn = new_off, rl = last_off;
+    for (uint32_t i = tid * perB; i < min(B, (tid + 1) * perB); ++i) {
+      if (!c.tab_last[i]) continue;
+      const bool is_new = c.tab_find[i] < 0;
+      if (is_new && rl >= d_batch) {
+        const uint32_t slot_rank = rn - n_dnew;
+        if (slot_rank < n_free) {
+          const uint32_t s = s_free[slot_rank];
+          for (uint32_t j = 0; j < k; ++j) {
+            const uint32_t dd = c.final_ds[(size_t)i * k + j];
+            c.tab_ds[(size_t)s * k + j] = dd;
+            c.tab_tpl[(size_t)s * k + j] = c.tid[dd];
+          }
+          c.tab_stamp[s] = stamp_of(b_cur, i);
+        } else {
+          latch(c.sc, IL_ERR_INTERNAL);
+        }
+      }
+      rn += is_new;
+      ++rl;
+    }
+  }
+  if (tid == 0) c.sc->table_entries = min(total, T);
+}
+
+}  // namespace il
+
+using namespace il;
+
+extern "C" il_status il_commit(il_ctx* c, il_stream s) {
+  if (!c->matched) { set_error("il_commit before il_prefix_match"); return IL_ERR_STATE; }
+  const bool pair = (c->cfg.flags & IL_F_PAIR) != 0;
+  if (pair && !c->refined) { set_error("il_commit before il_refine_batch"); return IL_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)s;
+  const uint32_t B = c->last_B;
+  const uint64_t b_cur = c->batch + 1;
+  if (B) {
+    const uint32_t g = cdiv(B * 32, 256);
+    k_commit_probe<<<g, 256, 0, st>>>(*c, B, b_cur);
+    k_commit_insert<<<g, 256, 0, st>>>(*c, B, b_cur);
+    k_commit_own<<<g, 256, 0, st>>>(*c, B);
+  }
+  {
+    static int rb_blocks = -1;
+    if (rb_blocks < 0) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0);
+      rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+    }
+    Ctx cc = *c;
+    void* args[] = {&cc};
+    IL_CUDA(cudaLaunchCooperativeKernel((void*)k_rebuild, dim3(rb_blocks), dim3(512), args, 0, st));
+  }
+  if (pair && B) {
+    k_tab_find<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B);
+    const size_t smem = (size_t)c->cfg.table_capacity * 8;
+    static bool attr = false;
+    if (!attr) {
+      IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+      attr = true;
+    }
+    k_tab_commit<<<1, 1024, smem, st>>>(*c, B, b_cur);
+  }
+  IL_LAUNCH_CHECK("il_commit");
+  c->batch = b_cur;
+  c->refined = c->matched = false;
+  return IL_OK;
+}

@@ -1,0 +1,166 @@
+// il_internal.cuh — context layout and device helpers shared by the CUDA translation
+// units of libinferlog_b200.so.  Nothing here is shared with the CPU checker.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/il.h"
+
+namespace il {
+
+constexpr uint32_t BS = 16;                 // KV block size (tokens)
+constexpr uint32_t TOK_SEP = 1, TOK_TPL = 2;
+constexpr uint64_t KEY_EMPTY = 0ull;
+constexpr uint64_t KEY_TOMB = ~0ull;
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+constexpr int MAXK = 8;
+
+// Device-resident scalars (one 256 B line).
+struct DevScalars {
+  uint32_t status;           // latched il_status
+  uint32_t n_free;           // free-page stack size
+  uint32_t resident;         // live index entries (== resident pages)
+  uint32_t used_slots;       // live + tombstones
+  uint32_t pinned;           // distinct pages pinned in the current batch
+  uint32_t need_total;       // pages the current batch allocates
+  uint32_t evict_m;          // blocks to evict
+  uint32_t evicted;          // evicted by the current batch
+  uint32_t suffix_total;     // sum of suffix lengths
+  uint32_t rebuilds;
+  uint32_t table_entries;
+  uint32_t n_new_keys;       // ICL commit scratch
+  uint32_t rebuild_flag;
+  uint32_t n_tiles;          // attention work items
+  uint32_t pad0[2];
+  uint64_t stamp_min;        // eviction radix-select scratch
+  uint64_t stamp_max;
+  uint64_t sel_prefix;       // selected key prefix
+  uint64_t sel_key;          // final threshold key
+  uint32_t sel_remaining;
+  uint32_t sel_shift;
+  uint32_t cand;             // eviction candidates
+  uint32_t pad1[17];
+};
+
+struct Ctx {
+  il_config cfg;
+  uint32_t max_blocks = 0, n_slots = 0, slot_mask = 0;
+  uint32_t n_demos = 0, n_instr = 0;
+  bool pool_loaded = false, refined = false, matched = false;
+  uint32_t last_B = 0;
+  uint64_t batch = 0;        // b of the last committed batch
+  // workspace carve
+  DevScalars* sc = nullptr;
+  // pool
+  uint32_t *log_off, *log_tok, *tpl_off, *tpl_tok, *tid, *src;
+  uint32_t *uniq_tok, *uniq_cnt, *uniq_n, *norm2;
+  uint32_t *rend_off, *rend_tok, *rend_len;
+  uint32_t *instr;
+  // ICL table
+  uint32_t *tab_ds, *tab_tpl;
+  uint64_t* tab_stamp;
+  // prefix index + pages
+  uint64_t* slot_key;
+  uint32_t* slot_page;
+  uint32_t* claim;
+  uint64_t* cstamp;
+  uint64_t *pg_hash, *pg_parent, *pg_stamp;
+  uint32_t *pg_tok, *pg_depth, *pg_slot, *pg_state, *pg_pin;
+  uint32_t* free_list;
+  // batch scratch
+  uint32_t *need_off, *occ, *hist;
+  int32_t *tab_find;         // per request: existing table slot of final_ds or -1
+  uint32_t *tab_last;        // per request: last in batch with this key
+  uint32_t *tile_off;        // attention work decomposition
+  uint64_t *evicted_list;
+  uint32_t *guard_prompt;    // guard: DS_current prompt rows
+  // pointers remembered between calls (caller-owned)
+  const uint32_t* final_ds = nullptr;
+  const il_refine_info* info = nullptr;
+  const uint32_t* prompt_tok = nullptr;
+  const uint32_t* prompt_len = nullptr;
+  const uint64_t* block_hash = nullptr;
+  const uint32_t* hit = nullptr;
+  const int32_t* block_table = nullptr;
+  int num_sms = 148;
+};
+
+// ---------------------------------------------------------------- error plumbing (host)
+void set_error(const std::string& msg);
+il_status cuda_check(cudaError_t e, const char* what);
+#define IL_CUDA(call)                                                  \
+  do {                                                                 \
+    cudaError_t _e = (call);                                           \
+    if (_e != cudaSuccess) return ::il::cuda_check(_e, #call);         \
+  } while (0)
+#define IL_LAUNCH_CHECK(what)                                          \
+  do {                                                                 \
+    cudaError_t _e = cudaGetLastError();                               \
+    if (_e != cudaSuccess) return ::il::cuda_check(_e, what);          \
+  } while (0)
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ void latch(DevScalars* sc, uint32_t code) {
+  atomicCAS(&sc->status, 0u, code);
+}
+
+// Chain hash (Z17): splitmix64 finalizer; 16 independent lane terms per block,
+// summed mod 2^64, then a serial fold H_j = mix(H_{j-1} * PHI + content_j).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+constexpr uint64_t PHI64 = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ uint64_t root_hash(uint64_t seed) {
+  return mix64(seed ^ 0x494E4645524C4F47ull);
+}
+__device__ __forceinline__ uint64_t lane_term(uint32_t tok, uint32_t i) {
+  return mix64(((uint64_t)tok << 8) ^ (uint64_t)i ^ PHI64);
+}
+__device__ __forceinline__ uint64_t chain_step(uint64_t prev, uint64_t content) {
+  uint64_t h = mix64(prev * PHI64 + content);
+  h = (h == KEY_EMPTY) ? 1ull : h;
+  h = (h == KEY_TOMB) ? (KEY_TOMB - 1ull) : h;
+  return h;
+}
+// content hash of the 16 tokens at t (16-byte aligned)
+__device__ __forceinline__ uint64_t block_content(const uint32_t* __restrict__ t, uint32_t tok[16]) {
+  const uint4* v = reinterpret_cast<const uint4*>(t);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 x = __ldg(v + q);
+    tok[4 * q + 0] = x.x; tok[4 * q + 1] = x.y; tok[4 * q + 2] = x.z; tok[4 * q + 3] = x.w;
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (uint32_t i = 0; i < 16; ++i) s += lane_term(tok[i], i);
+  return mix64(s);
+}
+
+__device__ __forceinline__ uint64_t stamp_of(uint64_t b, uint32_t i) { return (b << 32) | (uint64_t)i; }
+
+// open-addressing probe of the prefix index: returns page or NONE32
+__device__ __forceinline__ uint32_t index_find(const uint64_t* __restrict__ slot_key,
+                                               const uint32_t* __restrict__ slot_page,
+                                               uint32_t mask, uint64_t key, uint32_t* slot_out) {
+  uint32_t s = (uint32_t)(key ^ (key >> 32)) & mask;
+  for (uint32_t n = 0; n <= mask; ++n) {
+    uint64_t k = slot_key[s];
+    if (k == key) { if (slot_out) *slot_out = s; return slot_page[s]; }
+    if (k == KEY_EMPTY) return NONE32;
+    s = (s + 1) & mask;
+  }
+  return NONE32;
+}
+
+__host__ __device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+}  // namespace il
+
+struct il_ctx : public il::Ctx {};

@@ -1,0 +1,245 @@
+// match.cu — il_prefix_match: K5 chained block hash + longest cached prefix + touch/pin,
+// K6 page accounting, LRU eviction (grid-wide radix select) and block-table build.
+#include <cooperative_groups.h>
+
+#include "il_internal.cuh"
+#include "match_dev.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace il {
+
+// K5: one warp per request.  Hashes every full block (block_hash row), finds the capped
+// leading run of resident + verified blocks in the snapshot index, writes the hit pages to
+// the block table, and touches + pins them: stamp <- max(stamp, (b, i)) (Z21).
+__global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
+                                                    const uint32_t* __restrict__ prompt_len,
+                                                    uint64_t* __restrict__ block_hash, uint32_t* __restrict__ hit,
+                                                    int32_t* __restrict__ block_table, uint64_t b_cur) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t L = prompt_len[i];
+  const uint32_t* row = prompt_tok + (size_t)i * c.cfg.max_prompt_tokens;
+  int32_t* bt = block_table + (size_t)i * c.max_blocks;
+  const uint32_t h = warp_hash_match(c, row, L, block_hash + (size_t)i * c.max_blocks, bt, false);
+  __syncwarp();
+  const uint64_t st = stamp_of(b_cur, i);
+  const uint32_t epoch = (uint32_t)b_cur;
+  uint32_t newly = 0;
+  for (uint32_t j = lane; j < h; j += 32) {
+    const uint32_t p = (uint32_t)bt[j];
+    atomicMax((unsigned long long*)&c.pg_stamp[p], (unsigned long long)st);
+    newly += atomicExch(&c.pg_pin[p], epoch) != epoch;
+  }
+  for (int o = 16; o; o >>= 1) newly += __shfl_xor_sync(~0u, newly, o);
+  if (lane == 0) {
+    hit[i] = h;
+    if (newly) atomicAdd(&c.sc->pinned, newly);
+  }
+}
+
+// K6a (one CTA): per-request pages needed (ceil(L/16) - h), suffix lengths, exclusive scans
+// -> need_off, cu_q, prefix_len; how many blocks must be evicted.
+__global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
+                                                     const uint32_t* __restrict__ hit,
+                                                     int32_t* __restrict__ prefix_len, int32_t* __restrict__ cu_q) {
+  __shared__ uint32_t s_need[1024], s_suf[1024];
+  const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
+  uint32_t n = 0, sfx = 0;
+  for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
+    const uint32_t L = prompt_len[i], h = hit[i];
+    n += cdiv(L, BS) - h;
+    sfx += L - BS * h;
+  }
+  s_need[tid] = n; s_suf[tid] = sfx;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {          // Hillis-Steele inclusive scan
+    uint32_t a = tid >= o ? s_need[tid - o] : 0, b = tid >= o ? s_suf[tid - o] : 0;
+    __syncthreads();
+    s_need[tid] += a; s_suf[tid] += b;
+    __syncthreads();
+  }
+  uint32_t an = tid ? s_need[tid - 1] : 0, as = tid ? s_suf[tid - 1] : 0;
+  for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
+    const uint32_t L = prompt_len[i], h = hit[i];
+    c.need_off[i] = an; cu_q[i] = (int32_t)as; prefix_len[i] = (int32_t)(BS * h);
+    an += cdiv(L, BS) - h;
+    as += L - BS * h;
+  }
+  if (tid == 1023) {
+    const uint32_t need = s_need[1023], suf = s_suf[1023];
+    c.need_off[B] = need; cu_q[B] = (int32_t)suf;
+    DevScalars* sc = c.sc;
+    sc->need_total = need;
+    sc->suffix_total = suf;
+    sc->evicted = 0;
+    uint32_t m = need > sc->n_free ? need - sc->n_free : 0;
+    const uint32_t cand = sc->resident - sc->pinned;
+    if (m > cand) { latch(sc, IL_ERR_CAPACITY); m = 0; sc->need_total = 0; }
+    if (suf > c.cfg.max_suffix_tokens) latch(sc, IL_ERR_CAPACITY);
+    sc->evict_m = m;
+    sc->cand = cand;
+    sc->stamp_min = ~0ull;
+  }
+}
+
+// K6b: LRU eviction as one cooperative grid.  Candidates are resident, unpinned pages.
+// Order (Z21): stamp ascending, depth descending (hash ascending never decides: one stamp
+// (b, i) belongs to one request's chain, whose depths are distinct).  The key
+//   key = (b - b_min) << 25 | i << 12 | (4095 - depth)
+// is unique per candidate; an 11-bit-digit radix select over the grid finds the m-th
+// smallest key, then every candidate with key <= it is evicted: its slot becomes a
+// tombstone and its page returns to the free stack.
+constexpr int EV_THREADS = 512;
+constexpr uint32_t EV_BINS = 2048;
+
+__device__ __forceinline__ bool ev_cand(const Ctx& c, uint32_t p, uint32_t epoch) {
+  return c.pg_state[p] == 1 && c.pg_pin[p] != epoch;
+}
+__device__ __forceinline__ uint64_t ev_key(const Ctx& c, uint32_t p, uint64_t b_min) {
+  const uint64_t st = c.pg_stamp[p];
+  return (((st >> 32) - b_min) << 25) | ((st & 0x1FFFull) << 12) | (uint64_t)(4095u - min(c.pg_depth[p], 4095u));
+}
+
+__global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t b_cur) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t s_hist[EV_BINS];
+  __shared__ uint64_t s_red;
+  DevScalars* sc = c.sc;
+  const uint32_t m = sc->evict_m;
+  const uint32_t epoch = (uint32_t)b_cur, C = c.cfg.kv_pages;
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  if (m == 0) return;                                   // uniform across the grid
+  // pass 0: b_min over candidates
+  if (threadIdx.x == 0) s_red = ~0ull;
+  __syncthreads();
+  uint64_t bmin = ~0ull;
+  for (uint32_t p = gtid; p < C; p += gstride)
+    if (ev_cand(c, p, epoch)) bmin = min(bmin, c.pg_stamp[p] >> 32);
+  for (int o = 16; o; o >>= 1) bmin = min(bmin, __shfl_xor_sync(~0u, bmin, o));
+  if ((threadIdx.x & 31) == 0) atomicMin((unsigned long long*)&s_red, (unsigned long long)bmin);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMin((unsigned long long*)&sc->stamp_min, (unsigned long long)s_red);
+  grid.sync();
+  const uint64_t b_min = sc->stamp_min;
+  const uint64_t kmax = ((b_cur - b_min) << 25) | ((1ull << 25) - 1);
+  int top_bit = 63 - __clzll((long long)kmax);
+  int shift = (top_bit / 11) * 11;                      // lowest bit of the top digit
+  uint64_t prefix = 0;                                  // key bits above `shift` selected so far
+  uint32_t remaining = m;
+  for (int pass = 0; shift >= 0; ++pass, shift -= 11) {
+    uint32_t* ghist = c.hist + (pass & 1) * EV_BINS;
+    for (uint32_t x = threadIdx.x; x < EV_BINS; x += blockDim.x) s_hist[x] = 0;
+    __syncthreads();
+    for (uint32_t p = gtid; p < C; p += gstride) {
+      if (!ev_cand(c, p, epoch)) continue;
+      const uint64_t key = ev_key(c, p, b_min);
+      const uint64_t hi = (shift + 11 >= 64) ? 0 : (key >> (shift + 11));
+      if (hi != prefix) continue;
+      atomicAdd(&s_hist[(key >> shift) & (EV_BINS - 1)], 1u);
+    }
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < EV_BINS; x += blockDim.x)
+      if (s_hist[x]) atomicAdd(&ghist[x], s_hist[x]);
+    grid.sync();
+    // every CTA scans the global histogram identically (2048 bins, cheap)
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0, bin = 0;
+      for (bin = 0; bin < EV_BINS; ++bin) {
+        const uint32_t h = ghist[bin];
+        if (acc + h >= remaining) break;
+        acc += h;
+      }
+      s_red = ((uint64_t)bin << 32) | (remaining - acc);
+    }
+    __syncthreads();
+    const uint32_t bin = (uint32_t)(s_red >> 32);
+    remaining = (uint32_t)(s_red & 0xFFFFFFFFu);
+    prefix = (prefix << 11) | bin;
+    // clear the other histogram buffer for the next pass (CTA 0), ordered by the next sync
+    if (blockIdx.x == 0)
+      for (uint32_t x = threadIdx.x; x < EV_BINS; x += blockDim.x) c.hist[((pass + 1) & 1) * EV_BINS + x] = 0;
+    grid.sync();
+  }
+  // prefix is now the exact m-th smallest key; evict every candidate with key <= prefix
+  const uint64_t kstar = prefix;
+  uint32_t ev = 0;
+  for (uint32_t p = gtid; p < C; p += gstride) {
+    if (!ev_cand(c, p, epoch)) continue;
+    if (ev_key(c, p, b_min) > kstar) continue;
+    c.pg_state[p] = 0;
+    const uint32_t s = c.pg_slot[p];
+    c.slot_key[s] = KEY_TOMB;
+    c.slot_page[s] = NONE32;
+    c.pg_slot[p] = NONE32;
+    const uint32_t f = atomicAdd(&sc->n_free, 1u);
+    c.free_list[f] = p;
+    const uint32_t e = atomicAdd(&sc->evicted, 1u);
+    c.evicted_list[e] = c.pg_hash[p];
+    ++ev;
+  }
+  for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(~0u, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicSub(&sc->resident, ev);
+  grid.sync();
+  if (gtid == 0) {
+    c.hist[0] = 0;                                      // leave both buffers clean
+    for (uint32_t x = 0; x < 2 * EV_BINS; ++x) c.hist[x] = 0;
+    if (sc->evicted != m) latch(sc, IL_ERR_INTERNAL);
+  }
+}
+
+// K6c: pop the batch's pages (free stack top) into the block table after the hit pages.
+__global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
+                                                    const uint32_t* __restrict__ hit, int32_t* __restrict__ block_table) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  DevScalars* sc = c.sc;
+  if (sc->status == IL_ERR_CAPACITY) return;
+  const uint32_t base = sc->n_free - sc->need_total + c.need_off[i];
+  const uint32_t h = hit[i], nb = cdiv(prompt_len[i], BS);
+  int32_t* bt = block_table + (size_t)i * c.max_blocks;
+  for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
+}
+__global__ void k_alloc_commit(Ctx c) {
+  DevScalars* sc = c.sc;
+  if (sc->status != IL_ERR_CAPACITY) sc->n_free -= sc->need_total;
+}
+
+}  // namespace il
+
+using namespace il;
+
+extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const uint32_t* prompt_len,
+                                     uint64_t* block_hash, uint32_t* hit, int32_t* block_table,
+                                     int32_t* prefix_len, int32_t* cu_q, il_stream s) {
+  if (!c->pool_loaded) { set_error("il_prefix_match before il_pool_load"); return IL_ERR_STATE; }
+  if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)s;
+  const uint64_t b_cur = c->batch + 1;
+  IL_CUDA(cudaMemsetAsync(&c->sc->pinned, 0, 4, st));
+  if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
+  k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q);
+  {
+    static int ev_blocks = -1;
+    if (ev_blocks < 0) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_evict, EV_THREADS, 0);
+      ev_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+    }
+    Ctx cc = *c;
+    uint64_t bc = b_cur;
+    void* args[] = {&cc, &bc};
+    IL_CUDA(cudaLaunchCooperativeKernel((void*)k_evict, dim3(ev_blocks), dim3(EV_THREADS), args, 0, st));
+  }
+  if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
+  k_alloc_commit<<<1, 1, 0, st>>>(*c);
+  IL_LAUNCH_CHECK("il_prefix_match");
+  c->prompt_tok = prompt_tok;
+  c->prompt_len = prompt_len;
+  c->block_hash = block_hash;
+  c->hit = hit;
+  c->block_table = block_table;
+  c->matched = true;
+  c->last_B = B;
+  return IL_OK;
+}

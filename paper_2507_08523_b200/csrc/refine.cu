@@ -1,0 +1,335 @@
+// refine.cu — il_refine_batch: K1 exact similarity + top-k, K2/K3 PAIR (PMC, modify,
+// reorder, rules, guard) + prompt render.
+#include "il_internal.cuh"
+#include "match_dev.cuh"
+
+namespace il {
+
+// ---------------------------------------------------------------------------------------
+// K1  Similarity + top-k (Z4-Z8).
+// One CTA per query.  The query's token multiset goes into a shared-memory hash table;
+// every thread scores a strided subset of the pool by streaming each demo's sorted unique
+// tokens (+ counts) and probing the table, keeping a private top-k.  Scores are exact
+// fractions compared by cross-multiplication:
+//   cosine : cos^2 * |q|^2 = dot^2 / |m|^2  (|q|^2 is common to one query)
+//   jaccard: |A n B| / |A u B|
+// Selection is by (score desc, index asc); the k winners are emitted (score asc, index asc).
+// ---------------------------------------------------------------------------------------
+constexpr int SIM_THREADS = 256;
+constexpr int QHASH = 512;
+
+struct Cand {
+  uint64_t num, den;
+  uint32_t idx;
+};
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {   // a ranks before b
+  const uint64_t l = a.num * b.den, r = b.num * a.den;                   // < 2^48: exact in u64
+  return l > r || (l == r && a.idx < b.idx);
+}
+__device__ __forceinline__ uint32_t qslot(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 9); }
+
+__global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
+                                                          const uint32_t* __restrict__ q_tok,
+                                                          const uint32_t* __restrict__ q_src,
+                                                          uint32_t* __restrict__ topk) {
+  __shared__ uint32_t s_key[QHASH], s_cnt[QHASH];
+  __shared__ Cand s_best[SIM_THREADS / 32];
+  __shared__ uint32_t s_nq, s_nuq, s_win;
+  __shared__ Cand s_sel[MAXK];
+  __shared__ uint32_t s_btid[SIM_THREADS / 32];
+  const uint32_t i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t k = c.cfg.k;
+  for (uint32_t x = tid; x < QHASH; x += SIM_THREADS) { s_key[x] = NONE32; s_cnt[x] = 0; }
+  if (tid == 0) { s_nq = 0; s_nuq = 0; }
+  __syncthreads();
+  const uint32_t qa = q_off[i], qL = q_off[i + 1] - qa;
+  if (qL > c.cfg.max_log_tokens) {
+    if (tid == 0) latch(c.sc, IL_ERR_ARG);
+    return;
+  }
+  for (uint32_t x = tid; x < qL; x += SIM_THREADS) {
+    const uint32_t t = q_tok[qa + x];
+    uint32_t s = qslot(t);
+    while (true) {
+      const uint32_t old = atomicCAS(&s_key[s], NONE32, t);
+      if (old == NONE32 || old == t) break;
+      s = (s + 1) & (QHASH - 1);
+    }
+    atomicAdd(&s_cnt[s], 1u);
+  }
+  __syncthreads();
+  {
+    uint32_t nq = 0, nuq = 0;
+    for (uint32_t x = tid; x < QHASH; x += SIM_THREADS)
+      if (s_key[x] != NONE32) { nq += s_cnt[x] * s_cnt[x]; nuq += 1; }
+    for (int o = 16; o; o >>= 1) { nq += __shfl_xor_sync(~0u, nq, o); nuq += __shfl_xor_sync(~0u, nuq, o); }
+    if (lane == 0) { atomicAdd(&s_nq, nq); atomicAdd(&s_nuq, nuq); }
+  }
+  __syncthreads();
+  const uint32_t nq = s_nq, nuq = s_nuq;
+  const bool jac = c.cfg.metric == IL_SIM_JACCARD;
+  const bool excl = (c.cfg.flags & IL_F_EXCLUDE_SELF) != 0;
+  const uint32_t my_src = (excl && q_src) ? q_src[i] : NONE32;
+
+  Cand top[MAXK];
+  uint32_t ntop = 0;
+  for (uint32_t m = tid; m < c.n_demos; m += SIM_THREADS) {
+    if (excl && c.src[m] == my_src) continue;
+    const uint32_t a = c.log_off[m], nu = c.uniq_n[m];
+    uint32_t dot = 0, inter = 0;
+    for (uint32_t u = 0; u < nu; ++u) {
+      const uint32_t t = c.uniq_tok[a + u];
+      uint32_t s = qslot(t), cq = 0;
+      while (true) {
+        const uint32_t key = s_key[s];
+        if (key == t) { cq = s_cnt[s]; break; }
+        if (key == NONE32) break;
+        s = (s + 1) & (QHASH - 1);
+      }
+      dot += cq * c.uniq_cnt[a + u];
+      inter += cq != 0;
+    }
+    Cand x;
+    x.idx = m;
+    if (jac) {
+      if (nuq == 0 && nu == 0) { x.num = 1; x.den = 1; }
+      else { x.num = inter; x.den = nuq + nu - inter; }
+    } else {
+      const uint32_t nm = c.norm2[m];
+      if (nq == 0 || nm == 0) { x.num = 0; x.den = 1; }                   // zero norm (Z5)
+      else { x.num = (uint64_t)dot * dot; x.den = nm; }
+    }
+    // insert into the private sorted list (k <= 8; m increases, so equal scores go after)
+    bool ins = ntop < k;
+    if (!ins) {
+#pragma unroll
+      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == k - 1) ins = better(x, top[q]);
+    }
+    if (ins) {
+      uint32_t pos = ntop < k ? ntop : k - 1;
+#pragma unroll
+      for (int q = MAXK - 1; q > 0; --q) {
+        if ((uint32_t)q <= pos && better(x, top[q - 1])) { top[q] = top[q - 1]; pos = q - 1; }
+      }
+#pragma unroll
+      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == pos) top[q] = x;
+      if (ntop < k) ++ntop;
+    }
+  }
+  // block merge: k rounds of argmax over every thread's current head
+  uint32_t head = 0;
+  for (uint32_t r = 0; r < k; ++r) {
+    Cand h;
+    bool have = head < ntop;
+    if (have) {
+#pragma unroll
+      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == head) h = top[q];
+    } else {
+      h.num = 0; h.den = 1; h.idx = NONE32;
+    }
+    // warp argmax (NONE32 idx = absent)
+    Cand w = h;
+    uint32_t wtid = have ? tid : NONE32;
+    for (int o = 16; o; o >>= 1) {
+      Cand o_;
+      o_.num = __shfl_xor_sync(~0u, w.num, o); o_.den = __shfl_xor_sync(~0u, w.den, o);
+      o_.idx = __shfl_xor_sync(~0u, w.idx, o);
+      const uint32_t ot = __shfl_xor_sync(~0u, wtid, o);
+      const bool take = (ot != NONE32) && (wtid == NONE32 || better(o_, w));
+      if (take) { w = o_; wtid = ot; }
+    }
+    if (lane == 0) { s_best[wid] = w; s_btid[wid] = wtid; }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t bt = NONE32;
+      Cand b;
+      for (uint32_t q = 0; q < SIM_THREADS / 32; ++q) {
+        if (s_btid[q] == NONE32) continue;
+        if (bt == NONE32 || better(s_best[q], b)) { b = s_best[q]; bt = s_btid[q]; }
+      }
+      s_win = bt;
+      if (bt != NONE32) s_sel[r] = b;
+      else latch(c.sc, IL_ERR_ARG);                       // fewer than k candidates
+    }
+    __syncthreads();
+    if (s_win == tid) ++head;
+    if (s_win == NONE32) return;
+  }
+  if (tid == 0) {
+    // emit ascending by similarity, ties by index ascending
+    Cand e[MAXK];
+    for (uint32_t r = 0; r < k; ++r) e[r] = s_sel[r];
+    for (uint32_t a = 1; a < k; ++a)
+      for (uint32_t b = a; b > 0; --b) {
+        const uint64_t l = e[b].num * e[b - 1].den, rr = e[b - 1].num * e[b].den;
+        const bool lt = l < rr || (l == rr && e[b].idx < e[b - 1].idx);
+        if (lt) { Cand t = e[b]; e[b] = e[b - 1]; e[b - 1] = t; }
+      }
+    for (uint32_t r = 0; r < k; ++r) topk[(size_t)i * k + r] = e[r].idx;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2/K3  PAIR against the ICL-Table snapshot + render.  One warp per request.
+//  PMC (Z11): greedy multiset-feasible prefix; lanes scan table slots, warp argmax
+//  of (pmc, stamp).  Rules: 1 -> target verbatim; 2 -> unchanged;
+//  3 -> the target's first pmc demos replace the first unreplaced same-template current
+//  demos (Z13) and go first, the rest keep their order.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void render_row(const Ctx& c, const uint32_t* ds, uint32_t k,
+                                           const uint32_t* __restrict__ q, uint32_t qL,
+                                           uint32_t* __restrict__ out, uint32_t lane) {
+  uint32_t o = c.n_instr;
+  for (uint32_t x = lane; x < c.n_instr; x += 32) out[x] = c.instr[x];
+  for (uint32_t j = 0; j < k; ++j) {
+    const uint32_t d = ds[j], a = c.rend_off[d], n = c.rend_len[d];
+    for (uint32_t x = lane; x < n; x += 32) out[o + x] = c.rend_tok[a + x];
+    o += n;
+  }
+  for (uint32_t x = lane; x < qL; x += 32) out[o + x] = q[x];
+}
+
+__global__ void __launch_bounds__(256) k_refine(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
+                                                const uint32_t* __restrict__ q_tok,
+                                                const uint32_t* __restrict__ topk,
+                                                uint32_t* __restrict__ final_ds, il_refine_info* __restrict__ info,
+                                                uint32_t* __restrict__ prompt_tok, uint32_t* __restrict__ prompt_len) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t k = c.cfg.k, T = c.cfg.table_capacity;
+  uint32_t cur[MAXK], tc[MAXK], fin[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; ++j) {
+    cur[j] = (uint32_t)j < k ? topk[(size_t)i * k + j] : 0;
+    tc[j] = (uint32_t)j < k ? c.tid[cur[j]] : NONE32;
+    fin[j] = cur[j];
+  }
+  il_refine_info inf;
+  inf.target_stamp = 0; inf.target_slot = -1; inf.pmc = 0; inf.rule = 2; inf.reverted = 0; inf.matched = 0;
+  if (c.cfg.flags & IL_F_PAIR) {
+    uint32_t bp = 0, bs = NONE32;
+    uint64_t bst = 0;
+    for (uint32_t s = lane; s < T; s += 32) {
+      const uint64_t st = c.tab_stamp[s];
+      if (st == 0) continue;
+      uint32_t used = 0, p = 0;
+      for (uint32_t j = 0; j < k; ++j) {
+        const uint32_t t = c.tab_tpl[(size_t)s * k + j];
+        bool found = false;
+#pragma unroll
+        for (int q = 0; q < MAXK; ++q) {
+          if (!found && !((used >> q) & 1u) && tc[q] == t) { used |= 1u << q; found = true; }
+        }
+        if (!found) break;
+        ++p;
+      }
+      if (p > bp || (p == bp && p > 0 && st > bst)) { bp = p; bst = st; bs = s; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const uint32_t op = __shfl_xor_sync(~0u, bp, o), os = __shfl_xor_sync(~0u, bs, o);
+      const uint64_t ost = __shfl_xor_sync(~0u, bst, o);
+      if (op > bp || (op == bp && ost > bst)) { bp = op; bst = ost; bs = os; }
+    }
+    if (bp > 0) {
+      inf.pmc = (uint8_t)bp; inf.matched = 1; inf.target_stamp = bst; inf.target_slot = (int32_t)bs;
+      uint32_t tds[MAXK];
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j) tds[j] = (uint32_t)j < k ? c.tab_ds[(size_t)bs * k + j] : 0;
+      if (bp == k) {
+        inf.rule = 1;
+#pragma unroll
+        for (int j = 0; j < MAXK; ++j) fin[j] = tds[j];
+      } else {
+        inf.rule = 3;
+        uint32_t rep = 0, o = 0;
+        for (uint32_t j = 0; j < bp; ++j) {
+          const uint32_t t = c.tid[tds[j]];
+          bool found = false;
+#pragma unroll
+          for (int q = 0; q < MAXK; ++q)
+            if (!found && (uint32_t)q < k && !((rep >> q) & 1u) && tc[q] == t) { rep |= 1u << q; found = true; }
+          if (!found) latch(c.sc, IL_ERR_INTERNAL);          // cannot happen
+#pragma unroll
+          for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == o) fin[q] = tds[j];
+          ++o;
+        }
+#pragma unroll
+        for (int q = 0; q < MAXK; ++q) {
+          if ((uint32_t)q < k && !((rep >> q) & 1u)) {
+#pragma unroll
+            for (int r = 0; r < MAXK; ++r) if ((uint32_t)r == o) fin[r] = cur[q];
+            ++o;
+          }
+        }
+      }
+    }
+  }
+  const uint32_t qa = q_off[i], qL = q_off[i + 1] - qa;
+  const uint32_t stride = c.cfg.max_prompt_tokens;
+  auto plen = [&](const uint32_t* ds) {
+    uint32_t L = c.n_instr + qL;
+    for (uint32_t j = 0; j < k; ++j) L += c.rend_len[ds[j]];
+    return L;
+  };
+  uint32_t L = plen(fin);
+  uint32_t* row = prompt_tok + (size_t)i * stride;
+  bool changed = false, rendered = false;
+  for (uint32_t j = 0; j < k; ++j) changed |= fin[j] != cur[j];
+  if ((c.cfg.flags & IL_F_GUARD) && changed) {
+    // never-worse guard (Z25): compare the capped hits of DS_final and DS_current against
+    // the index snapshot; keep DS_current if DS_final is strictly worse.
+    const uint32_t Lc = plen(cur);
+    uint32_t* grow = c.guard_prompt + (size_t)i * stride;
+    if (L <= stride && Lc <= stride) {
+      render_row(c, fin, k, q_tok + qa, qL, row, lane);
+      render_row(c, cur, k, q_tok + qa, qL, grow, lane);
+      __syncwarp();
+      const uint32_t hf = warp_hash_match(c, row, L, nullptr, nullptr, true);
+      const uint32_t hc = warp_hash_match(c, grow, Lc, nullptr, nullptr, true);
+      rendered = true;
+      if (hf < hc) {
+        inf.reverted = 1;
+#pragma unroll
+        for (int j = 0; j < MAXK; ++j) fin[j] = cur[j];
+        L = Lc;
+        rendered = false;
+      }
+    }
+  }
+  if (L > stride) {
+    if (lane == 0) latch(c.sc, IL_ERR_ARG);
+    L = 0;
+  } else if (!rendered) {
+    render_row(c, fin, k, q_tok + qa, qL, row, lane);
+  }
+  if (lane == 0) {
+    prompt_len[i] = L;
+    info[i] = inf;
+  }
+  if (lane < k) {
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) if ((uint32_t)j == lane) final_ds[(size_t)i * k + j] = fin[j];
+  }
+}
+
+}  // namespace il
+
+using namespace il;
+
+extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
+                                     const uint32_t* q_src, uint32_t* topk, uint32_t* final_ds,
+                                     il_refine_info* info, uint32_t* prompt_tok, uint32_t* prompt_len,
+                                     il_stream s) {
+  if (!c->pool_loaded) { set_error("il_refine_batch before il_pool_load"); return IL_ERR_STATE; }
+  if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
+  if (B == 0) return IL_OK;
+  cudaStream_t st = (cudaStream_t)s;
+  k_sim_topk<<<B, SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+  k_refine<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
+  IL_LAUNCH_CHECK("il_refine_batch");
+  c->final_ds = final_ds;
+  c->info = info;
+  c->refined = true;
+  c->last_B = B;
+  return IL_OK;
+}

@@ -1,0 +1,116 @@
+"""Batch driver: one pass of the hot path over one batch of concurrent requests.
+
+    il_refine_batch -> il_prefix_match -> (il_synth_qkv: stands in for the QKV projection)
+    -> il_prefill_attn -> il_commit
+
+All buffers are preallocated for the configured maxima (PyTorch memory); all calls are
+asynchronous on one stream; nothing is copied back to the host in steady state.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .context import Config, Context, INFO_DTYPE
+
+
+def _dev_u32(a, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.uint32)).view(np.int32)).to(device)
+
+
+class Pipeline:
+    def __init__(self, cfg: Config, device="cuda", qkv_seed: int = 3000, q_scale: float = 1.0,
+                 max_query_tokens: int | None = None, stream: torch.cuda.Stream | None = None):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.stream = stream
+        self.ctx = Context(cfg, self.device, stream)
+        self.qkv_seed, self.q_scale = qkv_seed, q_scale
+        B, S, MB, k = cfg.max_batch, cfg.max_prompt_tokens, cfg.max_blocks, cfg.k
+        dev, i32 = self.device, torch.int32
+        self.topk = torch.zeros(B, k, dtype=i32, device=dev)
+        self.final_ds = torch.zeros(B, k, dtype=i32, device=dev)
+        self.info = torch.zeros(B, 16, dtype=torch.uint8, device=dev)
+        self.prompt_tok = torch.zeros(B, S, dtype=i32, device=dev)
+        self.prompt_len = torch.zeros(B, dtype=i32, device=dev)
+        self.block_hash = torch.zeros(B, MB, dtype=torch.int64, device=dev)
+        self.hit = torch.zeros(B, dtype=i32, device=dev)
+        self.block_table = torch.zeros(B, MB, dtype=i32, device=dev)
+        self.prefix_len = torch.zeros(B, dtype=i32, device=dev)
+        self.cu_q = torch.zeros(B + 1, dtype=i32, device=dev)
+        rows = cfg.max_suffix_tokens or B * S
+        Hq, Hkv, d = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+        bf = torch.bfloat16
+        self.q = torch.empty(rows, Hq, d, dtype=bf, device=dev)
+        self.k_new = torch.empty(rows, Hkv, d, dtype=bf, device=dev)
+        self.v_new = torch.empty(rows, Hkv, d, dtype=bf, device=dev)
+        self.out = torch.empty(rows, Hq, d, dtype=bf, device=dev)
+        self.lse = torch.empty(rows, Hq, dtype=torch.float32, device=dev)
+        self.k_pages = torch.zeros(cfg.kv_pages, Hkv, 16, d, dtype=bf, device=dev)
+        self.v_pages = torch.zeros(cfg.kv_pages, Hkv, 16, d, dtype=bf, device=dev)
+        mq = max_query_tokens or B * cfg.max_log_tokens
+        self.q_off = torch.zeros(B + 1, dtype=i32, device=dev)
+        self.q_tok = torch.zeros(mq, dtype=i32, device=dev)
+        self.q_src = torch.zeros(B, dtype=i32, device=dev)
+        self.scale = d ** -0.5
+        self.B = 0
+
+    # -------------------------------------------------------------- inputs
+    def load_pool(self, pool, instr) -> None:
+        dev = self.device
+        t = [_dev_u32(x, dev) for x in (pool.log_off, pool.log_tok, pool.tpl_off, pool.tpl_tok,
+                                        pool.template_id, pool.src_index, instr)]
+        self.ctx.pool_load(*t, stream=self.stream)
+        self._pool_keepalive = t
+        self.ctx.status_sync(self.stream)
+
+    def stage_batch(self, batch) -> None:
+        """Copy one batch of query logs into the resident input buffers (host -> device)."""
+        B = batch.B
+        n = int(batch.q_off[-1])
+        self.q_off[:B + 1].copy_(torch.from_numpy(batch.q_off.view(np.int32)), non_blocking=True)
+        self.q_tok[:n].copy_(torch.from_numpy(batch.q_tok.view(np.int32)), non_blocking=True)
+        self.q_src[:B].copy_(torch.from_numpy(batch.q_src.view(np.int32)), non_blocking=True)
+        self.B = B
+
+    # -------------------------------------------------------------- the path
+    def refine(self, B=None) -> None:
+        B = self.B if B is None else B
+        self.ctx.refine_batch(B, self.q_off, self.q_tok, self.q_src, self.topk, self.final_ds, self.info,
+                              self.prompt_tok, self.prompt_len, stream=self.stream)
+
+    def match(self, B=None) -> None:
+        B = self.B if B is None else B
+        self.ctx.prefix_match(B, self.prompt_tok, self.prompt_len, self.block_hash, self.hit,
+                              self.block_table, self.prefix_len, self.cu_q, stream=self.stream)
+
+    def synth(self, B=None) -> None:
+        B = self.B if B is None else B
+        self.ctx.synth_qkv(B, self.prompt_tok, self.cu_q, self.prefix_len, self.qkv_seed, self.q_scale,
+                           self.q, self.k_new, self.v_new, stream=self.stream)
+
+    def attn(self, B=None, lse: bool = True) -> None:
+        B = self.B if B is None else B
+        self.ctx.prefill_attn(B, self.cu_q, self.prefix_len, self.block_table, self.q, self.k_new, self.v_new,
+                              self.k_pages, self.v_pages, self.out, self.lse if lse else None, self.scale,
+                              stream=self.stream)
+
+    def commit(self) -> None:
+        self.ctx.commit(stream=self.stream)
+
+    def step(self, B=None, attention: bool = True) -> None:
+        self.refine(B)
+        self.match(B)
+        if attention:
+            self.synth(B)
+            self.attn(B)
+        self.commit()
+
+    # -------------------------------------------------------------- readback (tests / metrics)
+    def info_np(self, B=None) -> np.ndarray:
+        B = self.B if B is None else B
+        return self.info[:B].cpu().numpy().reshape(-1).view(INFO_DTYPE)
+
+    def u32(self, t: torch.Tensor) -> np.ndarray:
+        return t.cpu().numpy().view(np.uint32)

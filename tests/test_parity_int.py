@@ -1,0 +1,70 @@
+"""GPU vs oracle, bit-exact, over whole synthetic streams (integer stages a1-a7, a9)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.parity_util import StreamSpec, compare_batch, compare_state, gpu_pipeline, make_stream, oracle_for
+from workload import gen
+
+pytestmark = pytest.mark.gpu
+
+
+def run_stream(sp: StreamSpec, state_every: int = 1):
+    ds, pool, instr = make_stream(sp)
+    o = oracle_for(sp, pool, instr)
+    pl = gpu_pipeline(sp, pool, instr)
+    nb = sp.n_batches or (ds.n + sp.B - 1) // sp.B
+    hits = full = 0
+    for b in range(nb):
+        B = sp.B
+        batch = gen.make_batch(ds, b * B, B)
+        r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=(sp.max_prompt_tokens + 15) // 16)
+        pl.stage_batch(batch)
+        pl.refine(); pl.match(); pl.commit()
+        pl.ctx.status_sync()
+        compare_batch(r, pl, B, sp, where=f"batch {b}")
+        if b % state_every == 0 or b == nb - 1:
+            compare_state(o, pl, where=f"after batch {b}")
+        hits += int(r.hit.sum()); full += int((r.prompt_len // 16).sum())
+    st = pl.ctx.stats()
+    return hits / max(full, 1), st
+
+
+def test_c1_stream_pair():
+    rate, st = run_stream(StreamSpec())
+    assert 0 < rate <= 1
+
+
+def test_c1_stream_eviction_pressure_guard():
+    # C small enough that almost every batch evicts; guard on; tombstone rebuilds happen
+    sp = StreamSpec(C=1800, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
+    rate, st = run_stream(sp)
+    assert st["index_rebuilds"] >= 1
+
+
+def test_naive_pc_and_jaccard_exclude_self():
+    run_stream(StreamSpec(flags=O.F_VERIFY, n_batches=8))
+    run_stream(StreamSpec(metric=O.SIM_JACCARD, flags=O.F_PAIR | O.F_VERIFY | O.F_EXCLUDE_SELF, n_batches=8))
+
+
+def test_batch_size_one_and_ragged():
+    # B = 1 is the paper's sequential semantics; B = 37 leaves a ragged last batch of the pool walk
+    run_stream(StreamSpec(B=1, n_batches=150, C=300, T=16))
+    run_stream(StreamSpec(B=37, n_batches=20, k=5, C=900, T=40, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD))
+
+
+def test_k8_large_pool():
+    # k = 8, 2,000-demo pool (config-4-like selection), many templates
+    sp = StreamSpec(n_logs=6000, n_templates=300, zipf=1.3, M=2000, k=8, B=256, T=256, C=8192,
+                    max_prompt_tokens=1024, n_batches=6)
+    run_stream(sp, state_every=2)
+
+
+def test_long_instruction_c3_shape():
+    # ~2k-token prompts (1,836-token instruction, not block aligned): config-3 shape, small B
+    sp = StreamSpec(n_logs=4096, n_templates=300, zipf=1.1, seed=4000, M=200, pool_seed=4001, k=5, B=128,
+                    n_instr=1836, T=4096, C=6000, max_prompt_tokens=2560, n_batches=8,
+                    flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
+    run_stream(sp, state_every=4)
