@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: ICL requests/s of the InferLog hot path (refine + cached prefill) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+A step = one batch of B concurrent requests through the whole path:
+il_refine_batch (kNN + PAIR + render) -> il_prefix_match (chain hash, longest cached prefix,
+LRU evict, page allocation) -> il_synth_qkv (stands in for the QKV projection of the
+suffix tokens) -> il_prefill_attn (K/V append + paged prefill attention) -> il_commit.
+Rank 0 prints one JSON line.  --impl reference times the CPU oracle (oracle/) instead.
+Multi-GPU (torchrun): each rank runs its own slice of every global batch (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workload import gen  # noqa: E402
+
+METRIC = "ICL requests/s (refine+cached prefill), prefix-hit %, % HBM/TC roofline"
+UNIT = "requests/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm": d["hbm_gbs"], "tc": d["bf16_tflops"], "tc_sustained": d.get("bf16_tflops_sustained"),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "tc": 1590.0, "tc_sustained": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def workload(cfg_n: int, rank: int, world: int):
+    cfg = gen.config(cfg_n)
+    name, n, nt, s, seed = cfg.datasets[0]
+    ds = gen.make_dataset(name, n, nt, s, seed)
+    pool = gen.sample_pool(ds, cfg.M, cfg.pool_seed)
+    instr = gen.instruction(cfg.n_instr, cfg.instr_seed)
+    return cfg, ds, pool, instr
+
+
+def plan_batches(cfg, n_full: int, rank: int, world: int, ramp=(1, 64)):
+    """Cold-start ramp (each rank its own), then full batches: global batch g covers queries
+    [off + g*B*world, ...), rank r takes the r-th slice of B (weak scaling)."""
+    plan, off = [], 0
+    for r in ramp:
+        plan.append((off + rank * r, r)); off += r * world
+    for g in range(n_full):
+        plan.append((off + (g * world + rank) * cfg.B, cfg.B))
+    return plan
+
+
+def flops_bytes(plen, hit, bt, Hq, Hkv, d):
+    """Algorithmic work of prefill attention for one batch."""
+    L = plen.astype(np.int64); P = 16 * hit.astype(np.int64); S = L - P
+    flops = float(np.sum(4 * d * Hq * (S * P + S * (S + 1) // 2)))
+    pages = set()
+    for i in range(len(L)):
+        pages.update(bt[i, :hit[i]].tolist())
+    byts = float(np.sum(2 * d * S * (2 * Hq + 4 * Hkv))) + 4.0 * d * Hkv * 16 * len(pages)
+    return flops, byts
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out = self.p.communicate()[0]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_08523_b200 import IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg, ds, pool, instr = workload(args.config, rank, world)
+    flags = IL_F_PAIR | IL_F_VERIFY | (IL_F_GUARD if not args.no_guard else 0)
+    if args.naive:
+        flags = IL_F_VERIFY
+    ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
+                  max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
+                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                  max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
+                  head_dim=cfg.d, flags=flags)
+    stream = torch.cuda.Stream(dev)
+    pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
+    with torch.cuda.stream(stream):
+        pl.load_pool(pool, instr)
+    K, W = args.steps, args.warmup
+    plan = plan_batches(cfg, W + 2 * K, rank, world)
+    n_ramp = len(plan) - (W + 2 * K)
+    batches = [gen.make_batch(ds, s, b) for s, b in plan]
+    # device-resident inputs for the warm-up + device-timed steps
+    dev_in = []
+    for bt in batches[:n_ramp + W + K]:
+        dev_in.append((torch.from_numpy(bt.q_off.view(np.int32)).to(dev), torch.from_numpy(bt.q_tok.view(np.int32)).to(dev),
+                       torch.from_numpy(bt.q_src.view(np.int32)).to(dev), bt.B))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def set_inputs(x):
+        pl.q_off, pl.q_tok, pl.q_src, pl.B = x
+
+    # ---- warm-up (cold-start ramp + W full steps), not timed
+    with torch.cuda.stream(stream):
+        for x in dev_in[:n_ramp + W]:
+            set_inputs(x)
+            pl.step()
+    stream.synchronize()
+    pl.ctx.status_sync(stream)
+
+    # ---- device-timed steps: inputs resident in HBM, L2 flushed between steps
+    stage_names = ["refine", "match", "synth", "attn", "commit"]
+    step_ms, stage_ms, attn_ms, work = [], {n: [] for n in stage_names}, [], []
+    hits = fulls = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    t_wall = time.perf_counter()
+    launches0 = pl.launches()
+    for x in dev_in[n_ramp + W:]:
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            set_inputs(x)
+            e = [ev() for _ in range(6)]
+            e[0].record(stream); pl.refine()
+            e[1].record(stream); pl.match()
+            e[2].record(stream); pl.synth()
+            e[3].record(stream); pl.attn()
+            e[4].record(stream); pl.commit()
+            e[5].record(stream)
+        e[5].synchronize()
+        step_ms.append(e[0].elapsed_time(e[5]))
+        for j, n in enumerate(stage_names):
+            stage_ms[n].append(e[j].elapsed_time(e[j + 1]))
+        B = x[3]
+        plen = pl.prompt_len[:B].cpu().numpy(); hit = pl.hit[:B].cpu().numpy()
+        bt = pl.block_table[:B].cpu().numpy()
+        work.append(flops_bytes(plen, hit, bt, cfg.Hq, cfg.Hkv, cfg.d))
+        hits += int(hit.sum()); fulls += int((plen // 16).sum())
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    launches = pl.launches() - launches0
+    pl.ctx.status_sync(stream)
+    if world > 1:
+        dist.barrier()
+
+    # ---- end-to-end: host (pinned) inputs in, results out, every step
+    pinned = []
+    for bt in batches[n_ramp + W + K:]:
+        pinned.append(tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src))
+                      + (bt.B,))
+    out_fin = torch.empty(cfg.B, cfg.k, dtype=torch.int32).pin_memory()
+    out_hit = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
+    out_info = torch.empty(cfg.B, 16, dtype=torch.uint8).pin_memory()
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for qo, qt, qs, B in pinned:
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            pl.q_off[:B + 1].copy_(qo, non_blocking=True)
+            pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
+            pl.q_src[:B].copy_(qs, non_blocking=True)
+            pl.B = B
+            pl.step()
+            out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
+            out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
+            out_info[:B].copy_(pl.info[:B], non_blocking=True)
+            e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
+        d2h = 4 * B * cfg.k + 4 * B + 16 * B
+    pl.ctx.status_sync(stream)
+
+    # ---- reduce over ranks (max time)
+    ms = float(np.mean(step_ms)); e2e = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([ms, e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    pk = peaks()
+    fl = np.array([w[0] for w in work]); by = np.array([w[1] for w in work])
+    at = np.array(stage_ms["attn"]) * 1e-3
+    t_tc = fl / (pk["tc"] * 1e12); t_hbm = by / (pk["hbm"] * 1e9)
+    bound = "tensor" if t_tc.sum() >= t_hbm.sum() else "hbm"
+    if bound == "tensor":
+        achieved = float(fl.sum() / at.sum() / 1e12); peak = pk["tc"]; unitr = "TFLOP/s"
+    else:
+        achieved = float(by.sum() / at.sum() / 1e9); peak = pk["hbm"]; unitr = "GB/s"
+    B_all = cfg.B * world
+    line = {
+        "metric": METRIC, "value": B_all / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
+                   "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
+                   "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
+                   "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards)",
+                   "int_dtype": "u32/u64 bit-exact", "attn": "bf16 in, fp32 accumulate"},
+        "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
+        "stage_ms": {n: float(np.mean(v)) for n, v in stage_ms.items()},
+        "roofline": {"kernel": "il_prefill_attn (K/V append + attention)", "bound": bound, "achieved": achieved,
+                     "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": None,
+                     "peak_src": pk["src"] + (" burst bf16" if bound == "tensor" else ""),
+                     "flops_per_step": float(fl.mean()), "bytes_per_step": float(by.mean()),
+                     "t_star_ms": float(np.maximum(t_tc, t_hbm).mean() * 1e3)},
+        "e2e": {"value": B_all / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "wall_s_timed": wall,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, cfg, ds, pool, instr, plan, n_ramp + W, flags)
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn: int, n_steps: int = 1):
+    """The CPU oracle as it stands: replay the warm-up batches (untimed), then time the integer
+    path over full batches and fp64 attention over a sample of their requests."""
+    import oracle as O
+    o = O.Oracle(cfg.k, cfg.T, cfg.C, flags=flags)
+    o.pool_load(pool, instr)
+    for s, b in plan[:n_warm]:
+        o.run_batch(gen.make_batch(ds, s, b), prompt_stride=cfg.max_prompt_tokens, max_blocks=cfg.max_prompt_tokens // 16)
+    t_int = t_att = 0.0
+    n_int = n_att = 0
+    rng = np.random.default_rng(0)
+    for s, b in plan[n_warm:n_warm + n_steps]:
+        t0 = time.perf_counter()
+        r = o.run_batch(gen.make_batch(ds, s, b), prompt_stride=cfg.max_prompt_tokens,
+                        max_blocks=cfg.max_prompt_tokens // 16)
+        t_int += time.perf_counter() - t0
+        n_int += b
+        for i in rng.choice(b, size=min(n_attn, b), replace=False):
+            L, P = int(r.prompt_len[i]), 16 * int(r.hit[i])
+            toks, pos = r.prompt(i), np.arange(L)
+            q = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "q", toks[P:], pos[P:], cfg.Hq, cfg.d))
+            k = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "k", toks, pos, cfg.Hkv, cfg.d))
+            v = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "v", toks, pos, cfg.Hkv, cfg.d))
+            t0 = time.perf_counter()
+            O.attention(q, k, v, P=P, scale=cfg.d ** -0.5)
+            t_att += time.perf_counter() - t0
+            n_att += 1
+    per_req = t_int / n_int + t_att / max(n_att, 1)
+    return 1.0 / per_req, t_int, n_int, t_att, n_att
+
+
+def cpu_baseline(args, cfg, ds, pool, instr, plan, n_warm, flags):
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    v, t_int, n_int, t_att, n_att = oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn=args.cpu_attn_sample)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"integer path of {n_int} requests (one full batch after {n_warm} warm-up batches) in {t_int:.2f} s "
+                      f"+ fp64 attention of {n_att} sampled requests in {t_att:.2f} s; requests/s = 1 / per-request time",
+            "cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg, ds, pool, instr = workload(args.config, 0, 1)
+    import oracle as O
+    flags = O.F_PAIR | O.F_VERIFY | (0 if args.no_guard else O.F_GUARD)
+    K, W = args.steps, args.warmup
+    plan = plan_batches(cfg, W + K, 0, 1)
+    n_ramp = len(plan) - (W + K)
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    o = O.Oracle(cfg.k, cfg.T, cfg.C, flags=flags)
+    o.pool_load(pool, instr)
+    rng = np.random.default_rng(0)
+    per_req = []
+    for j, (s, b) in enumerate(plan):
+        t0 = time.perf_counter()
+        r = o.run_batch(gen.make_batch(ds, s, b), prompt_stride=cfg.max_prompt_tokens, max_blocks=cfg.max_prompt_tokens // 16)
+        t_int = time.perf_counter() - t0
+        if j < n_ramp + W:
+            continue
+        t_att, n_att = 0.0, 0
+        for i in rng.choice(b, size=min(args.cpu_attn_sample, b), replace=False):
+            L, P = int(r.prompt_len[i]), 16 * int(r.hit[i])
+            toks, pos = r.prompt(i), np.arange(L)
+            q = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "q", toks[P:], pos[P:], cfg.Hq, cfg.d))
+            kk = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "k", toks, pos, cfg.Hkv, cfg.d))
+            vv = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "v", toks, pos, cfg.Hkv, cfg.d))
+            t1 = time.perf_counter()
+            O.attention(q, kk, vv, P=P, scale=cfg.d ** -0.5)
+            t_att += time.perf_counter() - t1
+            n_att += 1
+        per_req.append(t_int / b + t_att / max(n_att, 1))
+    v = 1.0 / float(np.mean(per_req))
+    ms = 1e3 * cfg.B / v
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
+                   "requests_per_gpu_per_step": cfg.B},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"per step: integer path of one full batch of {cfg.B} requests + fp64 attention of "
+                                   f"{args.cpu_attn_sample} sampled requests; requests/s = 1 / mean per-request time",
+                         "cpu": cpu_model()},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-guard", action="store_true")
+    ap.add_argument("--naive", action="store_true", help="PAIR off (naive prefix caching)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-attn-sample", type=int, default=8)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,7 @@ typedef struct {               /* counters of the last committed batch (il_stats
   uint32_t suffix_tokens;      /* sum of suffix lengths of the last il_prefix_match */
   uint32_t index_rebuilds;     /* tombstone compactions so far */
   uint32_t status;             /* latched il_status */
+  uint64_t launches;           /* kernels this context has launched so far */
 } il_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */

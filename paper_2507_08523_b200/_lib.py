@@ -46,7 +46,8 @@ class il_refine_info(C.Structure):
 class il_stats(C.Structure):
     _fields_ = [("batch", C.c_uint64), ("resident_blocks", C.c_uint32), ("free_pages", C.c_uint32),
                 ("table_entries", C.c_uint32), ("evicted_blocks", C.c_uint32), ("need_pages", C.c_uint32),
-                ("suffix_tokens", C.c_uint32), ("index_rebuilds", C.c_uint32), ("status", C.c_uint32)]
+                ("suffix_tokens", C.c_uint32), ("index_rebuilds", C.c_uint32), ("status", C.c_uint32),
+                ("launches", C.c_uint64)]
 
 
 assert C.sizeof(il_refine_info) == 16

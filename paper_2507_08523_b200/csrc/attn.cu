@@ -191,6 +191,7 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
   k_kv_append<<<c->num_sms * 8, 256, 0, st>>>(*c, B, cu_q, prefix_len, block_table, (const uint4*)k_new,
                                               (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
   IL_LAUNCH_CHECK("k_kv_append");
+  c->launches += 1;
   if (attn_sm100_supported(c)) {
     return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
   }
@@ -212,5 +213,6 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
         (__nv_bfloat16*)out, lse, scale);
   }
   IL_LAUNCH_CHECK("k_attn_simple");
+  c->launches += 2;
   return IL_OK;
 }

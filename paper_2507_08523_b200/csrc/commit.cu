@@ -365,6 +365,7 @@ extern "C" il_status il_commit(il_ctx* c, il_stream s) {
     k_tab_commit<<<1, 1024, smem, st>>>(*c, B, b_cur);
   }
   IL_LAUNCH_CHECK("il_commit");
+  c->launches += (B ? 3 : 0) + 1 + ((pair && B) ? 2 : 0);
   c->batch = b_cur;
   c->refined = c->matched = false;
   return IL_OK;

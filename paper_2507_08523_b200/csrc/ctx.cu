@@ -276,6 +276,7 @@ il_status il_stats_sync(il_ctx* c, il_stream s, il_stats* out) {
   out->suffix_tokens = h.suffix_total;
   out->index_rebuilds = h.rebuilds;
   out->status = h.status;
+  out->launches = c->launches;
   return IL_OK;
 }
 

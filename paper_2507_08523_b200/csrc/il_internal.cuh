@@ -87,6 +87,7 @@ struct Ctx {
   const uint32_t* hit = nullptr;
   const int32_t* block_table = nullptr;
   int num_sms = 148;
+  uint64_t launches = 0;     // kernels launched by this context (host counter)
 };
 
 // ---------------------------------------------------------------- error plumbing (host)

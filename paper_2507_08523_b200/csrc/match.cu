@@ -234,6 +234,7 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
   k_alloc_commit<<<1, 1, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_prefix_match");
+  c->launches += B ? 5 : 3;
   c->prompt_tok = prompt_tok;
   c->prompt_len = prompt_len;
   c->block_hash = block_hash;

@@ -327,6 +327,7 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   k_sim_topk<<<B, SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
   k_refine<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
+  c->launches += 2;
   c->final_ds = final_ds;
   c->info = info;
   c->refined = true;

@@ -58,5 +58,6 @@ extern "C" il_status il_synth_qkv(il_ctx* c, uint32_t B, const uint32_t* prompt_
                                                         (__nv_bfloat16*)q, (__nv_bfloat16*)k_new,
                                                         (__nv_bfloat16*)v_new);
   IL_LAUNCH_CHECK("k_synth");
+  c->launches += 1;
   return IL_OK;
 }

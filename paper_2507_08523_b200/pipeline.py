@@ -99,6 +99,10 @@ class Pipeline:
     def commit(self) -> None:
         self.ctx.commit(stream=self.stream)
 
+    def launches(self) -> int:
+        """Kernels this context has launched so far (host-side counter in the library)."""
+        return int(self.ctx.stats(self.stream)["launches"])
+
     def step(self, B=None, attention: bool = True) -> None:
         self.refine(B)
         self.match(B)

@@ -30,6 +30,18 @@ class StreamSpec:
     flags: int = O.F_PAIR | O.F_VERIFY
     hash_seed: int = 0
     n_batches: int | None = None
+    ramp: tuple = ()           # sizes of the first batches (cold-start warm-up), then B
+
+
+def batch_plan(sp: StreamSpec, n_logs: int):
+    """(start, size) of each batch: the ramp, then full batches of B over the stream."""
+    plan, start = [], 0
+    for r in sp.ramp:
+        plan.append((start, r)); start += r
+    nb = sp.n_batches if sp.n_batches is not None else (n_logs - start + sp.B - 1) // sp.B + len(plan)
+    while len(plan) < nb:
+        plan.append((start, sp.B)); start += sp.B
+    return plan
 
 
 def make_stream(sp: StreamSpec):

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests.parity_util import StreamSpec, gpu_pipeline, make_stream, oracle_for
+from tests.parity_util import StreamSpec, batch_plan, gpu_pipeline, make_stream, oracle_for
 from workload import gen
 
 pytestmark = pytest.mark.gpu
@@ -53,15 +53,16 @@ def run(sp: StreamSpec, n_batches: int, seed=3000, q_scale=1.0, sample=6, max_ro
     pl.qkv_seed, pl.q_scale = seed, q_scale
     rng = np.random.default_rng(0)
     worst = 0.0
-    for b in range(n_batches):
-        batch = gen.make_batch(ds, b * sp.B, sp.B)
+    sp.n_batches = n_batches
+    for b, (start, B) in enumerate(batch_plan(sp, ds.n)):
+        batch = gen.make_batch(ds, start, B)
         r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=(sp.max_prompt_tokens + 15) // 16)
         pl.stage_batch(batch)
         pl.step()
         pl.ctx.status_sync()
-        np.testing.assert_array_equal(pl.u32(pl.hit[:sp.B]), r.hit)
-        picks = set(rng.choice(sp.B, size=min(sample, sp.B), replace=False).tolist())
-        picks |= {int(np.argmax(r.hit)), int(np.argmin(r.hit)), sp.B - 1}
+        np.testing.assert_array_equal(pl.u32(pl.hit[:B]), r.hit)
+        picks = set(rng.choice(B, size=min(sample, B), replace=False).tolist())
+        picks |= {int(np.argmax(r.hit)), int(np.argmin(r.hit)), B - 1}
         for i in sorted(picks):
             worst = max(worst, check_request(pl, r, i, sp, seed, q_scale, max_rows))
     return worst
@@ -86,5 +87,5 @@ def test_attention_qwen_shape_k8():
 
 def test_attention_long_prompts():
     sp = StreamSpec(n_logs=4096, n_templates=300, zipf=1.1, seed=4000, pool_seed=4001, k=5, B=8, n_instr=1836,
-                    T=4096, C=4096, max_prompt_tokens=2560, Hq=32, Hkv=8, d=128)
+                    T=4096, C=4096, max_prompt_tokens=2560, Hq=32, Hkv=8, d=128, ramp=(1,))
     run(sp, n_batches=3, sample=3, max_rows=48)

@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 import oracle as O
-from tests.parity_util import StreamSpec, compare_batch, compare_state, gpu_pipeline, make_stream, oracle_for
+from tests.parity_util import (StreamSpec, batch_plan, compare_batch, compare_state, gpu_pipeline, make_stream,
+                               oracle_for)
 from workload import gen
 
 pytestmark = pytest.mark.gpu
@@ -15,11 +16,11 @@ def run_stream(sp: StreamSpec, state_every: int = 1):
     ds, pool, instr = make_stream(sp)
     o = oracle_for(sp, pool, instr)
     pl = gpu_pipeline(sp, pool, instr)
-    nb = sp.n_batches or (ds.n + sp.B - 1) // sp.B
     hits = full = 0
-    for b in range(nb):
-        B = sp.B
-        batch = gen.make_batch(ds, b * B, B)
+    plan = batch_plan(sp, ds.n)
+    nb = len(plan)
+    for b, (start, B) in enumerate(plan):
+        batch = gen.make_batch(ds, start, B)
         r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=(sp.max_prompt_tokens + 15) // 16)
         pl.stage_batch(batch)
         pl.refine(); pl.match(); pl.commit()
@@ -39,8 +40,8 @@ def test_c1_stream_pair():
 
 def test_c1_stream_eviction_pressure_guard():
     # C small enough that almost every batch evicts; guard on; tombstone rebuilds happen
-    sp = StreamSpec(C=1800, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
-    rate, st = run_stream(sp)
+    sp = StreamSpec(C=1800, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, n_batches=60)
+    rate, st = run_stream(sp, state_every=3)
     assert st["index_rebuilds"] >= 1
 
 
@@ -65,6 +66,6 @@ def test_k8_large_pool():
 def test_long_instruction_c3_shape():
     # ~2k-token prompts (1,836-token instruction, not block aligned): config-3 shape, small B
     sp = StreamSpec(n_logs=4096, n_templates=300, zipf=1.1, seed=4000, M=200, pool_seed=4001, k=5, B=128,
-                    n_instr=1836, T=4096, C=6000, max_prompt_tokens=2560, n_batches=8,
+                    n_instr=1836, T=4096, C=6000, max_prompt_tokens=2560, n_batches=8, ramp=(1, 8),
                     flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
     run_stream(sp, state_every=4)
