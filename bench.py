@@ -196,6 +196,9 @@ def run_ours(args, rank, world, local_rank):
     out_hit = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
     out_info = torch.empty(cfg.B, 16, dtype=torch.uint8).pin_memory()
     h2d = d2h = 0
+    pl.q_off = torch.zeros(cfg.B + 1, dtype=torch.int32, device=dev)
+    pl.q_tok = torch.zeros(cfg.B * 256, dtype=torch.int32, device=dev)
+    pl.q_src = torch.zeros(cfg.B, dtype=torch.int32, device=dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -40,8 +40,8 @@ def test_c1_stream_pair():
 
 def test_c1_stream_eviction_pressure_guard():
     # C small enough that almost every batch evicts; guard on; tombstone rebuilds happen
-    sp = StreamSpec(C=1800, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, n_batches=60)
-    rate, st = run_stream(sp, state_every=3)
+    sp = StreamSpec(C=700, B=32, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, n_batches=240)
+    rate, st = run_stream(sp, state_every=5)
     assert st["index_rebuilds"] >= 1
 
 
