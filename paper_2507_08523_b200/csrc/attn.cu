@@ -192,9 +192,8 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
                                               (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
   IL_LAUNCH_CHECK("k_kv_append");
   c->launches += 1;
-  if (attn_sm100_supported(c)) {
+  if (attn_sm100_supported(c))
     return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
-  }
   if (g * SIMPLE_TQ > 128) { set_error("bring-up attention: Hq/Hkv > 8 unsupported"); return IL_ERR_ARG; }
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, SIMPLE_TQ);
   const uint32_t R = SIMPLE_TQ * g;

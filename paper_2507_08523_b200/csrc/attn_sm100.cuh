@@ -1,12 +1,449 @@
-// attn_sm100.cuh — tcgen05/TMA prefill attention (placeholder until the kernel lands).
+// attn_sm100.cuh — paged prefill attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// One work item = (request i, kv head kh, M-tile of TQ = 128/g suffix tokens).  The g q-heads
+// sharing kv head kh are packed as rows (row = token * g + head) so one 128-row tcgen05 tile
+// covers TQ tokens x g heads (GQA packing).  KV tiles are 128 keys = 8 pages of 16 tokens,
+// each page a [16][128] bf16 block of the caller's [C][Hkv][16][d] cache, fetched by TMA
+// (two 64-column boxes per page, 128-byte swizzle).  Per KV tile:
+//   S = Q K^T      tcgen05.mma kind::f16, A = Q (smem, K-major), B = K tile (smem, K-major),
+//                  D in TMEM (fp32, 128 lanes x 128 columns, double buffered)
+//   softmax        4 warps, one TMEM lane (= one row) per thread: causal mask, running max with
+//                  a lazy rescale (O is rescaled in TMEM only when the max grows by > 2^8), exp2,
+//                  P written as bf16 to smem in the UMMA K-major 128B-swizzled layout
+//   O += P V       A = P (smem, K-major), B = V tile (smem, MN-major), D = O in TMEM
+// Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer, warp 1 = MMA issuer
+// (one thread), warp 2 = TMEM allocator, warps 4-7 = softmax + epilogue.  Producer/consumer
+// hand-offs are mbarriers; MMA completion is signalled with tcgen05.commit.
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
 #include "il_internal.cuh"
 
 namespace il {
-static inline bool attn_sm100_supported(const Ctx*) { return false; }
-static inline il_status attn_sm100_launch(Ctx*, uint32_t, const int32_t*, const int32_t*, const int32_t*,
-                                          const il_bf16*, il_bf16*, il_bf16*, il_bf16*, float*, float,
-                                          cudaStream_t) {
-  return IL_ERR_INTERNAL;
+namespace sm100 {
+
+constexpr uint32_t D = 128;              // head dim handled by this kernel
+constexpr uint32_t BM = 128, BN = 128;   // rows per M-tile, keys per KV tile
+constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
+constexpr uint32_t TILE = 2 * CB;        // 128 x 128 bf16 = 32 KB
+constexpr uint32_t OFF_Q = 0;
+constexpr uint32_t OFF_K = TILE;                 // K[s] = OFF_K + s * 2 * TILE
+constexpr uint32_t OFF_V = 2 * TILE;             // V[s] = OFF_V + s * 2 * TILE
+constexpr uint32_t OFF_P = 5 * TILE;             // P[b] = OFF_P + b * TILE
+constexpr uint32_t OFF_BAR = 7 * TILE;
+constexpr uint32_t NBAR = 20;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;   // + alignment slack
+constexpr int THREADS = 256;
+
+enum Bar { Q_FULL = 0, Q_FREE = 1, KV_FULL = 2, KV_FREE = 4, S_FULL = 6, S_FREE = 8, P_FULL = 10,
+           P_FREE = 12, O_FULL = 14, O_FREE = 16 };
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread t of the warp gets its lane's 32 columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,"
+      "%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));   // low half = a
+  return r;
+}
+
+// UMMA shared-memory descriptor (sm100): start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46),
+// version 1 [46,48), layout SWIZZLE_128B = 2 [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+// A major [15] (0 = K), B major [16] (1 = MN), N >> 3 [17,23), M >> 4 [24,29)
+constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+constexpr uint32_t IDESC_PV = IDESC_QK | (1u << 16);
+
+struct Item {
+  uint32_t i, kh, mt, P, S, r0, ntok, n_kv, nblk;
+};
+__device__ __forceinline__ Item decode_item(const Ctx& c, uint32_t B, const int32_t* __restrict__ cu_q,
+                                            const int32_t* __restrict__ prefix_len, uint32_t w, uint32_t Hkv,
+                                            uint32_t TQ) {
+  Item it;
+  const uint32_t t = w / Hkv;
+  it.kh = w % Hkv;
+  uint32_t lo = 0, hi = B;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (c.tile_off[mid] <= t) lo = mid; else hi = mid;
+  }
+  it.i = lo;
+  it.mt = t - c.tile_off[lo];
+  it.P = (uint32_t)prefix_len[lo];
+  it.r0 = (uint32_t)cu_q[lo];
+  it.S = (uint32_t)cu_q[lo + 1] - it.r0;
+  it.ntok = min(TQ, it.S - it.mt * TQ);
+  const uint32_t p_last = it.P + it.mt * TQ + it.ntok - 1;
+  it.n_kv = p_last / BN + 1;
+  it.nblk = cdiv(it.P + it.S, BS);
+  return it;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
+                 const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                 float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
+                 const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto bar = [&](uint32_t idx) { return bar0 + 8 * idx; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
+  const uint32_t n_items = c.sc->n_tiles * Hkv;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar(KV_FULL + s), 1); mbar_init(bar(KV_FREE + s), 1);
+      mbar_init(bar(S_FULL + s), 1);  mbar_init(bar(S_FREE + s), 128);
+      mbar_init(bar(P_FULL + s), 128); mbar_init(bar(P_FREE + s), 1);
+      mbar_init(bar(O_FULL + s), 1);  mbar_init(bar(O_FREE + s), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_k) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_v) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ================= TMA producer =================
+    uint32_t kt = 0, it = 0;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
+      if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
+      mbar_expect_tx(bar(Q_FULL), 2 * 128 * g * TQ);
+      const int qrow = (int)(I.r0 + I.mt * TQ);
+      tma_load_3d(sbase + OFF_Q, &tm_q, 0, (int)(I.kh * g), qrow, bar(Q_FULL));
+      tma_load_3d(sbase + OFF_Q + CB, &tm_q, 64, (int)(I.kh * g), qrow, bar(Q_FULL));
+      const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
+      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
+        const uint32_t s = kt & 1;
+        if (kt >= 2) mbar_wait(bar(KV_FREE + s), ((kt - 2) >> 1) & 1);
+        mbar_expect_tx(bar(KV_FULL + s), 2 * TILE);
+        const uint32_t ks = sbase + OFF_K + s * 2 * TILE, vs = sbase + OFF_V + s * 2 * TILE;
+#pragma unroll 1
+        for (uint32_t p = 0; p < 8; ++p) {
+          const uint32_t blk = n * 8 + p;
+          const int32_t page = blk < I.nblk ? bt[blk] : bt[0];
+          const int row = (int)(((uint32_t)page * Hkv + I.kh) * BS);
+          tma_load_2d(ks + p * 2048, &tm_k, 0, row, bar(KV_FULL + s));
+          tma_load_2d(ks + CB + p * 2048, &tm_k, 64, row, bar(KV_FULL + s));
+          tma_load_2d(vs + p * 2048, &tm_v, 0, row, bar(KV_FULL + s));
+          tma_load_2d(vs + CB + p * 2048, &tm_v, 64, row, bar(KV_FULL + s));
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ================= MMA issuer (single thread) =================
+    uint32_t kt = 0, it = 0;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
+      const uint32_t ob = it & 1;
+      const uint32_t o_tmem = tmem + 256 + ob * 128;
+      mbar_wait(bar(Q_FULL), it & 1);
+      if (it >= 2) mbar_wait(bar(O_FREE + ob), ((it - 2) >> 1) & 1);
+      tc_fence_after();
+      auto pv = [&](uint32_t tt, bool first) {
+        const uint32_t pb = tt & 1;
+        mbar_wait(bar(P_FULL + pb), (tt >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ps = sbase + OFF_P + pb * TILE, vs = sbase + OFF_V + (tt & 1) * 2 * TILE;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          const uint64_t a = sdesc(ps + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc(vs + k * 2048, CB, 1024);
+          tc_mma(o_tmem, a, b, IDESC_PV, (first && k == 0) ? 0u : 1u);
+        }
+        tc_commit(bar(P_FREE + pb));
+        tc_commit(bar(KV_FREE + (tt & 1)));
+      };
+      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
+        const uint32_t s = kt & 1;
+        mbar_wait(bar(KV_FULL + s), (kt >> 1) & 1);
+        if (kt >= 2) mbar_wait(bar(S_FREE + s), ((kt - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ks = sbase + OFF_K + s * 2 * TILE;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          const uint64_t a = sdesc(sbase + OFF_Q + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc(ks + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
+          tc_mma(tmem + s * 128, a, b, IDESC_QK, k ? 1u : 0u);
+        }
+        tc_commit(bar(S_FULL + s));
+        if (n + 1 == I.n_kv) tc_commit(bar(Q_FREE));
+        if (n >= 1) pv(kt - 1, n == 1);
+      }
+      pv(kt - 1, I.n_kv == 1);
+      tc_commit(bar(O_FULL + ob));
+    }
+  } else if (warp >= 4) {
+    // ================= softmax + epilogue (thread = row) =================
+    const uint32_t r = threadIdx.x - 128, q4 = warp - 4;
+    const uint32_t lane_addr = (32 * q4) << 16;
+    uint32_t kt = 0, it = 0;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
+      const uint32_t t = r / g, hh = r % g;
+      const bool valid = (r < g * TQ) && (t < I.ntok);
+      const uint32_t pos_q = I.P + I.mt * TQ + min(t, I.ntok - 1);
+      const uint32_t ob = it & 1;
+      const uint32_t o_tmem = tmem + lane_addr + 256 + ob * 128;
+      float m_used = -INFINITY, l = 0.f;
+      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
+        const uint32_t s = kt & 1;
+        mbar_wait(bar(S_FULL + s), (kt >> 1) & 1);
+        tc_fence_after();
+        float sv[128];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tmem_ld32(tmem + lane_addr + s * 128 + 32 * q, *reinterpret_cast<float(*)[32]>(&sv[32 * q]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(bar(S_FREE + s));
+        const uint32_t key0 = n * BN;
+        if (key0 + BN - 1 > pos_q) {
+#pragma unroll
+          for (int j = 0; j < 128; ++j)
+            if (key0 + j > pos_q) sv[j] = -INFINITY;
+        }
+        float mx = sv[0];
+#pragma unroll
+        for (int j = 1; j < 128; ++j) mx = fmaxf(mx, sv[j]);
+        const float mx2 = mx * scale_log2;
+        bool need = false;
+        float factor = 1.f;
+        if (n == 0) {
+          m_used = mx2;
+        } else if (mx2 > m_used + 8.f) {
+          need = true;
+          factor = ex2(m_used - mx2);
+          m_used = mx2;
+          l *= factor;
+        }
+        if (__any_sync(~0u, need)) {
+          // lazy rescale of this warp's O rows: wait until PV of the previous tile has landed
+          mbar_wait(bar(P_FREE + ((kt - 1) & 1)), ((kt - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float ov[32];
+            tmem_ld32(o_tmem + 32 * q, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] *= factor;
+            tmem_st32(o_tmem + 32 * q, ov);
+          }
+          tmem_wait_st();
+        }
+        const float negm = -m_used;
+        float rs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+          sv[j] = ex2(fmaf(sv[j], scale_log2, negm));
+          rs += sv[j];
+        }
+        l += rs;
+        const uint32_t pb = kt & 1;
+        if (kt >= 2) mbar_wait(bar(P_FREE + pb), ((kt - 2) >> 1) & 1);
+        uint8_t* prow = smem + OFF_P + pb * TILE + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          uint4 v;
+          v.x = pack_bf16(sv[8 * ch + 0], sv[8 * ch + 1]);
+          v.y = pack_bf16(sv[8 * ch + 2], sv[8 * ch + 3]);
+          v.z = pack_bf16(sv[8 * ch + 4], sv[8 * ch + 5]);
+          v.w = pack_bf16(sv[8 * ch + 6], sv[8 * ch + 7]);
+          *reinterpret_cast<uint4*>(prow + (ch >> 3) * CB + (((ch & 7) ^ (r & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(bar(P_FULL + pb));
+      }
+      // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
+      mbar_wait(bar(O_FULL + ob), (it >> 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const size_t orow = ((size_t)(I.r0 + I.mt * TQ + t) * Hq + I.kh * g + hh);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float ov[32];
+        tmem_ld32(o_tmem + 32 * q, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint4 v;
+            v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
+            v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
+            v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
+            v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
+            dst[ch] = v;
+          }
+        }
+      }
+      if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+      tc_fence_before();
+      mbar_arrive(bar(O_FREE + ob));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+}  // namespace sm100
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+static inline bool attn_sm100_supported(const Ctx* c) {
+  const char* e = getenv("IL_ATTN");
+  if (e && e[0] == 's') return false;                 // IL_ATTN=simple: bring-up kernel (cross-checks)
+  const uint32_t g = c->cfg.n_q_heads / c->cfg.n_kv_heads;
+  return c->cfg.head_dim == sm100::D && g >= 1 && g <= 8;
+}
+
+static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
+                                          const int32_t* block_table, const il_bf16* q, il_bf16* k_pages,
+                                          il_bf16* v_pages, il_bf16* out, float* lse, float scale, cudaStream_t st) {
+  using namespace sm100;
+  const uint32_t Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads, g = Hq / Hkv, TQ = BM / g;
+  auto enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return IL_ERR_CUDA; }
+  CUtensorMap tq, tk, tv;
+  {
+    cuuint64_t dims[3] = {D, Hq, c->cfg.max_suffix_tokens};
+    cuuint64_t strides[2] = {D * 2, (cuuint64_t)Hq * D * 2};
+    cuuint32_t box[3] = {64, g, TQ};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)q, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("tensor map (q) encode failed"); return IL_ERR_CUDA; }
+  }
+  for (int which = 0; which < 2; ++which) {
+    cuuint64_t dims[2] = {D, (cuuint64_t)c->cfg.kv_pages * Hkv * BS};
+    cuuint64_t strides[1] = {D * 2};
+    cuuint32_t box[2] = {64, BS};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(which ? &tv : &tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, which ? (void*)v_pages : (void*)k_pages,
+                     dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("tensor map (kv) encode failed"); return IL_ERR_CUDA; }
+  }
+  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, TQ);
+  static bool attr = false;
+  if (!attr) {
+    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr = true;
+  }
+  k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out, lse,
+                                                        scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+  IL_LAUNCH_CHECK("k_attn_sm100");
+  c->launches += 2;
+  return IL_OK;
+}
+
 }  // namespace il
