@@ -9,11 +9,13 @@
 //                  D in TMEM (fp32, 128 lanes x 128 columns, double buffered)
 //   softmax        4 warps, one TMEM lane (= one row) per thread: causal mask, running max with
 //                  a lazy rescale (O is rescaled in TMEM only when the max grows by > 2^8), exp2,
-//                  P written as bf16 to smem in the UMMA K-major 128B-swizzled layout
-//   O += P V       A = P (smem, K-major), B = V tile (smem, MN-major), D = O in TMEM
-// Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer, warp 1 = MMA issuer
-// (one thread), warp 2 = TMEM allocator, warps 4-7 = softmax + epilogue.  Producer/consumer
-// hand-offs are mbarriers; MMA completion is signalled with tcgen05.commit.
+//                  P written back as packed bf16 over the first 64 columns of its S in TMEM
+//   O += P V       A = P (TMEM), B = V tile (smem, MN-major), D = O in TMEM
+// K and V stream through separate 3-deep smem rings (K is released right after QK, V after
+// PV).  Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer for Q and K,
+// warp 3 = TMA producer for V, warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
+// warps 4-7 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
+// tcgen05.commit; tcgen05.mma from one thread execute in order, which orders the reuse of S.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -28,17 +30,17 @@ constexpr uint32_t D = 128;              // head dim handled by this kernel
 constexpr uint32_t BM = 128, BN = 128;   // rows per M-tile, keys per KV tile
 constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
 constexpr uint32_t TILE = 2 * CB;        // 128 x 128 bf16 = 32 KB
+constexpr uint32_t NST = 3;              // K and V ring depth (each)
 constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_K = TILE;                 // K[s] = OFF_K + s * 2 * TILE
-constexpr uint32_t OFF_V = 2 * TILE;             // V[s] = OFF_V + s * 2 * TILE
-constexpr uint32_t OFF_P = 5 * TILE;             // P[b] = OFF_P + b * TILE
-constexpr uint32_t OFF_BAR = 7 * TILE;
-constexpr uint32_t NBAR = 20;
+constexpr uint32_t OFF_K = TILE;                 // K[s] = OFF_K + s * TILE
+constexpr uint32_t OFF_V = (1 + NST) * TILE;     // V[s] = OFF_V + s * TILE
+constexpr uint32_t OFF_BAR = (1 + 2 * NST) * TILE;
+constexpr uint32_t NBAR = 32;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;   // + alignment slack
 constexpr int THREADS = 256;
 
-enum Bar { Q_FULL = 0, Q_FREE = 1, KV_FULL = 2, KV_FREE = 4, S_FULL = 6, S_FREE = 8, P_FULL = 10,
-           P_FREE = 12, O_FULL = 14, O_FREE = 16 };
+enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 5, V_FULL = 8, V_FREE = 11, S_FULL = 14, P_FULL = 16,
+           PV_DONE = 18, O_FULL = 20, O_FREE = 22 };
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -85,6 +87,13 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from TMEM (lane = row, 32-bit column = 2 consecutive bf16 along K)
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // 32 lanes x 32 consecutive fp32 columns: thread t of the warp gets its lane's 32 columns
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -99,6 +108,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
       "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
@@ -175,11 +194,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(KV_FULL + s), 1); mbar_init(bar(KV_FREE + s), 1);
-      mbar_init(bar(S_FULL + s), 1);  mbar_init(bar(S_FREE + s), 128);
-      mbar_init(bar(P_FULL + s), 128); mbar_init(bar(P_FREE + s), 1);
-      mbar_init(bar(O_FULL + s), 1);  mbar_init(bar(O_FREE + s), 128);
+    for (uint32_t s = 0; s < NST; ++s) {
+      mbar_init(bar(K_FULL + s), 1); mbar_init(bar(K_FREE + s), 1);
+      mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(S_FULL + b), 1); mbar_init(bar(P_FULL + b), 128); mbar_init(bar(PV_DONE + b), 1);
+      mbar_init(bar(O_FULL + b), 1); mbar_init(bar(O_FREE + b), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
@@ -195,32 +216,38 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S[0] = [0,128), S[1] = [128,256) (P of a tile overwrites the first 64
+  // columns of its S as packed bf16), O[0] = [256,384), O[1] = [384,512).
 
-  if (warp == 0 && lane == 0) {
-    // ================= TMA producer =================
+  if ((warp == 0 || warp == 3) && lane == 0) {
+    // ================= TMA producers: warp 0 = Q + K tiles, warp 3 = V tiles =================
+    const bool is_k = warp == 0;
+    const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+    const uint32_t full0 = is_k ? K_FULL : V_FULL, free0 = is_k ? K_FREE : V_FREE;
+    const uint32_t ring = sbase + (is_k ? OFF_K : OFF_V);
     uint32_t kt = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
-      if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
-      mbar_expect_tx(bar(Q_FULL), 2 * 128 * g * TQ);
-      const int qrow = (int)(I.r0 + I.mt * TQ);
-      tma_load_3d(sbase + OFF_Q, &tm_q, 0, (int)(I.kh * g), qrow, bar(Q_FULL));
-      tma_load_3d(sbase + OFF_Q + CB, &tm_q, 64, (int)(I.kh * g), qrow, bar(Q_FULL));
+      if (is_k) {
+        if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
+        mbar_expect_tx(bar(Q_FULL), 2 * 128 * g * TQ);
+        const int qrow = (int)(I.r0 + I.mt * TQ);
+        tma_load_3d(sbase + OFF_Q, &tm_q, 0, (int)(I.kh * g), qrow, bar(Q_FULL));
+        tma_load_3d(sbase + OFF_Q + CB, &tm_q, 64, (int)(I.kh * g), qrow, bar(Q_FULL));
+      }
       const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const uint32_t s = kt & 1;
-        if (kt >= 2) mbar_wait(bar(KV_FREE + s), ((kt - 2) >> 1) & 1);
-        mbar_expect_tx(bar(KV_FULL + s), 2 * TILE);
-        const uint32_t ks = sbase + OFF_K + s * 2 * TILE, vs = sbase + OFF_V + s * 2 * TILE;
+        const uint32_t s = kt % NST, u = kt / NST;
+        if (kt >= NST) mbar_wait(bar(free0 + s), (u - 1) & 1);
+        mbar_expect_tx(bar(full0 + s), TILE);
+        const uint32_t dst = ring + s * TILE;
 #pragma unroll 1
         for (uint32_t p = 0; p < 8; ++p) {
           const uint32_t blk = n * 8 + p;
           const int32_t page = blk < I.nblk ? bt[blk] : bt[0];
           const int row = (int)(((uint32_t)page * Hkv + I.kh) * BS);
-          tma_load_2d(ks + p * 2048, &tm_k, 0, row, bar(KV_FULL + s));
-          tma_load_2d(ks + CB + p * 2048, &tm_k, 64, row, bar(KV_FULL + s));
-          tma_load_2d(vs + p * 2048, &tm_v, 0, row, bar(KV_FULL + s));
-          tma_load_2d(vs + CB + p * 2048, &tm_v, 64, row, bar(KV_FULL + s));
+          tma_load_2d(dst + p * 2048, tm, 0, row, bar(full0 + s));
+          tma_load_2d(dst + CB + p * 2048, tm, 64, row, bar(full0 + s));
         }
       }
     }
@@ -235,32 +262,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (it >= 2) mbar_wait(bar(O_FREE + ob), ((it - 2) >> 1) & 1);
       tc_fence_after();
       auto pv = [&](uint32_t tt, bool first) {
-        const uint32_t pb = tt & 1;
-        mbar_wait(bar(P_FULL + pb), (tt >> 1) & 1);
+        const uint32_t b = tt & 1, s = tt % NST;
+        mbar_wait(bar(P_FULL + b), (tt >> 1) & 1);
+        mbar_wait(bar(V_FULL + s), (tt / NST) & 1);
         tc_fence_after();
-        const uint32_t ps = sbase + OFF_P + pb * TILE, vs = sbase + OFF_V + (tt & 1) * 2 * TILE;
+        const uint32_t vs = sbase + OFF_V + s * TILE;
 #pragma unroll
         for (uint32_t k = 0; k < 8; ++k) {
-          const uint64_t a = sdesc(ps + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
-          const uint64_t b = sdesc(vs + k * 2048, CB, 1024);
-          tc_mma(o_tmem, a, b, IDESC_PV, (first && k == 0) ? 0u : 1u);
+          const uint64_t bd = sdesc(vs + k * 2048, CB, 1024);
+          tc_mma_ts(o_tmem, tmem + b * 128 + k * 8, bd, IDESC_PV, (first && k == 0) ? 0u : 1u);
         }
-        tc_commit(bar(P_FREE + pb));
-        tc_commit(bar(KV_FREE + (tt & 1)));
+        tc_commit(bar(PV_DONE + b));
+        tc_commit(bar(V_FREE + s));
       };
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const uint32_t s = kt & 1;
-        mbar_wait(bar(KV_FULL + s), (kt >> 1) & 1);
-        if (kt >= 2) mbar_wait(bar(S_FREE + s), ((kt - 2) >> 1) & 1);
+        const uint32_t s = kt % NST, b = kt & 1;
+        mbar_wait(bar(K_FULL + s), (kt / NST) & 1);
         tc_fence_after();
-        const uint32_t ks = sbase + OFF_K + s * 2 * TILE;
+        const uint32_t ks = sbase + OFF_K + s * TILE;
 #pragma unroll
         for (uint32_t k = 0; k < 8; ++k) {
           const uint64_t a = sdesc(sbase + OFF_Q + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
-          const uint64_t b = sdesc(ks + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
-          tc_mma(tmem + s * 128, a, b, IDESC_QK, k ? 1u : 0u);
+          const uint64_t bd = sdesc(ks + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
+          tc_mma(tmem + b * 128, a, bd, IDESC_QK, k ? 1u : 0u);
         }
-        tc_commit(bar(S_FULL + s));
+        tc_commit(bar(S_FULL + b));
+        tc_commit(bar(K_FREE + s));
         if (n + 1 == I.n_kv) tc_commit(bar(Q_FREE));
         if (n >= 1) pv(kt - 1, n == 1);
       }
@@ -281,25 +308,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t o_tmem = tmem + lane_addr + 256 + ob * 128;
       float m_used = -INFINITY, l = 0.f;
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const uint32_t s = kt & 1;
-        mbar_wait(bar(S_FULL + s), (kt >> 1) & 1);
+        const uint32_t b = kt & 1;
+        const uint32_t s_tmem = tmem + lane_addr + b * 128;
+        mbar_wait(bar(S_FULL + b), (kt >> 1) & 1);
         tc_fence_after();
         float sv[128];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tmem_ld32(tmem + lane_addr + s * 128 + 32 * q, *reinterpret_cast<float(*)[32]>(&sv[32 * q]));
+        for (int q = 0; q < 4; ++q) tmem_ld32(s_tmem + 32 * q, *reinterpret_cast<float(*)[32]>(&sv[32 * q]));
         tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(bar(S_FREE + s));
         const uint32_t key0 = n * BN;
         if (key0 + BN - 1 > pos_q) {
 #pragma unroll
           for (int j = 0; j < 128; ++j)
             if (key0 + j > pos_q) sv[j] = -INFINITY;
         }
-        float mx = sv[0];
+        float mxa[8];
 #pragma unroll
-        for (int j = 1; j < 128; ++j) mx = fmaxf(mx, sv[j]);
+        for (int a = 0; a < 8; ++a) mxa[a] = sv[a];
+#pragma unroll
+        for (int j = 8; j < 128; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], sv[j]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float mx2 = mx * scale_log2;
         bool need = false;
         float factor = 1.f;
@@ -312,8 +341,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           l *= factor;
         }
         if (__any_sync(~0u, need)) {
-          // lazy rescale of this warp's O rows: wait until PV of the previous tile has landed
-          mbar_wait(bar(P_FREE + ((kt - 1) & 1)), ((kt - 1) >> 1) & 1);
+          // lazy rescale of this warp's O rows once PV of the previous tile has landed
+          mbar_wait(bar(PV_DONE + ((kt - 1) & 1)), ((kt - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -327,28 +356,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_wait_st();
         }
         const float negm = -m_used;
-        float rs = 0.f;
+        float rsa[8];
 #pragma unroll
-        for (int j = 0; j < 128; ++j) {
-          sv[j] = ex2(fmaf(sv[j], scale_log2, negm));
-          rs += sv[j];
-        }
-        l += rs;
-        const uint32_t pb = kt & 1;
-        if (kt >= 2) mbar_wait(bar(P_FREE + pb), ((kt - 2) >> 1) & 1);
-        uint8_t* prow = smem + OFF_P + pb * TILE + (r >> 3) * 1024 + (r & 7) * 128;
+        for (int a = 0; a < 8; ++a) rsa[a] = 0.f;
+        uint32_t pk[64];
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
-          uint4 v;
-          v.x = pack_bf16(sv[8 * ch + 0], sv[8 * ch + 1]);
-          v.y = pack_bf16(sv[8 * ch + 2], sv[8 * ch + 3]);
-          v.z = pack_bf16(sv[8 * ch + 4], sv[8 * ch + 5]);
-          v.w = pack_bf16(sv[8 * ch + 6], sv[8 * ch + 7]);
-          *reinterpret_cast<uint4*>(prow + (ch >> 3) * CB + (((ch & 7) ^ (r & 7)) << 4)) = v;
+        for (int j = 0; j < 128; j += 2) {
+          const float p0 = ex2(fmaf(sv[j], scale_log2, negm));
+          const float p1 = ex2(fmaf(sv[j + 1], scale_log2, negm));
+          rsa[(j >> 1) & 7] += p0 + p1;
+          pk[j >> 1] = pack_bf16(p0, p1);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        l += ((rsa[0] + rsa[1]) + (rsa[2] + rsa[3])) + ((rsa[4] + rsa[5]) + (rsa[6] + rsa[7]));
+        // P (bf16) overwrites the first 64 columns of this tile's S in TMEM
+        tmem_st32u(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32u(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(bar(P_FULL + pb));
+        mbar_arrive(bar(P_FULL + b));
       }
       // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
       mbar_wait(bar(O_FULL + ob), (it >> 1) & 1);
