@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int
   uint32_t acc = tid ? s[tid - 1] : 0;
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     c.tile_off[i] = acc;
-    acc += cdiv((uint32_t)(cu_q[i + 1] - cu_q[i]), tq);
+    const uint32_t nt = cdiv((uint32_t)(cu_q[i + 1] - cu_q[i]), tq);
+    for (uint32_t t = 0; t < nt; ++t) c.tile_req[acc + t] = i;
+    acc += nt;
   }
   if (tid == 1023) { c.tile_off[B] = s[1023]; c.sc->n_tiles = s[1023]; }
 }

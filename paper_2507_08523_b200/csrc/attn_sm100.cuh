@@ -14,8 +14,9 @@
 // K and V stream through separate 3-deep smem rings (K is released right after QK, V after
 // PV).  Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer for Q and K,
 // warp 3 = TMA producer for V, warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
-// warps 4-7 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
+// warps 4-11 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
 // tcgen05.commit; tcgen05.mma from one thread execute in order, which orders the reuse of S.
+// Softmax runs on two warpgroups (warps 4-7 and 8-11) that split each tile's key columns.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -34,10 +35,12 @@ constexpr uint32_t NST = 3;              // K and V ring depth (each)
 constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_K = TILE;                 // K[s] = OFF_K + s * TILE
 constexpr uint32_t OFF_V = (1 + NST) * TILE;     // V[s] = OFF_V + s * TILE
-constexpr uint32_t OFF_BAR = (1 + 2 * NST) * TILE;
+constexpr uint32_t OFF_RED = (1 + 2 * NST) * TILE;   // float red[2 tiles][2 WGs][128 rows]
+constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * 128 * 4;
 constexpr uint32_t NBAR = 32;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;   // + alignment slack
-constexpr int THREADS = 256;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
+constexpr int THREADS = 384;
+constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
 enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 5, V_FULL = 8, V_FREE = 11, S_FULL = 14, P_FULL = 16,
            PV_DONE = 18, O_FULL = 20, O_FREE = 22 };
@@ -160,11 +163,7 @@ __device__ __forceinline__ Item decode_item(const Ctx& c, uint32_t B, const int3
   Item it;
   const uint32_t t = w / Hkv;
   it.kh = w % Hkv;
-  uint32_t lo = 0, hi = B;
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (c.tile_off[mid] <= t) lo = mid; else hi = mid;
-  }
+  const uint32_t lo = c.tile_req[t];
   it.i = lo;
   it.mt = t - c.tile_off[lo];
   it.P = (uint32_t)prefix_len[lo];
@@ -177,13 +176,18 @@ __device__ __forceinline__ Item decode_item(const Ctx& c, uint32_t B, const int3
   return it;
 }
 
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
                  const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                  float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023) != 0) __trap();          // swizzle atoms need 1024-byte alignment
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + OFF_BAR;
   auto bar = [&](uint32_t idx) { return bar0 + 8 * idx; };
@@ -199,8 +203,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(S_FULL + b), 1); mbar_init(bar(P_FULL + b), 128); mbar_init(bar(PV_DONE + b), 1);
-      mbar_init(bar(O_FULL + b), 1); mbar_init(bar(O_FREE + b), 128);
+      mbar_init(bar(S_FULL + b), 1); mbar_init(bar(P_FULL + b), SM_THREADS); mbar_init(bar(PV_DONE + b), 1);
+      mbar_init(bar(O_FULL + b), 1); mbar_init(bar(O_FREE + b), SM_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
@@ -219,8 +223,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // TMEM columns: S[0] = [0,128), S[1] = [128,256) (P of a tile overwrites the first 64
   // columns of its S as packed bf16), O[0] = [256,384), O[1] = [384,512).
 
-  if ((warp == 0 || warp == 3) && lane == 0) {
+  if (warp == 0 || warp == 3) {
     // ================= TMA producers: warp 0 = Q + K tiles, warp 3 = V tiles =================
+    // The whole warp fetches the 8 page ids of a KV tile in parallel (one tile ahead); lane 0
+    // issues the TMA boxes.
     const bool is_k = warp == 0;
     const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
     const uint32_t full0 = is_k ? K_FULL : V_FULL, free0 = is_k ? K_FREE : V_FREE;
@@ -228,26 +234,36 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t kt = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
-      if (is_k) {
+      const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
+      auto page_of = [&](uint32_t n) -> int32_t {
+        const uint32_t blk = n * 8 + (lane & 7);
+        return blk < I.nblk ? __ldg(bt + blk) : __ldg(bt);
+      };
+      int32_t nxt = page_of(0);
+      if (is_k && lane == 0) {
         if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
         mbar_expect_tx(bar(Q_FULL), 2 * 128 * g * TQ);
         const int qrow = (int)(I.r0 + I.mt * TQ);
         tma_load_3d(sbase + OFF_Q, &tm_q, 0, (int)(I.kh * g), qrow, bar(Q_FULL));
         tma_load_3d(sbase + OFF_Q + CB, &tm_q, 64, (int)(I.kh * g), qrow, bar(Q_FULL));
       }
-      const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
+        const int32_t cur = nxt;
+        if (n + 1 < I.n_kv) nxt = page_of(n + 1);
         const uint32_t s = kt % NST, u = kt / NST;
-        if (kt >= NST) mbar_wait(bar(free0 + s), (u - 1) & 1);
-        mbar_expect_tx(bar(full0 + s), TILE);
+        if (lane == 0) {
+          if (kt >= NST) mbar_wait(bar(free0 + s), (u - 1) & 1);
+          mbar_expect_tx(bar(full0 + s), TILE);
+        }
         const uint32_t dst = ring + s * TILE;
-#pragma unroll 1
+#pragma unroll
         for (uint32_t p = 0; p < 8; ++p) {
-          const uint32_t blk = n * 8 + p;
-          const int32_t page = blk < I.nblk ? bt[blk] : bt[0];
-          const int row = (int)(((uint32_t)page * Hkv + I.kh) * BS);
-          tma_load_2d(dst + p * 2048, tm, 0, row, bar(full0 + s));
-          tma_load_2d(dst + CB + p * 2048, tm, 64, row, bar(full0 + s));
+          const int32_t page = __shfl_sync(~0u, cur, p);
+          if (lane == 0) {
+            const int row = (int)(((uint32_t)page * Hkv + I.kh) * BS);
+            tma_load_2d(dst + p * 2048, tm, 0, row, bar(full0 + s));
+            tma_load_2d(dst + CB + p * 2048, tm, 64, row, bar(full0 + s));
+          }
         }
       }
     }
@@ -295,9 +311,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_commit(bar(O_FULL + ob));
     }
   } else if (warp >= 4) {
-    // ================= softmax + epilogue (thread = row) =================
-    const uint32_t r = threadIdx.x - 128, q4 = warp - 4;
+    // ================= softmax + epilogue: 2 warpgroups x 128 threads, thread = row =========
+    // WG w owns key columns [64w, 64w+64) of every S tile and O columns [64w, 64w+64); the row
+    // max is combined through shared memory, so both WGs exponentiate against the same max.
+    const uint32_t sm_t = threadIdx.x - 128, wg = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
     const uint32_t lane_addr = (32 * q4) << 16;
+    float* red = reinterpret_cast<float*>(smem + OFF_RED);
     uint32_t kt = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
@@ -305,31 +324,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = (r < g * TQ) && (t < I.ntok);
       const uint32_t pos_q = I.P + I.mt * TQ + min(t, I.ntok - 1);
       const uint32_t ob = it & 1;
-      const uint32_t o_tmem = tmem + lane_addr + 256 + ob * 128;
+      const uint32_t o_tmem = tmem + lane_addr + 256 + ob * 128 + 64 * wg;
       float m_used = -INFINITY, l = 0.f;
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
         const uint32_t b = kt & 1;
         const uint32_t s_tmem = tmem + lane_addr + b * 128;
         mbar_wait(bar(S_FULL + b), (kt >> 1) & 1);
         tc_fence_after();
-        float sv[128];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) tmem_ld32(s_tmem + 32 * q, *reinterpret_cast<float(*)[32]>(&sv[32 * q]));
+        float sv[64];
+        tmem_ld32(s_tmem + 64 * wg, *reinterpret_cast<float(*)[32]>(&sv[0]));
+        tmem_ld32(s_tmem + 64 * wg + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
         tmem_wait_ld();
-        const uint32_t key0 = n * BN;
-        if (key0 + BN - 1 > pos_q) {
+        const uint32_t key0 = n * BN + 64 * wg;
+        if (key0 + 63 > pos_q) {
 #pragma unroll
-          for (int j = 0; j < 128; ++j)
+          for (int j = 0; j < 64; ++j)
             if (key0 + j > pos_q) sv[j] = -INFINITY;
         }
         float mxa[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) mxa[a] = sv[a];
 #pragma unroll
-        for (int j = 8; j < 128; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], sv[j]);
-        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-        const float mx2 = mx * scale_log2;
+        for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], sv[j]);
+        float* rb = red + b * 256;
+        rb[wg * 128 + r] = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                 fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        named_bar_sync(1, SM_THREADS);
+        const float mx2 = fmaxf(rb[r], rb[128 + r]) * scale_log2;
         bool need = false;
         float factor = 1.f;
         if (n == 0) {
@@ -341,11 +362,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           l *= factor;
         }
         if (__any_sync(~0u, need)) {
-          // lazy rescale of this warp's O rows once PV of the previous tile has landed
+          // lazy rescale of this warp's rows of its O half once PV of the previous tile landed
           mbar_wait(bar(PV_DONE + ((kt - 1) & 1)), ((kt - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 2; ++q) {
             float ov[32];
             tmem_ld32(o_tmem + 32 * q, ov);
             tmem_wait_ld();
@@ -356,37 +377,39 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_wait_st();
         }
         const float negm = -m_used;
-        float rsa[8];
+        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) rsa[a] = 0.f;
-        uint32_t pk[64];
-#pragma unroll
-        for (int j = 0; j < 128; j += 2) {
+        for (int j = 0; j < 64; j += 2) {
           const float p0 = ex2(fmaf(sv[j], scale_log2, negm));
           const float p1 = ex2(fmaf(sv[j + 1], scale_log2, negm));
-          rsa[(j >> 1) & 7] += p0 + p1;
+          rsa[(j >> 1) & 3] += p0 + p1;
           pk[j >> 1] = pack_bf16(p0, p1);
         }
-        l += ((rsa[0] + rsa[1]) + (rsa[2] + rsa[3])) + ((rsa[4] + rsa[5]) + (rsa[6] + rsa[7]));
-        // P (bf16) overwrites the first 64 columns of this tile's S in TMEM
-        tmem_st32u(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st32u(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        // P (bf16 pairs) of keys [64wg, 64wg+64) -> TMEM columns [32wg, 32wg+32) of this S
+        tmem_st32u(s_tmem + 32 * wg, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bar(P_FULL + b));
       }
-      // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
+      // epilogue: combine the two row-sum halves, O / l -> bf16, natural-log LSE
+      float* lb = red + ((kt & 1) * 256);              // the buffer the next tile writes last
+      lb[wg * 128 + r] = l;
       mbar_wait(bar(O_FULL + ob), (it >> 1) & 1);
       tc_fence_after();
-      const float inv = 1.f / l;
+      named_bar_sync(1, SM_THREADS);
+      const float lt = lb[r] + lb[128 + r];
+      named_bar_sync(1, SM_THREADS);
+      const float inv = 1.f / lt;
       const size_t orow = ((size_t)(I.r0 + I.mt * TQ + t) * Hq + I.kh * g + hh);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         float ov[32];
         tmem_ld32(o_tmem + 32 * q, ov);
         tmem_wait_ld();
         if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
+          uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 64 * wg + 32 * q);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             uint4 v;
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+      if (valid && lse && wg == 0) lse[orow] = (m_used + __log2f(lt)) * 0.69314718055994531f;
       tc_fence_before();
       mbar_arrive(bar(O_FREE + ob));
     }

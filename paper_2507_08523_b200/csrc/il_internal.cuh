@@ -76,6 +76,7 @@ struct Ctx {
   int32_t *tab_find;         // per request: existing table slot of final_ds or -1
   uint32_t *tab_last;        // per request: last in batch with this key
   uint32_t *tile_off;        // attention work decomposition
+  uint32_t *tile_req;        // attention M-tile -> request
   uint64_t *evicted_list;
   uint32_t *guard_prompt;    // guard: DS_current prompt rows
   // pointers remembered between calls (caller-owned)
