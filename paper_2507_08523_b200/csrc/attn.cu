@@ -217,3 +217,11 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
   c->launches += 2;
   return IL_OK;
 }
+
+#ifdef IL_ATTN_TRACE
+extern "C" il_status il_debug_trace(unsigned long long* out_h) {
+  IL_CUDA(cudaDeviceSynchronize());
+  IL_CUDA(cudaMemcpyFromSymbol(out_h, il::sm100::g_trace, sizeof(il::sm100::g_trace)));
+  return IL_OK;
+}
+#endif

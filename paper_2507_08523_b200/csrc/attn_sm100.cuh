@@ -27,6 +27,15 @@
 namespace il {
 namespace sm100 {
 
+#ifdef IL_ATTN_TRACE
+// debug build only (build.py --trace): per-tile clock64 stamps of each role in CTA 0
+__device__ unsigned long long g_trace[8][4096];
+#define IL_TRACE(slot, idx) \
+  do { if (blockIdx.x == 0 && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
+#else
+#define IL_TRACE(slot, idx) do { } while (0)
+#endif
+
 constexpr uint32_t D = 128;              // head dim handled by this kernel
 constexpr uint32_t BM = 128, BN = 128;   // rows per M-tile, keys per KV tile
 constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
       const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
-      auto page_of = [&](uint32_t n) -> int32_t {
+      auto page_of = [&](uint32_t n) -> int32_t {   // lane's page: lane & 7
         const uint32_t blk = n * 8 + (lane & 7);
         return blk < I.nblk ? __ldg(bt + blk) : __ldg(bt);
       };
@@ -253,17 +262,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t s = kt % NST, u = kt / NST;
         if (lane == 0) {
           if (kt >= NST) mbar_wait(bar(free0 + s), (u - 1) & 1);
+          IL_TRACE(is_k ? 0 : 1, kt);
           mbar_expect_tx(bar(full0 + s), TILE);
         }
         const uint32_t dst = ring + s * TILE;
-#pragma unroll
-        for (uint32_t p = 0; p < 8; ++p) {
-          const int32_t page = __shfl_sync(~0u, cur, p);
-          if (lane == 0) {
-            const int row = (int)(((uint32_t)page * Hkv + I.kh) * BS);
-            tma_load_2d(dst + p * 2048, tm, 0, row, bar(full0 + s));
-            tma_load_2d(dst + CB + p * 2048, tm, 64, row, bar(full0 + s));
-          }
+        __syncwarp();
+        if (lane < 16) {                                 // lane = (page, column half)
+          const uint32_t p = lane & 7, h = lane >> 3;
+          const int row = (int)(((uint32_t)cur * Hkv + I.kh) * BS);
+          tma_load_2d(dst + h * CB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
         }
       }
     }
@@ -281,6 +288,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t b = tt & 1, s = tt % NST;
         mbar_wait(bar(P_FULL + b), (tt >> 1) & 1);
         mbar_wait(bar(V_FULL + s), (tt / NST) & 1);
+        IL_TRACE(3, tt);
         tc_fence_after();
         const uint32_t vs = sbase + OFF_V + s * TILE;
 #pragma unroll
@@ -294,6 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
         const uint32_t s = kt % NST, b = kt & 1;
         mbar_wait(bar(K_FULL + s), (kt / NST) & 1);
+        IL_TRACE(2, kt);
         tc_fence_after();
         const uint32_t ks = sbase + OFF_K + s * TILE;
 #pragma unroll
@@ -330,6 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t b = kt & 1;
         const uint32_t s_tmem = tmem + lane_addr + b * 128;
         mbar_wait(bar(S_FULL + b), (kt >> 1) & 1);
+        if (sm_t == 0) IL_TRACE(4, kt);
         tc_fence_after();
         float sv[64];
         tmem_ld32(s_tmem + 64 * wg, *reinterpret_cast<float(*)[32]>(&sv[0]));
@@ -350,6 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         rb[wg * 128 + r] = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                  fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         named_bar_sync(1, SM_THREADS);
+        if (sm_t == 0) IL_TRACE(5, kt);
         const float mx2 = fmaxf(rb[r], rb[128 + r]) * scale_log2;
         bool need = false;
         float factor = 1.f;
@@ -391,6 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_st32u(s_tmem + 32 * wg, pk);
         tmem_wait_st();
         tc_fence_before();
+        if (r == 0) IL_TRACE(6 + wg, kt);
         mbar_arrive(bar(P_FULL + b));
       }
       // epilogue: combine the two row-sum halves, O / l -> bf16, natural-log LSE
