@@ -48,6 +48,8 @@ static size_t carve(Ctx* c, void* ws) {
   c->rend_off = w.take<uint32_t>(M + 1); c->rend_tok = w.take<uint32_t>(2 * PT + 2 * M);
   c->rend_len = w.take<uint32_t>(M);
   c->instr = w.take<uint32_t>(g.max_prompt_tokens);
+  c->instr_hash = w.take<uint64_t>(g.max_prompt_tokens / 16 + 1);
+  c->instr_pages = w.take<int32_t>(g.max_prompt_tokens / 16 + 1);
   c->tab_ds = w.take<uint32_t>(T * g.k); c->tab_tpl = w.take<uint32_t>(T * g.k);
   c->tab_stamp = w.take<uint64_t>(T);
   c->slot_key = w.take<uint64_t>(NS); c->slot_page = w.take<uint32_t>(NS);
@@ -59,7 +61,7 @@ static size_t carve(Ctx* c, void* ws) {
   c->need_off = w.take<uint32_t>(B + 1);
   c->occ = w.take<uint32_t>(B * MB);
   c->hist = w.take<uint32_t>(4096);
-  c->tab_find = w.take<int32_t>(B); c->tab_last = w.take<uint32_t>(B);
+  c->tab_find = w.take<int32_t>(B); c->tab_last = w.take<uint32_t>(B); c->tab_hash = w.take<uint64_t>(B);
   c->tile_off = w.take<uint32_t>(B + 1);
   c->tile_req = w.take<uint32_t>((size_t)g.max_suffix_tokens / 16 + B + 1);
   c->evicted_list = w.take<uint64_t>(C);
@@ -154,6 +156,24 @@ __global__ void k_pool_copy(Ctx c, uint32_t n, const uint32_t* __restrict__ log_
   for (uint32_t x = t0; x < log_off[n]; x += stride) c.log_tok[x] = log_tok[x];
   for (uint32_t x = t0; x < tpl_off[n]; x += stride) c.tpl_tok[x] = tpl_tok[x];
   for (uint32_t x = t0; x < n_instr; x += stride) c.instr[x] = instr[x];
+}
+
+// chain hashes of the instruction's full blocks (one warp; the same fold as every prompt's
+// first blocks, since every prompt starts with the instruction)
+__global__ void k_instr_hash(Ctx c, uint32_t nI) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t prev = root_hash(c.cfg.hash_seed);
+  for (uint32_t base = 0; base < nI; base += 32) {
+    const uint32_t j = base + lane;
+    uint32_t tok[16];
+    uint64_t content = 0;
+    if (j < nI) content = block_content(c.instr + (size_t)BS * j, tok);
+    const uint32_t nb = min(32u, nI - base);
+    for (uint32_t t = 0; t < nb; ++t) {
+      prev = chain_step(prev, __shfl_sync(~0u, content, t));
+      if (lane == t) c.instr_hash[j] = prev;
+    }
+  }
 }
 
 // exclusive scan of rend_len -> rend_off (one CTA)
@@ -304,9 +324,11 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   k_pool_sets<<<cdiv(n, 8), 256, 0, st>>>(*c, n, log_off, log_tok);
   k_pool_scan<<<1, 1024, 0, st>>>(*c, n);
   k_pool_render<<<cdiv(n * 32, 256), 256, 0, st>>>(*c, n);
+  if (n_instr / BS) k_instr_hash<<<1, 32, 0, st>>>(*c, n_instr / BS);
   IL_LAUNCH_CHECK("pool_load kernels");
   c->n_demos = n;
   c->n_instr = n_instr;
+  c->n_instr_blocks = n_instr / BS;
   c->pool_loaded = true;
   c->refined = c->matched = false;
   c->batch = 0;

@@ -35,7 +35,8 @@ struct DevScalars {
   uint32_t n_new_keys;       // ICL commit scratch
   uint32_t rebuild_flag;
   uint32_t n_tiles;          // attention work items
-  uint32_t pad0[2];
+  uint32_t instr_hits;       // per batch: leading resident (verified) instruction blocks
+  uint32_t pad0;
   uint64_t stamp_min;        // eviction radix-select scratch
   uint64_t stamp_max;
   uint64_t sel_prefix;       // selected key prefix
@@ -49,7 +50,7 @@ struct DevScalars {
 struct Ctx {
   il_config cfg;
   uint32_t max_blocks = 0, n_slots = 0, slot_mask = 0;
-  uint32_t n_demos = 0, n_instr = 0;
+  uint32_t n_demos = 0, n_instr = 0, n_instr_blocks = 0;
   bool pool_loaded = false, refined = false, matched = false;
   uint32_t last_B = 0;
   uint64_t batch = 0;        // b of the last committed batch
@@ -60,8 +61,11 @@ struct Ctx {
   uint32_t *uniq_tok, *uniq_cnt, *uniq_n, *norm2;
   uint32_t *rend_off, *rend_tok, *rend_len;
   uint32_t *instr;
+  uint64_t *instr_hash;       // chain hashes of the instruction's full blocks (pool_load)
+  int32_t *instr_pages;      // per batch: pages of the instruction's leading resident blocks
   // ICL table
-  uint32_t *tab_ds, *tab_tpl;
+  uint32_t *tab_ds;          // [T][k] demo ids
+  uint32_t *tab_tpl;         // [k][T] template ids (SoA: coalesced PMC scans)
   uint64_t* tab_stamp;
   // prefix index + pages
   uint64_t* slot_key;
@@ -75,6 +79,7 @@ struct Ctx {
   uint32_t *need_off, *occ, *hist;
   int32_t *tab_find;         // per request: existing table slot of final_ds or -1
   uint32_t *tab_last;        // per request: last in batch with this key
+  uint64_t *tab_hash;        // per request: hash of the final DS tuple
   uint32_t *tile_off;        // attention work decomposition
   uint32_t *tile_req;        // attention M-tile -> request
   uint64_t *evicted_list;

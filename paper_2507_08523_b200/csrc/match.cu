@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
   const uint64_t st = stamp_of(b_cur, i);
   const uint32_t epoch = (uint32_t)b_cur;
   uint32_t newly = 0;
-  for (uint32_t j = lane; j < h; j += 32) {
+  // instruction blocks are touched once per batch by k_alloc_scan
+  for (uint32_t j = min(c.n_instr_blocks, h) + lane; j < h; j += 32) {
     const uint32_t p = (uint32_t)bt[j];
     atomicMax((unsigned long long*)&c.pg_stamp[p], (unsigned long long)st);
     newly += atomicExch(&c.pg_pin[p], epoch) != epoch;
@@ -42,9 +43,33 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
 // -> need_off, cu_q, prefix_len; how many blocks must be evicted.
 __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
                                                      const uint32_t* __restrict__ hit,
-                                                     int32_t* __restrict__ prefix_len, int32_t* __restrict__ cu_q) {
+                                                     int32_t* __restrict__ prefix_len, int32_t* __restrict__ cu_q,
+                                                     uint64_t b_cur) {
   __shared__ uint32_t s_need[1024], s_suf[1024];
+  __shared__ int32_t s_top[1025];
   const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
+  // Touch + pin the instruction's hit blocks once: block j gets stamp (b, max{i : h_i > j}).
+  const uint32_t nI = min(c.n_instr_blocks, 1024u);
+  for (uint32_t x = tid; x <= nI; x += 1024) s_top[x] = -1;
+  __syncthreads();
+  for (uint32_t i = tid; i < B; i += 1024) atomicMax(&s_top[min(hit[i], nI)], (int32_t)i);
+  __syncthreads();
+  if (tid == 0) {                                       // suffix max: s_top[c] = max over c' >= c
+    for (int x = (int)nI - 1; x >= 0; --x) s_top[x] = max(s_top[x], s_top[x + 1]);
+  }
+  __syncthreads();
+  {
+    uint32_t newly = 0;
+    for (uint32_t j = tid; j < nI; j += 1024) {
+      const int32_t who = s_top[j + 1];                 // max i with min(h_i, nI) > j
+      if (who < 0) continue;
+      const uint32_t p = (uint32_t)c.instr_pages[j];
+      atomicMax((unsigned long long*)&c.pg_stamp[p], (unsigned long long)stamp_of(b_cur, (uint32_t)who));
+      newly += atomicExch(&c.pg_pin[p], (uint32_t)b_cur) != (uint32_t)b_cur;
+    }
+    if (newly) atomicAdd(&c.sc->pinned, newly);
+  }
+  __syncthreads();
   uint32_t n = 0, sfx = 0;
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     const uint32_t L = prompt_len[i], h = hit[i];
@@ -217,8 +242,9 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   cudaStream_t st = (cudaStream_t)s;
   const uint64_t b_cur = c->batch + 1;
   IL_CUDA(cudaMemsetAsync(&c->sc->pinned, 0, 4, st));
+  k_instr_probe<<<1, 256, 0, st>>>(*c);
   if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
-  k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q);
+  k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q, b_cur);
   {
     static int ev_blocks = -1;
     if (ev_blocks < 0) {
@@ -234,7 +260,7 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
   k_alloc_commit<<<1, 1, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_prefix_match");
-  c->launches += B ? 5 : 3;
+  c->launches += B ? 6 : 4;
   c->prompt_tok = prompt_tok;
   c->prompt_len = prompt_len;
   c->block_hash = block_hash;

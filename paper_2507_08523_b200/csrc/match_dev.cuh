@@ -9,6 +9,9 @@ namespace il {
 // base+j (16 independent lane terms, Z17), the serial fold H_j = mix(H_{j-1}*PHI + c_j) is
 // evaluated redundantly by all lanes (content broadcast by shuffle), then the 32 blocks are
 // probed in parallel and a ballot gives the leading run of resident + verified blocks.
+// Every prompt starts with the same instruction, so its nI full blocks are taken from
+// the per-pool hashes (k_instr_hash) and the per-batch probe (k_instr_probe): an exact
+// shortcut, the same keys against the same snapshot.
 // Returns the hit count capped at floor((L-1)/16) (Z20).  Optionally stores every block hash
 // (hash_out[j]) and the pages of the leading run (page_out[j]).  If stop_at_miss, returns as
 // soon as the run ends (the guard only needs the count).
@@ -18,10 +21,18 @@ __device__ __forceinline__ uint32_t warp_hash_match(const Ctx& c, const uint32_t
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t F = L / BS;
   const bool verify = (c.cfg.flags & IL_F_VERIFY) != 0;
-  uint64_t prev = root_hash(c.cfg.hash_seed);
-  uint32_t h = 0;
-  bool run = true;
-  for (uint32_t base = 0; base < F; base += 32) {
+  const uint32_t nI = min(c.n_instr_blocks, F);
+  const uint32_t hI = min(c.sc->instr_hits, nI);
+  if (hash_out)
+    for (uint32_t j = lane; j < nI; j += 32) hash_out[j] = c.instr_hash[j];
+  if (page_out)
+    for (uint32_t j = lane; j < hI; j += 32) page_out[j] = c.instr_pages[j];
+  uint64_t prev = nI ? c.instr_hash[nI - 1] : root_hash(c.cfg.hash_seed);
+  uint32_t h = hI;
+  bool run = hI == nI;
+  const uint32_t cap = L ? (L - 1) / BS : 0;
+  if (!run && stop_at_miss) return min(h, cap);
+  for (uint32_t base = nI; base < F; base += 32) {
     const uint32_t j = base + lane;
     const bool active = j < F;
     uint32_t tok[16];
@@ -59,8 +70,30 @@ __device__ __forceinline__ uint32_t warp_hash_match(const Ctx& c, const uint32_t
     }
     if (!run && stop_at_miss) break;
   }
-  const uint32_t cap = L ? (L - 1) / BS : 0;
   return min(h, cap);
+}
+
+// Once per batch: the leading run of the instruction's blocks resident (and verified) in the
+// index snapshot, and their pages.  One CTA, one thread per block.
+static __global__ void __launch_bounds__(256) k_instr_probe(Ctx c) {
+  __shared__ uint32_t s_first_bad;
+  const uint32_t nI = c.n_instr_blocks;
+  const bool verify = (c.cfg.flags & IL_F_VERIFY) != 0;
+  if (threadIdx.x == 0) s_first_bad = nI;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nI; j += blockDim.x) {
+    const uint64_t H = c.instr_hash[j];
+    const uint32_t page = index_find(c.slot_key, c.slot_page, c.slot_mask, H, nullptr);
+    bool ok = page != NONE32;
+    if (ok && verify) {
+      ok = c.pg_parent[page] == (j ? c.instr_hash[j - 1] : root_hash(c.cfg.hash_seed));
+      for (uint32_t x = 0; x < BS; ++x) ok &= c.pg_tok[(size_t)page * BS + x] == c.instr[BS * j + x];
+    }
+    c.instr_pages[j] = ok ? (int32_t)page : -1;
+    if (!ok) atomicMin(&s_first_bad, j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) c.sc->instr_hits = s_first_bad;
 }
 
 }  // namespace il

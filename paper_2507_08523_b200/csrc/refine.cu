@@ -189,32 +189,41 @@ __device__ __forceinline__ void render_row(const Ctx& c, const uint32_t* ds, uin
   for (uint32_t x = lane; x < qL; x += 32) out[o + x] = q[x];
 }
 
-__global__ void __launch_bounds__(256) k_refine(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
-                                                const uint32_t* __restrict__ q_tok,
-                                                const uint32_t* __restrict__ topk,
-                                                uint32_t* __restrict__ final_ds, il_refine_info* __restrict__ info,
-                                                uint32_t* __restrict__ prompt_tok, uint32_t* __restrict__ prompt_len) {
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= B) return;
+// One CTA (128 threads) per request: threads scan table slots (SoA template rows: coalesced),
+// block argmax of (pmc, stamp), thread 0 applies the rules, all threads render, warp 0 runs
+// the guard's two hash-match passes.
+constexpr int REF_THREADS = 128;
+
+__global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
+                                                        const uint32_t* __restrict__ q_tok,
+                                                        const uint32_t* __restrict__ topk,
+                                                        uint32_t* __restrict__ final_ds, il_refine_info* __restrict__ info,
+                                                        uint32_t* __restrict__ prompt_tok,
+                                                        uint32_t* __restrict__ prompt_len) {
+  __shared__ uint32_t s_cur[MAXK], s_fin[MAXK];
+  __shared__ uint32_t s_bp[REF_THREADS / 32], s_bs[REF_THREADS / 32];
+  __shared__ uint64_t s_bst[REF_THREADS / 32];
+  __shared__ il_refine_info s_inf;
+  __shared__ uint32_t s_L, s_rendered;
+  const uint32_t i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t k = c.cfg.k, T = c.cfg.table_capacity;
-  uint32_t cur[MAXK], tc[MAXK], fin[MAXK];
+  if (tid < k) s_cur[tid] = topk[(size_t)i * k + tid];
+  __syncthreads();
+  uint32_t cur[MAXK], tc[MAXK];
 #pragma unroll
   for (int j = 0; j < MAXK; ++j) {
-    cur[j] = (uint32_t)j < k ? topk[(size_t)i * k + j] : 0;
+    cur[j] = (uint32_t)j < k ? s_cur[j] : 0;
     tc[j] = (uint32_t)j < k ? c.tid[cur[j]] : NONE32;
-    fin[j] = cur[j];
   }
-  il_refine_info inf;
-  inf.target_stamp = 0; inf.target_slot = -1; inf.pmc = 0; inf.rule = 2; inf.reverted = 0; inf.matched = 0;
+  uint32_t bp = 0, bs = NONE32;
+  uint64_t bst = 0;
   if (c.cfg.flags & IL_F_PAIR) {
-    uint32_t bp = 0, bs = NONE32;
-    uint64_t bst = 0;
-    for (uint32_t s = lane; s < T; s += 32) {
+    for (uint32_t s = tid; s < T; s += REF_THREADS) {
       const uint64_t st = c.tab_stamp[s];
       if (st == 0) continue;
       uint32_t used = 0, p = 0;
       for (uint32_t j = 0; j < k; ++j) {
-        const uint32_t t = c.tab_tpl[(size_t)s * k + j];
+        const uint32_t t = c.tab_tpl[(size_t)j * T + s];
         bool found = false;
 #pragma unroll
         for (int q = 0; q < MAXK; ++q) {
@@ -230,39 +239,51 @@ __global__ void __launch_bounds__(256) k_refine(Ctx c, uint32_t B, const uint32_
       const uint64_t ost = __shfl_xor_sync(~0u, bst, o);
       if (op > bp || (op == bp && ost > bst)) { bp = op; bst = ost; bs = os; }
     }
-    if (bp > 0) {
-      inf.pmc = (uint8_t)bp; inf.matched = 1; inf.target_stamp = bst; inf.target_slot = (int32_t)bs;
-      uint32_t tds[MAXK];
-#pragma unroll
-      for (int j = 0; j < MAXK; ++j) tds[j] = (uint32_t)j < k ? c.tab_ds[(size_t)bs * k + j] : 0;
-      if (bp == k) {
-        inf.rule = 1;
-#pragma unroll
-        for (int j = 0; j < MAXK; ++j) fin[j] = tds[j];
-      } else {
-        inf.rule = 3;
-        uint32_t rep = 0, o = 0;
-        for (uint32_t j = 0; j < bp; ++j) {
-          const uint32_t t = c.tid[tds[j]];
-          bool found = false;
-#pragma unroll
-          for (int q = 0; q < MAXK; ++q)
-            if (!found && (uint32_t)q < k && !((rep >> q) & 1u) && tc[q] == t) { rep |= 1u << q; found = true; }
-          if (!found) latch(c.sc, IL_ERR_INTERNAL);          // cannot happen
-#pragma unroll
-          for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == o) fin[q] = tds[j];
-          ++o;
-        }
-#pragma unroll
-        for (int q = 0; q < MAXK; ++q) {
-          if ((uint32_t)q < k && !((rep >> q) & 1u)) {
-#pragma unroll
-            for (int r = 0; r < MAXK; ++r) if ((uint32_t)r == o) fin[r] = cur[q];
-            ++o;
+    if (lane == 0) { s_bp[wid] = bp; s_bs[wid] = bs; s_bst[wid] = bst; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    il_refine_info inf;
+    inf.target_stamp = 0; inf.target_slot = -1; inf.pmc = 0; inf.rule = 2; inf.reverted = 0; inf.matched = 0;
+    uint32_t fin[MAXK];
+    for (uint32_t j = 0; j < k; ++j) fin[j] = cur[j];
+    if (c.cfg.flags & IL_F_PAIR) {
+      bp = 0; bs = NONE32; bst = 0;
+      for (uint32_t q = 0; q < REF_THREADS / 32; ++q)
+        if (s_bp[q] > bp || (s_bp[q] == bp && s_bst[q] > bst)) { bp = s_bp[q]; bst = s_bst[q]; bs = s_bs[q]; }
+      if (bp > 0) {
+        inf.pmc = (uint8_t)bp; inf.matched = 1; inf.target_stamp = bst; inf.target_slot = (int32_t)bs;
+        uint32_t tds[MAXK];
+        for (uint32_t j = 0; j < k; ++j) tds[j] = c.tab_ds[(size_t)bs * k + j];
+        if (bp == k) {
+          inf.rule = 1;
+          for (uint32_t j = 0; j < k; ++j) fin[j] = tds[j];
+        } else {
+          inf.rule = 3;
+          uint32_t rep = 0, o = 0;
+          for (uint32_t j = 0; j < bp; ++j) {
+            const uint32_t t = c.tid[tds[j]];
+            uint32_t q = 0;
+            while (q < k && (((rep >> q) & 1u) || c.tid[cur[q]] != t)) ++q;
+            if (q == k) latch(c.sc, IL_ERR_INTERNAL);             // cannot happen
+            rep |= 1u << q;
+            fin[o++] = tds[j];
           }
+          for (uint32_t q = 0; q < k; ++q)
+            if (!((rep >> q) & 1u)) fin[o++] = cur[q];
         }
       }
     }
+    for (uint32_t j = 0; j < k; ++j) s_fin[j] = fin[j];
+    s_inf = inf;
+  }
+  __syncthreads();
+  uint32_t fin[MAXK];
+  bool changed = false;
+#pragma unroll
+  for (int j = 0; j < MAXK; ++j) {
+    fin[j] = (uint32_t)j < k ? s_fin[j] : 0;
+    changed |= (uint32_t)j < k && fin[j] != cur[j];
   }
   const uint32_t qa = q_off[i], qL = q_off[i + 1] - qa;
   const uint32_t stride = c.cfg.max_prompt_tokens;
@@ -271,45 +292,57 @@ __global__ void __launch_bounds__(256) k_refine(Ctx c, uint32_t B, const uint32_
     for (uint32_t j = 0; j < k; ++j) L += c.rend_len[ds[j]];
     return L;
   };
-  uint32_t L = plen(fin);
   uint32_t* row = prompt_tok + (size_t)i * stride;
-  bool changed = false, rendered = false;
-  for (uint32_t j = 0; j < k; ++j) changed |= fin[j] != cur[j];
+  auto render = [&](const uint32_t* ds, uint32_t* out) {        // all threads of the CTA
+    uint32_t o = c.n_instr;
+    for (uint32_t x = tid; x < c.n_instr; x += REF_THREADS) out[x] = c.instr[x];
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t d = ds[j], a = c.rend_off[d], n = c.rend_len[d];
+      for (uint32_t x = tid; x < n; x += REF_THREADS) out[o + x] = c.rend_tok[a + x];
+      o += n;
+    }
+    for (uint32_t x = tid; x < qL; x += REF_THREADS) out[o + x] = q_tok[qa + x];
+  };
+  uint32_t L = plen(fin);
+  if (tid == 0) { s_L = L; s_rendered = 0; }
   if ((c.cfg.flags & IL_F_GUARD) && changed) {
     // never-worse guard (Z25): compare the capped hits of DS_final and DS_current against
     // the index snapshot; keep DS_current if DS_final is strictly worse.
     const uint32_t Lc = plen(cur);
     uint32_t* grow = c.guard_prompt + (size_t)i * stride;
     if (L <= stride && Lc <= stride) {
-      render_row(c, fin, k, q_tok + qa, qL, row, lane);
-      render_row(c, cur, k, q_tok + qa, qL, grow, lane);
-      __syncwarp();
-      const uint32_t hf = warp_hash_match(c, row, L, nullptr, nullptr, true);
-      const uint32_t hc = warp_hash_match(c, grow, Lc, nullptr, nullptr, true);
-      rendered = true;
-      if (hf < hc) {
-        inf.reverted = 1;
+      render(fin, row);
+      render(cur, grow);
+      __syncthreads();
+      if (wid == 0) {
+        const uint32_t hf = warp_hash_match(c, row, L, nullptr, nullptr, true);
+        const uint32_t hc = warp_hash_match(c, grow, Lc, nullptr, nullptr, true);
+        if (lane == 0) {
+          s_rendered = 1;
+          if (hf < hc) { s_inf.reverted = 1; s_L = Lc; s_rendered = 0; }
+        }
+      }
+      __syncthreads();
+      if (s_inf.reverted) {
 #pragma unroll
         for (int j = 0; j < MAXK; ++j) fin[j] = cur[j];
-        L = Lc;
-        rendered = false;
       }
     }
   }
+  __syncthreads();
+  L = s_L;
   if (L > stride) {
-    if (lane == 0) latch(c.sc, IL_ERR_ARG);
+    if (tid == 0) latch(c.sc, IL_ERR_ARG);
     L = 0;
-  } else if (!rendered) {
-    render_row(c, fin, k, q_tok + qa, qL, row, lane);
+  } else if (!s_rendered) {
+    render(fin, row);
   }
-  if (lane == 0) {
+  if (tid == 0) {
     prompt_len[i] = L;
-    info[i] = inf;
+    info[i] = s_inf;
   }
-  if (lane < k) {
-#pragma unroll
-    for (int j = 0; j < MAXK; ++j) if ((uint32_t)j == lane) final_ds[(size_t)i * k + j] = fin[j];
-  }
+  if (tid == 0)
+    for (uint32_t j = 0; j < k; ++j) final_ds[(size_t)i * k + j] = fin[j];
 }
 
 }  // namespace il
@@ -325,9 +358,10 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   if (B == 0) return IL_OK;
   cudaStream_t st = (cudaStream_t)s;
   k_sim_topk<<<B, SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
-  k_refine<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
+  if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
+  k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
-  c->launches += 2;
+  c->launches += (c->cfg.flags & IL_F_GUARD) ? 3 : 2;
   c->final_ds = final_ds;
   c->info = info;
   c->refined = true;

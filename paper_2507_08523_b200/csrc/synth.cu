@@ -10,35 +10,46 @@
 
 namespace il {
 
-__device__ __forceinline__ __nv_bfloat16 synth_val(uint64_t seed_t, uint32_t tok, uint32_t pos, uint32_t hd, float mul) {
-  const uint64_t u = mix64(mix64(mix64(seed_t ^ (uint64_t)tok) ^ (uint64_t)pos) ^ (uint64_t)hd);
+__device__ __forceinline__ __nv_bfloat16 synth_val(uint64_t row_key, uint32_t hd, float mul) {
+  const uint64_t u = mix64(row_key ^ (uint64_t)hd);
   const float x = (float)((int32_t)(u >> 40) - (1 << 23)) * mul;
   return __float2bfloat16_rn(x);
 }
 
+// One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
+// row and tensor; each element then costs one mix.  Lanes write 8 consecutive bf16 (16 B).
+template <int D>
 __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
                                                const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
                                                uint64_t sq, uint64_t sk, uint64_t sv, float qmul, float kvmul,
                                                __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ kn,
                                                __nv_bfloat16* __restrict__ vn) {
-  const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads, d = c.cfg.head_dim;
+  const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
   const uint32_t total = (uint32_t)cu_q[B];
-  const uint32_t per_row = (Hq + 2 * Hkv) * d;
-  for (uint32_t r = blockIdx.x; r < total; r += gridDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr uint32_t VPH = D / 8;                       // 16-byte vectors per head
+  for (uint32_t r = gw; r < total; r += nw) {
     const uint32_t i = row_owner(cu_q, B, r);
     const uint32_t pos = (uint32_t)prefix_len[i] + r - (uint32_t)cu_q[i];
     const uint32_t tok = prompt_tok[(size_t)i * c.cfg.max_prompt_tokens + pos];
-    for (uint32_t e = threadIdx.x; e < per_row; e += blockDim.x) {
-      const uint32_t h = e / d, x = e % d;
-      if (h < Hq) {
-        q[((size_t)r * Hq + h) * d + x] = synth_val(sq, tok, pos, h * 256 + x, qmul);
-      } else if (h < Hq + Hkv) {
-        const uint32_t hk = h - Hq;
-        kn[((size_t)r * Hkv + hk) * d + x] = synth_val(sk, tok, pos, hk * 256 + x, kvmul);
-      } else {
-        const uint32_t hv = h - Hq - Hkv;
-        vn[((size_t)r * Hkv + hv) * d + x] = synth_val(sv, tok, pos, hv * 256 + x, kvmul);
-      }
+    const uint64_t kq = mix64(mix64(sq ^ (uint64_t)tok) ^ (uint64_t)pos);
+    const uint64_t kk = mix64(mix64(sk ^ (uint64_t)tok) ^ (uint64_t)pos);
+    const uint64_t kv = mix64(mix64(sv ^ (uint64_t)tok) ^ (uint64_t)pos);
+    const uint32_t nvec = (Hq + 2 * Hkv) * VPH;
+    for (uint32_t e = lane; e < nvec; e += 32) {
+      const uint32_t h = e / VPH, x0 = (e % VPH) * 8;
+      uint64_t key;
+      float mul;
+      __nv_bfloat16* dst;
+      uint32_t hh;
+      if (h < Hq) { key = kq; mul = qmul; hh = h; dst = q + ((size_t)r * Hq + h) * D + x0; }
+      else if (h < Hq + Hkv) { key = kk; mul = kvmul; hh = h - Hq; dst = kn + ((size_t)r * Hkv + hh) * D + x0; }
+      else { key = kv; mul = kvmul; hh = h - Hq - Hkv; dst = vn + ((size_t)r * Hkv + hh) * D + x0; }
+      __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = synth_val(key, hh * 256 + x0 + j, mul);
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
     }
   }
 }
@@ -53,10 +64,13 @@ extern "C" il_status il_synth_qkv(il_ctx* c, uint32_t B, const uint32_t* prompt_
   if (B == 0) return IL_OK;
   auto tseed = [&](uint64_t salt) { return mix64((seed << 8) ^ salt); };
   const float unit = 1.0f / 8388608.0f;
-  k_synth<<<c->num_sms * 16, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),
-                                                        tseed(0x4B), tseed(0x56), q_scale * unit, unit,
-                                                        (__nv_bfloat16*)q, (__nv_bfloat16*)k_new,
-                                                        (__nv_bfloat16*)v_new);
+  const uint32_t d = c->cfg.head_dim;
+  if (d == 128)
+    k_synth<128><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),
+        tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (__nv_bfloat16*)v_new);
+  else
+    k_synth<64><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),
+        tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (__nv_bfloat16*)v_new);
   IL_LAUNCH_CHECK("k_synth");
   c->launches += 1;
   return IL_OK;
