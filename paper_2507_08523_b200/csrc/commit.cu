@@ -131,65 +131,55 @@ __global__ void __launch_bounds__(512) k_rebuild(Ctx c) {
 // ---------------------------------------------------------------------------------------
 // ICL Table commit.
 // ---------------------------------------------------------------------------------------
-// k_tab_key: a 64-bit hash of each request's final DS tuple (dedup prefilter; equal hashes
-// are confirmed by comparing the tuples).
+// k_tab_key: each request's final DS tuple -> 64-bit hash -> slot of a per-batch dedup table
+// (lock-free CAS insert), and dd_max[slot] = 1 + the last admission index presenting it.
 __global__ void k_tab_key(Ctx c, uint32_t B) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
   uint64_t h = 0x5851F42D4C957F2Dull;
   for (uint32_t j = 0; j < c.cfg.k; ++j) h = mix64(h ^ ((uint64_t)c.final_ds[(size_t)i * c.cfg.k + j] + PHI64 * (j + 1)));
-  c.tab_hash[i] = h;
+  h |= 1ull;                                           // never the EMPTY key 0
+  uint32_t s = (uint32_t)(h ^ (h >> 32)) & c.dd_mask;
+  while (true) {
+    const uint64_t old = atomicCAS((unsigned long long*)&c.dd_key[s], 0ull, (unsigned long long)h);
+    if (old == 0 || old == h) break;
+    s = (s + 1) & c.dd_mask;
+  }
+  c.tab_slot[i] = s;
+  atomicMax(&c.dd_max[s], i + 1);
 }
 
-// k_tab_find: per request, the slot already holding its final DS (or -1) and whether it is
-// the last request of the batch presenting that key.  Where the key can already be in the
-// table follows from the rules: a rule-1 final DS IS the target's key (its slot is known);
-// a rule-2/3 final DS cannot be in the snapshot table, since an entry with the same template
-// multiset would have PMC = k and the request would be rule 1; only a guard-reverted request
-// (final = DS_current, possibly an existing entry) needs a table scan.
-constexpr int TF_THREADS = 128;
-__global__ void __launch_bounds__(TF_THREADS) k_tab_find(Ctx c, uint32_t B) {
-  extern __shared__ uint64_t s_h[];                   // [B] tuple hashes
-  __shared__ uint32_t s_scan[TF_THREADS];
-  __shared__ int32_t s_found[TF_THREADS];
-  __shared__ uint32_t s_nscan;
-  const uint32_t tid = threadIdx.x, i = blockIdx.x * TF_THREADS + tid, k = c.cfg.k;
-  for (uint32_t x = tid; x < B; x += TF_THREADS) s_h[x] = c.tab_hash[x];
-  if (tid == 0) s_nscan = 0;
-  __syncthreads();
+// k_tab_find: one warp per request: whether it is the last request of the batch presenting its
+// final DS (confirmed by comparing tuples: a 64-bit hash collision latches IL_ERR_INTERNAL
+// instead of merging two keys), and the slot already holding the key in the table (or -1).
+// Where the key can already be in the table follows from the rules: a rule-1 final DS IS the
+// target's key (its slot is known); a rule-2/3 final DS cannot be in the snapshot table, since
+// an entry with the same template multiset would have PMC = k and the request would be rule 1;
+// only a guard-reverted request (final = DS_current, possibly an existing entry) needs a scan.
+__global__ void __launch_bounds__(256) k_tab_find(Ctx c, uint32_t B) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t k = c.cfg.k;
+  const uint32_t rep = c.dd_max[c.tab_slot[i]] - 1;
+  if (lane == 0 && rep != i) {
+    bool eq = true;
+    for (uint32_t q = 0; q < k; ++q) eq &= c.final_ds[(size_t)rep * k + q] == c.final_ds[(size_t)i * k + q];
+    if (!eq) latch(c.sc, IL_ERR_INTERNAL);
+  }
+  const il_refine_info inf = c.info[i];
   int32_t found = -1;
-  bool last = true;
-  if (i < B) {
-    const il_refine_info inf = c.info[i];
-    if (inf.rule == 1 && !inf.reverted) found = inf.target_slot;
-    if (inf.reverted) s_scan[atomicAdd(&s_nscan, 1u)] = tid;
-    const uint64_t h = s_h[i];
-    for (uint32_t j = i + 1; j < B && last; ++j) {
-      if (s_h[j] != h) continue;
+  if (inf.rule == 1 && !inf.reverted) {
+    found = inf.target_slot;
+  } else if (inf.reverted) {
+    for (uint32_t sl = lane; sl < c.cfg.table_capacity; sl += 32) {
+      if (c.tab_stamp[sl] == 0) continue;
       bool eq = true;
-      for (uint32_t q = 0; q < k; ++q) eq &= c.final_ds[(size_t)j * k + q] == c.final_ds[(size_t)i * k + q];
-      last = !eq;
+      for (uint32_t q = 0; q < k; ++q) eq &= c.tab_ds[(size_t)sl * k + q] == c.final_ds[(size_t)i * k + q];
+      if (eq) found = (int32_t)sl;
     }
+    for (int o = 16; o; o >>= 1) found = max(found, __shfl_xor_sync(~0u, found, o));
   }
-  s_found[tid] = found;
-  __syncthreads();
-  // rare: warp 0 scans the table for each guard-reverted request of this CTA
-  if (tid < 32) {
-    for (uint32_t a = 0; a < s_nscan; ++a) {
-      const uint32_t r = s_scan[a], ir = blockIdx.x * TF_THREADS + r;
-      int32_t f = -1;
-      for (uint32_t sl = tid; sl < c.cfg.table_capacity; sl += 32) {
-        if (c.tab_stamp[sl] == 0) continue;
-        bool eq = true;
-        for (uint32_t q = 0; q < k; ++q) eq &= c.tab_ds[(size_t)sl * k + q] == c.final_ds[(size_t)ir * k + q];
-        if (eq) f = (int32_t)sl;
-      }
-      for (int o = 16; o; o >>= 1) f = max(f, __shfl_xor_sync(~0u, f, o));
-      if (tid == 0) s_found[r] = f;
-    }
-  }
-  __syncthreads();
-  if (i < B) { c.tab_find[i] = s_found[tid]; c.tab_last[i] = last; }
+  if (lane == 0) { c.tab_find[i] = found; c.tab_last[i] = rep == i; }
 }
 
 // block-wide exclusive scan of one value per thread (1024 threads)
@@ -358,6 +348,11 @@ __global__ void __launch_bounds__(1024) k_tab_commit(Ctx c, uint32_t B, uint64_t
     }
   }
   if (tid == 0) c.sc->table_entries = min(total, T);
+  for (uint32_t i = tid; i < B; i += 1024) {          // leave the dedup table empty
+    const uint32_t sl = c.tab_slot[i];
+    c.dd_key[sl] = 0;
+    c.dd_max[sl] = 0;
+  }
 }
 
 }  // namespace il
@@ -390,14 +385,7 @@ extern "C" il_status il_commit(il_ctx* c, il_stream s) {
   }
   if (pair && B) {
     k_tab_key<<<cdiv(B, 256), 256, 0, st>>>(*c, B);
-    {
-      static bool tf_attr = false;
-      if (!tf_attr) {
-        IL_CUDA(cudaFuncSetAttribute(k_tab_find, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
-        tf_attr = true;
-      }
-    }
-    k_tab_find<<<cdiv(B, TF_THREADS), TF_THREADS, (size_t)B * 8, st>>>(*c, B);
+    k_tab_find<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B);
     const size_t smem = (size_t)c->cfg.table_capacity * 8;
     static bool attr = false;
     if (!attr) {

@@ -62,6 +62,13 @@ static size_t carve(Ctx* c, void* ws) {
   c->occ = w.take<uint32_t>(B * MB);
   c->hist = w.take<uint32_t>(4096);
   c->tab_find = w.take<int32_t>(B); c->tab_last = w.take<uint32_t>(B); c->tab_hash = w.take<uint64_t>(B);
+  c->tab_slot = w.take<uint32_t>(B);
+  {
+    uint32_t n = 64;
+    while (n < 2 * B) n <<= 1;
+    c->dd_mask = n - 1;
+    c->dd_key = w.take<uint64_t>(n); c->dd_max = w.take<uint32_t>(n);
+  }
   c->tile_off = w.take<uint32_t>(B + 1);
   c->tile_req = w.take<uint32_t>((size_t)g.max_suffix_tokens / 16 + B + 1);
   c->evicted_list = w.take<uint64_t>(C);
@@ -97,6 +104,7 @@ __global__ void k_reset_index(Ctx c) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < c.cfg.table_capacity; t += stride)
     c.tab_stamp[t] = 0;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4096; t += stride) c.hist[t] = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.dd_mask; t += stride) { c.dd_key[t] = 0; c.dd_max[t] = 0; }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevScalars z;
     memset(&z, 0, sizeof(z));

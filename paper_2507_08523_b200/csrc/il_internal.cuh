@@ -80,6 +80,10 @@ struct Ctx {
   int32_t *tab_find;         // per request: existing table slot of final_ds or -1
   uint32_t *tab_last;        // per request: last in batch with this key
   uint64_t *tab_hash;        // per request: hash of the final DS tuple
+  uint32_t *tab_slot;        // per request: its slot in the dedup table
+  uint64_t *dd_key;          // per-batch dedup table of final-DS hashes (cleared after use)
+  uint32_t *dd_max;          // 1 + last admission index presenting the key
+  uint32_t dd_mask = 0;
   uint32_t *tile_off;        // attention work decomposition
   uint32_t *tile_req;        // attention M-tile -> request
   uint64_t *evicted_list;
