@@ -222,6 +222,7 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
 extern "C" il_status il_debug_trace(unsigned long long* out_h) {
   IL_CUDA(cudaDeviceSynchronize());
   IL_CUDA(cudaMemcpyFromSymbol(out_h, il::sm100::g_trace, sizeof(il::sm100::g_trace)));
+  IL_CUDA(cudaMemcpyFromSymbol(out_h + 8 * 4096, il::sm100::g_trace_item, sizeof(il::sm100::g_trace_item)));
   return IL_OK;
 }
 #endif

@@ -2,17 +2,18 @@
 //
 // One work item = (request i, kv head kh, M-tile of TQ = 128/g suffix tokens).  The g q-heads
 // sharing kv head kh are packed as rows (row = token * g + head) so one 128-row tcgen05 tile
-// covers TQ tokens x g heads (GQA packing).  KV tiles are 128 keys = 8 pages of 16 tokens,
+// covers TQ tokens x g heads (GQA packing).  KV tiles are 64 keys = 4 pages of 16 tokens,
 // each page a [16][128] bf16 block of the caller's [C][Hkv][16][d] cache, fetched by TMA
 // (two 64-column boxes per page, 128-byte swizzle).  Per KV tile:
 //   S = Q K^T      tcgen05.mma kind::f16, A = Q (smem, K-major), B = K tile (smem, K-major),
 //                  D in TMEM (fp32, 128 lanes x 128 columns, double buffered)
-//   softmax        4 warps, one TMEM lane (= one row) per thread: causal mask, running max with
+//   softmax        one warpgroup per Q tile, one TMEM lane (= one row) per thread: causal mask, running max with
 //                  a lazy rescale (O is rescaled in TMEM only when the max grows by > 2^8), exp2,
 //                  P written back as packed bf16 over the first 64 columns of its S in TMEM
 //   O += P V       A = P (TMEM), B = V tile (smem, MN-major), D = O in TMEM
-// K and V stream through separate 3-deep smem rings (K is released right after QK, V after
-// PV).  Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer for Q and K,
+// K and V stream through separate smem rings (K is released right after QK, V after its
+// last PV).  Two M-tiles share each CTA (see "work decomposition"): a KV tile both need is
+// loaded once, and their softmax warpgroups ping-pong against one tensor core.  Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer for Q and K,
 // warp 3 = TMA producer for V, warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
 // warps 4-11 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
 // tcgen05.commit; tcgen05.mma from one thread execute in order, which orders the reuse of S.
@@ -30,6 +31,7 @@ namespace sm100 {
 #ifdef IL_ATTN_TRACE
 // debug build only (build.py --trace): per-tile clock64 stamps of each role in CTA 0
 __device__ unsigned long long g_trace[8][4096];
+__device__ unsigned int g_trace_item[1024][4];
 #define IL_TRACE(slot, idx) \
   do { if (blockIdx.x == 0 && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
 #else
@@ -37,22 +39,25 @@ __device__ unsigned long long g_trace[8][4096];
 #endif
 
 constexpr uint32_t D = 128;              // head dim handled by this kernel
-constexpr uint32_t BM = 128, BN = 128;   // rows per M-tile, keys per KV tile
-constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
-constexpr uint32_t TILE = 2 * CB;        // 128 x 128 bf16 = 32 KB
-constexpr uint32_t NST = 3;              // K and V ring depth (each)
-constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_K = TILE;                 // K[s] = OFF_K + s * TILE
-constexpr uint32_t OFF_V = (1 + NST) * TILE;     // V[s] = OFF_V + s * TILE
-constexpr uint32_t OFF_RED = (1 + 2 * NST) * TILE;   // float red[2 tiles][2 WGs][128 rows]
-constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * 128 * 4;
-constexpr uint32_t NBAR = 32;
+constexpr uint32_t BM = 128;             // rows per M-tile
+constexpr uint32_t BN = 64;              // keys per KV tile (= 4 pages) = one softmax step
+constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile (Q)
+constexpr uint32_t QTILE = 2 * CB;       // 128 x 128 bf16 = 32 KB
+constexpr uint32_t KCB = 8192;           // one 64-column block of a 64-key K/V tile
+constexpr uint32_t KVTILE = 2 * KCB;     // 64 x 128 bf16 = 16 KB
+constexpr uint32_t NSTK = 4, NSTV = 6;   // K and V ring depths
+constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
+constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
+constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
+constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
+constexpr uint32_t NBAR = 34;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int THREADS = 384;
 constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
-enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 5, V_FULL = 8, V_FREE = 11, S_FULL = 14, P_FULL = 16,
-           PV_DONE = 18, O_FULL = 20, O_FREE = 22 };
+// S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
+enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 6, V_FULL = 10, V_FREE = 16, S_FULL = 22, P_FULL = 26,
+           PV_DONE = 30, O_FULL = 32, O_FREE = 33 };
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -160,29 +165,64 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 // instruction descriptor kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // A major [15] (0 = K), B major [16] (1 = MN), N >> 3 [17,23), M >> 4 [24,29)
-constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
-constexpr uint32_t IDESC_PV = IDESC_QK | (1u << 16);
+constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((BM >> 4) << 24);  // N = 64 keys
+constexpr uint32_t IDESC_PV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((D >> 3) << 17) | ((BM >> 4) << 24);
 
-struct Item {
-  uint32_t i, kh, mt, P, S, r0, ntok, n_kv, nblk;
+// ------------------------------------------------------------------ work decomposition
+// M-tile t = (request i, tile mt of TQ tokens).  A work item is a PAIR of consecutive M-tiles
+// (A = 2u, B = 2u+1) with one kv head.  Their KV tile sequences usually start with the same
+// pages (the instruction and often the demonstrations, P:182 / PAIR rule 1), counted by nsh
+// (k_pair_scan); a shared KV tile is loaded once and feeds both Q tiles.
+struct Tile {
+  uint32_t i, mt, P, S, r0, ntok, n_kv, nblk;
+  bool valid;
 };
-__device__ __forceinline__ Item decode_item(const Ctx& c, uint32_t B, const int32_t* __restrict__ cu_q,
+__device__ __forceinline__ Tile decode_tile(const Ctx& c, const int32_t* __restrict__ cu_q,
+                                            const int32_t* __restrict__ prefix_len, uint32_t t, uint32_t TQ) {
+  Tile T;
+  T.valid = t < c.sc->n_tiles;
+  if (!T.valid) { T.i = T.mt = T.P = T.S = T.r0 = T.ntok = T.n_kv = T.nblk = 0; return T; }
+  const uint32_t i = c.tile_req[t];
+  T.i = i;
+  T.mt = t - c.tile_off[i];
+  T.P = (uint32_t)prefix_len[i];
+  T.r0 = (uint32_t)cu_q[i];
+  T.S = (uint32_t)cu_q[i + 1] - T.r0;
+  T.ntok = min(TQ, T.S - T.mt * TQ);
+  T.n_kv = (T.P + T.mt * TQ + T.ntok - 1) / BN + 1;
+  T.nblk = cdiv(T.P + T.S, BS);
+  return T;
+}
+struct Pair {
+  Tile a, b;
+  uint32_t kh, nsh, nload;
+};
+__device__ __forceinline__ Pair decode_pair(const Ctx& c, const int32_t* __restrict__ cu_q,
                                             const int32_t* __restrict__ prefix_len, uint32_t w, uint32_t Hkv,
                                             uint32_t TQ) {
-  Item it;
-  const uint32_t t = w / Hkv;
-  it.kh = w % Hkv;
-  const uint32_t lo = c.tile_req[t];
-  it.i = lo;
-  it.mt = t - c.tile_off[lo];
-  it.P = (uint32_t)prefix_len[lo];
-  it.r0 = (uint32_t)cu_q[lo];
-  it.S = (uint32_t)cu_q[lo + 1] - it.r0;
-  it.ntok = min(TQ, it.S - it.mt * TQ);
-  const uint32_t p_last = it.P + it.mt * TQ + it.ntok - 1;
-  it.n_kv = p_last / BN + 1;
-  it.nblk = cdiv(it.P + it.S, BS);
-  return it;
+  Pair p;
+  const uint32_t u = w / Hkv;
+  p.kh = w % Hkv;
+  p.a = decode_tile(c, cu_q, prefix_len, 2 * u, TQ);
+  p.b = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ);
+  p.nsh = p.b.valid ? c.pair_nsh[u] : 0;
+  p.nload = p.a.n_kv + (p.b.valid ? p.b.n_kv - p.nsh : 0);
+  return p;
+}
+// Load order: the nsh shared tiles (targets A and B), then the rest of A and of B interleaved
+// (A, B, A, B, ...), then the longer remainder.  Returns the KV tile index, the request whose
+// pages it reads, and the target mask (bit 0 = A, bit 1 = B).
+__device__ __forceinline__ void load_info(const Pair& p, uint32_t l, uint32_t& n, uint32_t& req, uint32_t& tgt) {
+  if (l < p.nsh) { n = l; req = p.a.i; tgt = 3; return; }
+  const uint32_t ra = p.a.n_kv - p.nsh, rb = p.b.valid ? p.b.n_kv - p.nsh : 0;
+  const uint32_t x = l - p.nsh, m = min(ra, rb);
+  if (x < 2 * m) {
+    const uint32_t j = x >> 1;
+    if ((x & 1) == 0) { n = p.nsh + j; req = p.a.i; tgt = 1; } else { n = p.nsh + j; req = p.b.i; tgt = 2; }
+    return;
+  }
+  const uint32_t j = m + (x - 2 * m);
+  if (ra > rb) { n = p.nsh + j; req = p.a.i; tgt = 1; } else { n = p.nsh + j; req = p.b.i; tgt = 2; }
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
@@ -203,18 +243,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
-  const uint32_t n_items = c.sc->n_tiles * Hkv;
+  const uint32_t n_items = cdiv(c.sc->n_tiles, 2) * Hkv;
 
   if (threadIdx.x == 0) {
     mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
-    for (uint32_t s = 0; s < NST; ++s) {
-      mbar_init(bar(K_FULL + s), 1); mbar_init(bar(K_FREE + s), 1);
-      mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(S_FULL + b), 1); mbar_init(bar(P_FULL + b), SM_THREADS); mbar_init(bar(PV_DONE + b), 1);
-      mbar_init(bar(O_FULL + b), 1); mbar_init(bar(O_FREE + b), SM_THREADS);
-    }
+    for (uint32_t s = 0; s < NSTK; ++s) { mbar_init(bar(K_FULL + s), 1); mbar_init(bar(K_FREE + s), 1); }
+    static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
+    for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
+    for (int x = 0; x < 4; ++x) { mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), 128); }
+    for (int x = 0; x < 2; ++x) mbar_init(bar(PV_DONE + x), 1);
+    mbar_init(bar(O_FULL), 1); mbar_init(bar(O_FREE), SM_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_k) : "memory");
@@ -229,139 +267,173 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S[0] = [0,128), S[1] = [128,256) (P of a tile overwrites the first 64
-  // columns of its S as packed bf16), O[0] = [256,384), O[1] = [384,512).
+  // TMEM columns: Q tile x owns S/P columns [128x, 128x+128) as two 64-key sub-tile buffers
+  // h (columns 128x + 64h ..): the P of a sub-tile overwrites the first 32 columns of its S as
+  // packed bf16.  O_A = [256,384), O_B = [384,512).
 
   if (warp == 0 || warp == 3) {
-    // ================= TMA producers: warp 0 = Q + K tiles, warp 3 = V tiles =================
-    // The whole warp fetches the 8 page ids of a KV tile in parallel (one tile ahead); lane 0
-    // issues the TMA boxes.
+    // ============ TMA producers: warp 0 = Q tiles + K tiles, warp 3 = V tiles ============
     const bool is_k = warp == 0;
     const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+    const uint32_t nst = is_k ? NSTK : NSTV;
     const uint32_t full0 = is_k ? K_FULL : V_FULL, free0 = is_k ? K_FREE : V_FREE;
     const uint32_t ring = sbase + (is_k ? OFF_K : OFF_V);
-    uint32_t kt = 0, it = 0;
+    uint32_t lc = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
-      const int32_t* bt = block_table + (size_t)I.i * c.max_blocks;
-      auto page_of = [&](uint32_t n) -> int32_t {   // lane's page: lane & 7
-        const uint32_t blk = n * 8 + (lane & 7);
-        return blk < I.nblk ? __ldg(bt + blk) : __ldg(bt);
-      };
-      int32_t nxt = page_of(0);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
       if (is_k && lane == 0) {
         if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
-        mbar_expect_tx(bar(Q_FULL), 2 * 128 * g * TQ);
-        const int qrow = (int)(I.r0 + I.mt * TQ);
-        tma_load_3d(sbase + OFF_Q, &tm_q, 0, (int)(I.kh * g), qrow, bar(Q_FULL));
-        tma_load_3d(sbase + OFF_Q + CB, &tm_q, 64, (int)(I.kh * g), qrow, bar(Q_FULL));
-      }
-      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const int32_t cur = nxt;
-        if (n + 1 < I.n_kv) nxt = page_of(n + 1);
-        const uint32_t s = kt % NST, u = kt / NST;
-        if (lane == 0) {
-          if (kt >= NST) mbar_wait(bar(free0 + s), (u - 1) & 1);
-          IL_TRACE(is_k ? 0 : 1, kt);
-          mbar_expect_tx(bar(full0 + s), TILE);
+        const uint32_t qbytes = 2 * 128 * g * TQ;
+        mbar_expect_tx(bar(Q_FULL), pr.b.valid ? 2 * qbytes : qbytes);
+        const int ra = (int)(pr.a.r0 + pr.a.mt * TQ);
+        tma_load_3d(sbase + OFF_QA, &tm_q, 0, (int)(pr.kh * g), ra, bar(Q_FULL));
+        tma_load_3d(sbase + OFF_QA + CB, &tm_q, 64, (int)(pr.kh * g), ra, bar(Q_FULL));
+        if (pr.b.valid) {
+          const int rb = (int)(pr.b.r0 + pr.b.mt * TQ);
+          tma_load_3d(sbase + OFF_QB, &tm_q, 0, (int)(pr.kh * g), rb, bar(Q_FULL));
+          tma_load_3d(sbase + OFF_QB + CB, &tm_q, 64, (int)(pr.kh * g), rb, bar(Q_FULL));
         }
-        const uint32_t dst = ring + s * TILE;
+      }
+      for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
+        uint32_t n, req, tgt;
+        load_info(pr, l, n, req, tgt);
+        const uint32_t nblk = req == pr.a.i ? pr.a.nblk : pr.b.nblk;
+        const int32_t* bt = block_table + (size_t)req * c.max_blocks;
+        const uint32_t blk = n * 4 + (lane & 3);
+        const int32_t page = blk < nblk ? __ldg(bt + blk) : __ldg(bt);
+        const uint32_t s = lc % nst, u = lc / nst;
+        if (lane == 0) {
+          if (lc >= nst) mbar_wait(bar(free0 + s), (u - 1) & 1);
+          IL_TRACE(is_k ? 0 : 1, lc & 4095);
+          mbar_expect_tx(bar(full0 + s), KVTILE);
+        }
         __syncwarp();
-        if (lane < 16) {                                 // lane = (page, column half)
-          const uint32_t p = lane & 7, h = lane >> 3;
-          const int row = (int)(((uint32_t)cur * Hkv + I.kh) * BS);
-          tma_load_2d(dst + h * CB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
+        if (lane < 8) {                                  // lane = (page, column half)
+          const uint32_t p = lane & 3, h = lane >> 2;
+          const int row = (int)(((uint32_t)page * Hkv + pr.kh) * BS);
+          tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
         }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ================= MMA issuer (single thread) =================
-    uint32_t kt = 0, it = 0;
+    // Per Q tile x the 64-key sub-tiles n = 0, 1, 2, ... alternate TMEM buffers n & 1; QK of
+    // sub-tile n+2 reuses the buffer of n, so it is issued right after PV(n) (tcgen05 ops from
+    // one thread execute in order).  The two Q tiles' chains interleave on the tensor pipe.
+    uint32_t lc = 0, it = 0, cnt[2] = {0, 0};        // load counter, per-Q-tile sub-tile counters
+    uint32_t vusers[8] = {0, 0, 0, 0, 0, 0, 0, 0};    // PVs still to read V of load lc (by lc % 8)
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
-      const uint32_t ob = it & 1;
-      const uint32_t o_tmem = tmem + 256 + ob * 128;
-      mbar_wait(bar(Q_FULL), it & 1);
-      if (it >= 2) mbar_wait(bar(O_FREE + ob), ((it - 2) >> 1) & 1);
-      tc_fence_after();
-      auto pv = [&](uint32_t tt, bool first) {
-        const uint32_t b = tt & 1, s = tt % NST;
-        mbar_wait(bar(P_FULL + b), (tt >> 1) & 1);
-        mbar_wait(bar(V_FULL + s), (tt / NST) & 1);
-        IL_TRACE(3, tt);
-        tc_fence_after();
-        const uint32_t vs = sbase + OFF_V + s * TILE;
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-          const uint64_t bd = sdesc(vs + k * 2048, CB, 1024);
-          tc_mma_ts(o_tmem, tmem + b * 128 + k * 8, bd, IDESC_PV, (first && k == 0) ? 0u : 1u);
-        }
-        tc_commit(bar(PV_DONE + b));
-        tc_commit(bar(V_FREE + s));
-      };
-      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const uint32_t s = kt % NST, b = kt & 1;
-        mbar_wait(bar(K_FULL + s), (kt / NST) & 1);
-        IL_TRACE(2, kt);
-        tc_fence_after();
-        const uint32_t ks = sbase + OFF_K + s * TILE;
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-          const uint64_t a = sdesc(sbase + OFF_Q + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc(ks + (k >> 2) * CB + (k & 3) * 32, 16, 1024);
-          tc_mma(tmem + b * 128, a, bd, IDESC_QK, k ? 1u : 0u);
-        }
-        tc_commit(bar(S_FULL + b));
-        tc_commit(bar(K_FREE + s));
-        if (n + 1 == I.n_kv) tc_commit(bar(Q_FREE));
-        if (n >= 1) pv(kt - 1, n == 1);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
+      uint32_t last[2] = {0, 0};
+      for (uint32_t l = 0; l < pr.nload; ++l) {
+        uint32_t n_, r_, t_;
+        load_info(pr, l, n_, r_, t_);
+        if (t_ & 1u) last[0] = l;
+        if (t_ & 2u) last[1] = l;
       }
-      pv(kt - 1, I.n_kv == 1);
-      tc_commit(bar(O_FULL + ob));
+      mbar_wait(bar(Q_FULL), it & 1);
+#ifdef IL_ATTN_TRACE
+      if (blockIdx.x == 0 && it < 1024) {
+        g_trace_item[it][0] = lc; g_trace_item[it][1] = pr.nload; g_trace_item[it][2] = pr.nsh;
+        g_trace_item[it][3] = pr.a.n_kv | (pr.b.n_kv << 16);
+      }
+#endif
+      tc_fence_after();
+      // pending PVs per Q tile: up to two tiles (ring), each = (load counter, tile count)
+      uint32_t pq_l[2][2], pq_c[2][2], pq_n[2] = {0, 0}, pq_head[2] = {0, 0};
+      bool first[2] = {true, true}, o_ready = it == 0;
+      auto pv_one = [&](uint32_t x) {                  // issue the oldest pending PV of Q tile x
+        const uint32_t slot = pq_head[x];
+        const uint32_t pl = pq_l[x][slot], pc = pq_c[x][slot], vs = pl % NSTV;
+        if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
+        mbar_wait(bar(P_FULL + 2 * x + (pc & 1)), (pc >> 1) & 1);
+        mbar_wait(bar(V_FULL + vs), (pl / NSTV) & 1);
+        IL_TRACE(3, (2 * pl + x) & 4095);
+        tc_fence_after();
+        const uint32_t vaddr = sbase + OFF_V + vs * KVTILE;
+        const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x + 64 * (pc & 1);
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k)
+          tc_mma_ts(o_tmem, p_tmem + k * 8, sdesc(vaddr + k * 2048, KCB, 1024), IDESC_PV, (first[x] && k == 0) ? 0u : 1u);
+        first[x] = false;
+        tc_commit(bar(PV_DONE + x));
+        if (--vusers[pl & 7] == 0) tc_commit(bar(V_FREE + vs));
+        pq_head[x] ^= 1;
+        --pq_n[x];
+      };
+      for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
+        uint32_t n, req, tgt;
+        load_info(pr, l, n, req, tgt);
+#pragma unroll
+        for (uint32_t x = 0; x < 2; ++x)               // a Q tile whose loads ended drains its PVs
+          if (last[x] < l) while (pq_n[x]) pv_one(x);
+        const uint32_t ks = lc % NSTK;
+        mbar_wait(bar(K_FULL + ks), (lc / NSTK) & 1);
+        IL_TRACE(2, lc & 4095);
+        tc_fence_after();
+        vusers[lc & 7] = (tgt == 3) ? 2u : 1u;
+        const uint32_t kaddr = sbase + OFF_K + ks * KVTILE;
+#pragma unroll
+        for (uint32_t x = 0; x < 2; ++x) {
+          if (!((tgt >> x) & 1u)) continue;
+          if (pq_n[x] == 2) pv_one(x);                 // frees the TMEM buffer this QK overwrites
+          const uint32_t qaddr = sbase + (x ? OFF_QB : OFF_QA);
+          const uint32_t sc = cnt[x]++;
+          const uint32_t s_tmem = tmem + 128 * x + 64 * (sc & 1);
+#pragma unroll
+          for (uint32_t k = 0; k < 8; ++k)
+            tc_mma(s_tmem, sdesc(qaddr + (k >> 2) * CB + (k & 3) * 32, 16, 1024),
+                   sdesc(kaddr + (k >> 2) * KCB + (k & 3) * 32, 16, 1024), IDESC_QK, k ? 1u : 0u);
+          tc_commit(bar(S_FULL + 2 * x + (sc & 1)));
+          const uint32_t slot = (pq_head[x] + pq_n[x]) & 1;
+          pq_l[x][slot] = lc; pq_c[x][slot] = sc;
+          ++pq_n[x];
+        }
+        tc_commit(bar(K_FREE + ks));
+        if (l + 1 == pr.nload) tc_commit(bar(Q_FREE));
+      }
+      while (pq_n[0]) pv_one(0);
+      while (pq_n[1]) pv_one(1);
+      if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
+      tc_commit(bar(O_FULL));
     }
   } else if (warp >= 4) {
-    // ================= softmax + epilogue: 2 warpgroups x 128 threads, thread = row =========
-    // WG w owns key columns [64w, 64w+64) of every S tile and O columns [64w, 64w+64); the row
-    // max is combined through shared memory, so both WGs exponentiate against the same max.
-    const uint32_t sm_t = threadIdx.x - 128, wg = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
+    // ====== softmax + epilogue: warpgroup x owns Q tile x (A: warps 4-7, B: warps 8-11) ======
+    const uint32_t sm_t = threadIdx.x - 128, x = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
     const uint32_t lane_addr = (32 * q4) << 16;
-    float* red = reinterpret_cast<float*>(smem + OFF_RED);
-    uint32_t kt = 0, it = 0;
+    const uint32_t s_tmem = tmem + lane_addr + 128 * x, o_tmem = tmem + lane_addr + 256 + 128 * x;
+    uint32_t it = 0, cnt = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Item I = decode_item(c, B, cu_q, prefix_len, w, Hkv, TQ);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
+      const Tile& T = x ? pr.b : pr.a;
       const uint32_t t = r / g, hh = r % g;
-      const bool valid = (r < g * TQ) && (t < I.ntok);
-      const uint32_t pos_q = I.P + I.mt * TQ + min(t, I.ntok - 1);
-      const uint32_t ob = it & 1;
-      const uint32_t o_tmem = tmem + lane_addr + 256 + ob * 128 + 64 * wg;
+      const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
+      const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
       float m_used = -INFINITY, l = 0.f;
-      for (uint32_t n = 0; n < I.n_kv; ++n, ++kt) {
-        const uint32_t b = kt & 1;
-        const uint32_t s_tmem = tmem + lane_addr + b * 128;
-        mbar_wait(bar(S_FULL + b), (kt >> 1) & 1);
-        if (sm_t == 0) IL_TRACE(4, kt);
+      const uint32_t nsub = T.valid ? T.n_kv : 0;      // 64-key KV tiles
+      for (uint32_t n = 0; n < nsub; ++n, ++cnt) {
+        const uint32_t b = cnt & 1;
+        const uint32_t sb_tmem = s_tmem + 64 * b;
+        mbar_wait(bar(S_FULL + 2 * x + b), (cnt >> 1) & 1);
+        if (r == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
         tc_fence_after();
-        float sv[64];
-        tmem_ld32(s_tmem + 64 * wg, *reinterpret_cast<float(*)[32]>(&sv[0]));
-        tmem_ld32(s_tmem + 64 * wg + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
+        const uint32_t key0 = n * BN;
+        float a[64];
+        tmem_ld32(sb_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
+        tmem_ld32(sb_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
         tmem_wait_ld();
-        const uint32_t key0 = n * BN + 64 * wg;
-        if (key0 + 63 > pos_q) {
+        if (key0 + BN - 1 > pos_q) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (key0 + j > pos_q) sv[j] = -INFINITY;
+          for (int j = 0; j < 64; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
         }
         float mxa[8];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) mxa[a] = sv[a];
+        for (int q = 0; q < 8; ++q) mxa[q] = a[q];
 #pragma unroll
-        for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], sv[j]);
-        float* rb = red + b * 256;
-        rb[wg * 128 + r] = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                 fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-        named_bar_sync(1, SM_THREADS);
-        if (sm_t == 0) IL_TRACE(5, kt);
-        const float mx2 = fmaxf(rb[r], rb[128 + r]) * scale_log2;
+        for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float mx2 = mx * scale_log2;
         bool need = false;
         float factor = 1.f;
         if (n == 0) {
@@ -373,11 +445,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           l *= factor;
         }
         if (__any_sync(~0u, need)) {
-          // lazy rescale of this warp's rows of its O half once PV of the previous tile landed
-          mbar_wait(bar(PV_DONE + ((kt - 1) & 1)), ((kt - 1) >> 1) & 1);
+          // lazy rescale of this warp's O rows once the previous sub-tile's PV has landed
+          mbar_wait(bar(PV_DONE + x), (cnt - 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
+          for (int q = 0; q < 4; ++q) {
             float ov[32];
             tmem_ld32(o_tmem + 32 * q, ov);
             tmem_wait_ld();
@@ -392,56 +464,83 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 64; j += 2) {
-          const float p0 = ex2(fmaf(sv[j], scale_log2, negm));
-          const float p1 = ex2(fmaf(sv[j + 1], scale_log2, negm));
+          const float p0 = ex2(fmaf(a[j], scale_log2, negm)), p1 = ex2(fmaf(a[j + 1], scale_log2, negm));
           rsa[(j >> 1) & 3] += p0 + p1;
           pk[j >> 1] = pack_bf16(p0, p1);
         }
         l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
-        // P (bf16 pairs) of keys [64wg, 64wg+64) -> TMEM columns [32wg, 32wg+32) of this S
-        tmem_st32u(s_tmem + 32 * wg, pk);
+        tmem_st32u(sb_tmem, pk);                        // P (bf16 pairs) over this S's first 32 columns
         tmem_wait_st();
         tc_fence_before();
-        if (r == 0) IL_TRACE(6 + wg, kt);
-        mbar_arrive(bar(P_FULL + b));
+        if (r == 0) IL_TRACE(5 + 2 * x, cnt & 4095);
+        mbar_arrive(bar(P_FULL + 2 * x + b));
       }
-      // epilogue: combine the two row-sum halves, O / l -> bf16, natural-log LSE
-      float* lb = red + ((kt & 1) * 256);              // the buffer the next tile writes last
-      lb[wg * 128 + r] = l;
-      mbar_wait(bar(O_FULL + ob), (it >> 1) & 1);
+      // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
+      mbar_wait(bar(O_FULL), it & 1);
       tc_fence_after();
-      named_bar_sync(1, SM_THREADS);
-      const float lt = lb[r] + lb[128 + r];
-      named_bar_sync(1, SM_THREADS);
-      const float inv = 1.f / lt;
-      const size_t orow = ((size_t)(I.r0 + I.mt * TQ + t) * Hq + I.kh * g + hh);
+      if (T.valid) {
+        const float inv = 1.f / l;
+        const size_t orow = ((size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float ov[32];
-        tmem_ld32(o_tmem + 32 * q, ov);
-        tmem_wait_ld();
-        if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 64 * wg + 32 * q);
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+          tmem_ld32(o_tmem + 32 * q, ov);
+          tmem_wait_ld();
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint4 v;
-            v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
-            v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
-            v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
-            v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
-            dst[ch] = v;
+            for (int ch = 0; ch < 4; ++ch) {
+              uint4 v;
+              v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
+              v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
+              v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
+              v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
+              dst[ch] = v;
+            }
           }
         }
+        if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
       }
-      if (valid && lse && wg == 0) lse[orow] = (m_used + __log2f(lt)) * 0.69314718055994531f;
       tc_fence_before();
-      mbar_arrive(bar(O_FREE + ob));
+      mbar_arrive(bar(O_FREE));
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// k_pair_scan: for every pair of consecutive M-tiles, how many leading KV tiles read the same
+// 4 pages for both (one warp per pair).
+__global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restrict__ cu_q,
+                                                   const int32_t* __restrict__ prefix_len,
+                                                   const int32_t* __restrict__ block_table, uint32_t TQ) {
+  const uint32_t lane = threadIdx.x & 31, nt = c.sc->n_tiles;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < cdiv(nt, 2);
+       u += (gridDim.x * blockDim.x) >> 5) {
+  const Tile A = decode_tile(c, cu_q, prefix_len, 2 * u, TQ), Bt = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ);
+  uint32_t nsh = 0;
+  if (Bt.valid) {
+    const uint32_t ntile = min(A.n_kv, Bt.n_kv);
+    const int32_t* ba = block_table + (size_t)A.i * c.max_blocks;
+    const int32_t* bb = block_table + (size_t)Bt.i * c.max_blocks;
+    // tile n is shared iff its 4 page ids agree (blocks past a request's end read page bt[0])
+    uint32_t n = 0;
+    for (; n < ntile; n += 8) {
+      const uint32_t tn = n + (lane >> 2), blk = tn * 4 + (lane & 3);
+      bool eq = true;
+      if (tn < ntile) {
+        const int32_t pa = blk < A.nblk ? ba[blk] : ba[0], pb = blk < Bt.nblk ? bb[blk] : bb[0];
+        eq = pa == pb;
+      }
+      const uint32_t bad = __ballot_sync(~0u, !eq);
+      if (bad) { n += (__ffs(bad) - 1) >> 2; break; }
+    }
+    nsh = min(n, ntile);
+  }
+  if (lane == 0) c.pair_nsh[u] = nsh;
+  }
 }
 
 }  // namespace sm100
@@ -494,6 +593,7 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
     if (r != CUDA_SUCCESS) { set_error("tensor map (kv) encode failed"); return IL_ERR_CUDA; }
   }
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, TQ);
+  k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
   static bool attr = false;
   if (!attr) {
     IL_CUDA(cudaFuncSetAttribute(k_attn_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -502,7 +602,7 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out, lse,
                                                         scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
   IL_LAUNCH_CHECK("k_attn_sm100");
-  c->launches += 2;
+  c->launches += 3;
   return IL_OK;
 }
 

@@ -86,6 +86,7 @@ struct Ctx {
   uint32_t dd_mask = 0;
   uint32_t *tile_off;        // attention work decomposition
   uint32_t *tile_req;        // attention M-tile -> request
+  uint32_t *pair_nsh;        // attention M-tile pair -> leading shared KV tiles
   uint64_t *evicted_list;
   uint32_t *guard_prompt;    // guard: DS_current prompt rows
   // pointers remembered between calls (caller-owned)

@@ -1,4 +1,4 @@
-"""Profiling aid: run config-3 steps with libinferlog_b200_trace.so (per-tile clock64 stamps of
+"""Profiling aid: run config-3 steps with libinferlog_b200_trace.so (per-load clock64 stamps of
 every role of the attention kernel in CTA 0) and print the steady-state timeline."""
 import ctypes as C
 import os
@@ -31,25 +31,33 @@ def main():
         pl.stage_batch(gen.make_batch(ds, s, b))
         pl.step()
     torch.cuda.synchronize()
-    tr = np.zeros((8, 4096), np.uint64)
+    raw = np.zeros(8 * 4096 + 1024 * 4 // 2 + 8, np.uint64)
     lib = _lib.load()
     lib.il_debug_trace.argtypes = [C.c_void_p]
-    _lib.check(lib.il_debug_trace(tr.ctypes.data_as(C.c_void_p)), "trace")
-    names = ["K-load", "V-load", "QK-issue", "PV-issue", "sm-start", "sm-maxsync", "P0-done", "P1-done"]
-    n = int((tr[2] > 0).sum())
-    t0 = int(tr[2][0])
-    rel = tr.astype(np.int64) - t0
-    print("tiles traced:", n)
-    lo, hi = 40, 56
-    print("kt   " + " ".join(f"{x:>10s}" for x in names))
-    for k in range(lo, hi):
-        print(f"{k:4d} " + " ".join(f"{int(rel[s][k]):10d}" for s in range(8)))
-    d = np.diff(rel[2][20:n - 5])
-    print("QK issue period: median", np.median(d), "mean", d.mean())
-    print("softmax: start->maxsync", np.median(rel[5][20:n - 5] - rel[4][20:n - 5]),
-          "maxsync->P0", np.median(rel[6][20:n - 5] - rel[5][20:n - 5]),
-          "S_FULL-wait(QK issue->sm start)", np.median(rel[4][20:n - 5] - rel[2][20:n - 5]),
-          "P0->PV issue", np.median(rel[3][20:n - 5] - rel[6][20:n - 5]))
+    _lib.check(lib.il_debug_trace(raw.ctypes.data_as(C.c_void_p)), "trace")
+    tr = raw[:8 * 4096].reshape(8, 4096).astype(np.int64)
+    items = raw[8 * 4096:8 * 4096 + 2048].view(np.uint32).reshape(1024, 4)
+    t0 = tr[2][0]
+    rel = np.where(tr > 0, tr - t0, -1)
+    n_it = int((items[:, 1] > 0).sum())
+    print("items in CTA 0:", n_it, "loads:", int(items[:n_it, 1].sum()))
+    print("first items (lc0, nload, nsh, nA|nB<<16):")
+    for k in range(min(8, n_it)):
+        print("  ", items[k, 0], items[k, 1], items[k, 2], items[k, 3] & 0xFFFF, items[k, 3] >> 16)
+    nsh = items[:n_it, 2].astype(float); nl = items[:n_it, 1].astype(float)
+    print(f"mean nsh {nsh.mean():.2f}, mean nload {nl.mean():.2f}, shared load share {nsh.sum() / nl.sum():.2%}")
+    lo = int(items[2, 0]) if n_it > 3 else 0
+    names = ["K-ready", "V-ready", "K_FULL", "PV(A)", "PV(B)", "smA-start", "smA-done", "smB-start", "smB-done"]
+    print("lc    K-load  V-load  QK(K_FULL)  PV_A   PV_B")
+    for l in range(lo, lo + 20):
+        print(f"{l:4d} {rel[0][l]:8d} {rel[1][l]:8d} {rel[2][l]:8d} {rel[3][2*l] if 2*l < 4096 else -1:8d} {rel[3][2*l+1] if 2*l+1 < 4096 else -1:8d}")
+    print("softmax tiles (A start, A done, B start, B done):")
+    for k in range(64, 84):
+        print(f"{k:4d} {rel[4][k]:8d} {rel[5][k]:8d} {rel[6][k]:8d} {rel[7][k]:8d}  durA {rel[5][k]-rel[4][k]:6d} durB {rel[7][k]-rel[6][k]:6d}")
+    tot_cycles = rel[2][int(items[n_it - 1, 0])] - rel[2][int(items[1, 0])]
+    loads = int(items[1:n_it - 1, 1].sum())
+    print("cycles per load (steady):", tot_cycles / max(loads, 1))
+    da = rel[5][20:400] - rel[4][20:400]; print("softmax A duration median", np.median(da))
 
 
 if __name__ == "__main__":
