@@ -104,6 +104,30 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Warp-uniform variants: every lane of the warp executes them, one elected lane issues (keeps
+// the operands in uniform registers: no per-instruction waterfall).
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_ss_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred e, q; setp.ne.b32 q, %3, 0; elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, q; }" ::"r"(d_tmem), "l"(a), "l"(b), "r"(acc),
+      "n"(IDESC)
+      : "memory");
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred e, q; setp.ne.b32 q, %3, 0; elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, q; }" ::"r"(d_tmem), "r"(a_tmem), "l"(b), "r"(acc),
+      "n"(IDESC)
+      : "memory");
+}
+__device__ __forceinline__ void commit_w(uint32_t bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar)
+      : "memory");
+}
 // A operand from TMEM (lane = row, 32-bit column = 2 consecutive bf16 along K)
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -315,87 +339,97 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ================= MMA issuer (single thread) =================
-    // Per Q tile x the 64-key sub-tiles n = 0, 1, 2, ... alternate TMEM buffers n & 1; QK of
-    // sub-tile n+2 reuses the buffer of n, so it is issued right after PV(n) (tcgen05 ops from
-    // one thread execute in order).  The two Q tiles' chains interleave on the tensor pipe.
-    uint32_t lc = 0, it = 0, cnt[2] = {0, 0};        // load counter, per-Q-tile sub-tile counters
-    uint32_t vusers[8] = {0, 0, 0, 0, 0, 0, 0, 0};    // PVs still to read V of load lc (by lc % 8)
+  } else if (warp == 1) {
+    // ================= MMA issuer: warp-uniform loop, one elected lane issues ==============
+    // Per Q tile x the 64-key tiles n = 0, 1, 2, ... alternate TMEM buffers n & 1; QK of tile
+    // n+2 reuses the buffer of n, so it is issued right after PV(n) (tcgen05 ops from one
+    // thread execute in order).  The two Q tiles' chains interleave on the tensor pipe.
+    const uint64_t dqa = sdesc(sbase + OFF_QA, 16, 1024), dqb = sdesc(sbase + OFF_QB, 16, 1024);
+    const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024), dv0 = sdesc(sbase + OFF_V, KCB, 1024);
+    uint32_t lc = 0, it = 0, cnt0 = 0, cnt1 = 0;
+    uint32_t vus = 0;                                 // 2-bit PV-user counters per load (lc % 8)
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
-      uint32_t last[2] = {0, 0};
+      uint32_t last0 = 0, last1 = 0;
       for (uint32_t l = 0; l < pr.nload; ++l) {
         uint32_t n_, r_, t_;
         load_info(pr, l, n_, r_, t_);
-        if (t_ & 1u) last[0] = l;
-        if (t_ & 2u) last[1] = l;
+        if (t_ & 1u) last0 = l;
+        if (t_ & 2u) last1 = l;
       }
       mbar_wait(bar(Q_FULL), it & 1);
 #ifdef IL_ATTN_TRACE
-      if (blockIdx.x == 0 && it < 1024) {
+      if (blockIdx.x == 0 && it < 1024 && lane == 0) {
         g_trace_item[it][0] = lc; g_trace_item[it][1] = pr.nload; g_trace_item[it][2] = pr.nsh;
         g_trace_item[it][3] = pr.a.n_kv | (pr.b.n_kv << 16);
       }
 #endif
       tc_fence_after();
-      // pending PVs per Q tile: up to two tiles (ring), each = (load counter, tile count)
-      uint32_t pq_l[2][2], pq_c[2][2], pq_n[2] = {0, 0}, pq_head[2] = {0, 0};
-      bool first[2] = {true, true}, o_ready = it == 0;
-      auto pv_one = [&](uint32_t x) {                  // issue the oldest pending PV of Q tile x
-        const uint32_t slot = pq_head[x];
-        const uint32_t pl = pq_l[x][slot], pc = pq_c[x][slot], vs = pl % NSTV;
+      // pending PVs per Q tile (<= 2, oldest first): (load counter, tile count)
+      uint32_t q0n = 0, q0l0 = 0, q0c0 = 0, q0l1 = 0, q0c1 = 0;
+      uint32_t q1n = 0, q1l0 = 0, q1c0 = 0, q1l1 = 0, q1c1 = 0;
+      bool first0 = true, first1 = true, o_ready = it == 0;
+      auto pv_one = [&](const uint32_t x) {           // oldest pending PV of Q tile x
+        const uint32_t pl = x ? q1l0 : q0l0, pc = x ? q1c0 : q0c0, vs = pl % NSTV;
         if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
         mbar_wait(bar(P_FULL + 2 * x + (pc & 1)), (pc >> 1) & 1);
         mbar_wait(bar(V_FULL + vs), (pl / NSTV) & 1);
-        IL_TRACE(3, (2 * pl + x) & 4095);
+        if (lane == 0) IL_TRACE(3, (2 * pl + x) & 4095);
         tc_fence_after();
-        const uint32_t vaddr = sbase + OFF_V + vs * KVTILE;
+        const uint64_t dv = dv0 + (uint64_t)((vs * KVTILE) >> 4);
         const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x + 64 * (pc & 1);
+        const bool fst = x ? first1 : first0;
+        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 0, dv + 0 * 128, fst ? 0u : 1u);
+        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8, dv + 1 * 128, 1u);
+        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 16, dv + 2 * 128, 1u);
+        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 24, dv + 3 * 128, 1u);
+        if (x) first1 = false; else first0 = false;
+        commit_w(bar(PV_DONE + x));
+        const uint32_t sh = 2 * (pl & 7);
+        vus -= 1u << sh;
+        if (((vus >> sh) & 3u) == 0) commit_w(bar(V_FREE + vs));
+        if (x) { q1l0 = q1l1; q1c0 = q1c1; --q1n; } else { q0l0 = q0l1; q0c0 = q0c1; --q0n; }
+      };
+      auto qk = [&](const uint32_t x, const uint64_t dk) {
+        if ((x ? q1n : q0n) == 2) pv_one(x);          // frees the TMEM buffer this QK overwrites
+        const uint32_t sc = x ? cnt1++ : cnt0++;
+        const uint32_t s_tmem = tmem + 128 * x + 64 * (sc & 1);
+        const uint64_t dq = x ? dqb : dqa;
+        // K = 128 (head dim) in 8 steps of 16: +32 B within a 64-column block, +CB / +KCB across
 #pragma unroll
-        for (uint32_t k = 0; k < 4; ++k)
-          tc_mma_ts(o_tmem, p_tmem + k * 8, sdesc(vaddr + k * 2048, KCB, 1024), IDESC_PV, (first[x] && k == 0) ? 0u : 1u);
-        first[x] = false;
-        tc_commit(bar(PV_DONE + x));
-        if (--vusers[pl & 7] == 0) tc_commit(bar(V_FREE + vs));
-        pq_head[x] ^= 1;
-        --pq_n[x];
+        for (uint32_t k = 0; k < 8; ++k)
+          mma_ss_w<IDESC_QK>(s_tmem, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
+                             dk + (uint64_t)(((k >> 2) * KCB + (k & 3) * 32) >> 4), k ? 1u : 0u);
+        commit_w(bar(S_FULL + 2 * x + (sc & 1)));
+        if (x) {
+          if (q1n == 0) { q1l0 = lc; q1c0 = sc; } else { q1l1 = lc; q1c1 = sc; }
+          ++q1n;
+        } else {
+          if (q0n == 0) { q0l0 = lc; q0c0 = sc; } else { q0l1 = lc; q0c1 = sc; }
+          ++q0n;
+        }
       };
       for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
         uint32_t n, req, tgt;
         load_info(pr, l, n, req, tgt);
-#pragma unroll
-        for (uint32_t x = 0; x < 2; ++x)               // a Q tile whose loads ended drains its PVs
-          if (last[x] < l) while (pq_n[x]) pv_one(x);
+        if (last0 < l) while (q0n) pv_one(0);         // a Q tile whose loads ended drains its PVs
+        if (last1 < l) while (q1n) pv_one(1);
         const uint32_t ks = lc % NSTK;
         mbar_wait(bar(K_FULL + ks), (lc / NSTK) & 1);
-        IL_TRACE(2, lc & 4095);
+        if (lane == 0) IL_TRACE(2, lc & 4095);
         tc_fence_after();
-        vusers[lc & 7] = (tgt == 3) ? 2u : 1u;
-        const uint32_t kaddr = sbase + OFF_K + ks * KVTILE;
-#pragma unroll
-        for (uint32_t x = 0; x < 2; ++x) {
-          if (!((tgt >> x) & 1u)) continue;
-          if (pq_n[x] == 2) pv_one(x);                 // frees the TMEM buffer this QK overwrites
-          const uint32_t qaddr = sbase + (x ? OFF_QB : OFF_QA);
-          const uint32_t sc = cnt[x]++;
-          const uint32_t s_tmem = tmem + 128 * x + 64 * (sc & 1);
-#pragma unroll
-          for (uint32_t k = 0; k < 8; ++k)
-            tc_mma(s_tmem, sdesc(qaddr + (k >> 2) * CB + (k & 3) * 32, 16, 1024),
-                   sdesc(kaddr + (k >> 2) * KCB + (k & 3) * 32, 16, 1024), IDESC_QK, k ? 1u : 0u);
-          tc_commit(bar(S_FULL + 2 * x + (sc & 1)));
-          const uint32_t slot = (pq_head[x] + pq_n[x]) & 1;
-          pq_l[x][slot] = lc; pq_c[x][slot] = sc;
-          ++pq_n[x];
-        }
-        tc_commit(bar(K_FREE + ks));
-        if (l + 1 == pr.nload) tc_commit(bar(Q_FREE));
+        const uint32_t sh = 2 * (lc & 7);
+        vus = (vus & ~(3u << sh)) | (((tgt == 3) ? 2u : 1u) << sh);
+        const uint64_t dk = dk0 + (uint64_t)((ks * KVTILE) >> 4);
+        if (tgt & 1u) qk(0, dk);
+        if (tgt & 2u) qk(1, dk);
+        commit_w(bar(K_FREE + ks));
+        if (l + 1 == pr.nload) commit_w(bar(Q_FREE));
       }
-      while (pq_n[0]) pv_one(0);
-      while (pq_n[1]) pv_one(1);
+      while (q0n) pv_one(0);
+      while (q1n) pv_one(1);
       if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
-      tc_commit(bar(O_FULL));
+      commit_w(bar(O_FULL));
     }
   } else if (warp >= 4) {
     // ====== softmax + epilogue: warpgroup x owns Q tile x (A: warps 4-7, B: warps 8-11) ======
