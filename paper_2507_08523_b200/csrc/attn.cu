@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(256) k_attn_simple(Ctx c, uint32_t B, const in
 }  // namespace il
 
 #include "attn_sm100.cuh"
+#include "attn_sm100_single.cuh"
 
 using namespace il;
 
@@ -194,8 +195,12 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
                                               (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
   IL_LAUNCH_CHECK("k_kv_append");
   c->launches += 1;
-  if (attn_sm100_supported(c))
+  if (attn_sm100_supported(c)) {
+    const char* kv = getenv("IL_ATTN_KERNEL");
+    if (kv && kv[0] == 's')
+      return attn_sm100s_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
     return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
+  }
   if (g * SIMPLE_TQ > 128) { set_error("bring-up attention: Hq/Hkv > 8 unsupported"); return IL_ERR_ARG; }
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, SIMPLE_TQ);
   const uint32_t R = SIMPLE_TQ * g;
