@@ -2,7 +2,7 @@
 //
 // One work item = (request i, kv head kh, M-tile of TQ = 128/g suffix tokens).  The g q-heads
 // sharing kv head kh are packed as rows (row = token * g + head) so one 128-row tcgen05 tile
-// covers TQ tokens x g heads (GQA packing).  KV tiles are 64 keys = 4 pages of 16 tokens,
+// covers TQ tokens x g heads (GQA packing).  KV tiles are 128 keys = 8 pages of 16 tokens,
 // each page a [16][128] bf16 block of the caller's [C][Hkv][16][d] cache, fetched by TMA
 // (two 64-column boxes per page, 128-byte swizzle).  Per KV tile:
 //   S = Q K^T      tcgen05.mma kind::f16, A = Q (smem, K-major), B = K tile (smem, K-major),
@@ -40,24 +40,24 @@ __device__ unsigned int g_trace_item[1024][4];
 
 constexpr uint32_t D = 128;              // head dim handled by this kernel
 constexpr uint32_t BM = 128;             // rows per M-tile
-constexpr uint32_t BN = 64;              // keys per KV tile (= 4 pages) = one softmax step
-constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile (Q)
+constexpr uint32_t BN = 128;             // keys per KV tile (= 8 pages) = one softmax step
+constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
 constexpr uint32_t QTILE = 2 * CB;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t KCB = 8192;           // one 64-column block of a 64-key K/V tile
-constexpr uint32_t KVTILE = 2 * KCB;     // 64 x 128 bf16 = 16 KB
-constexpr uint32_t NSTK = 4, NSTV = 6;   // K and V ring depths
+constexpr uint32_t KCB = CB;             // one 64-column block of a 128-key K/V tile
+constexpr uint32_t KVTILE = 2 * KCB;     // 128 x 128 bf16 = 32 KB
+constexpr uint32_t NSTK = 3, NSTV = 2;   // K and V ring depths
 constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
 constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
 constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
 constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
-constexpr uint32_t NBAR = 34;
+constexpr uint32_t NBAR = 20;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int THREADS = 384;
 constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
 // S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
-enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 6, V_FULL = 10, V_FREE = 16, S_FULL = 22, P_FULL = 26,
-           PV_DONE = 30, O_FULL = 32, O_FREE = 33 };
+enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 5, V_FULL = 8, V_FREE = 10, S_FULL = 12, P_FULL = 14,
+           PV_DONE = 16, O_FULL = 18, O_FREE = 19 };
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -175,6 +175,38 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes (exp2 emulation, offloads the MUFU unit): x = j + f with j the
+// nearest integer (magic-number rounding), 2^f by a cubic on [-0.5, 0.5] (relative error
+// < 7e-5, far below the bf16 rounding of P), 2^j added to the exponent field.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;                   // 1.5 * 2^23
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(f, 0.05550411f, 0.24022651f);
+  p = fmaf(p, f, 0.69314718f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+#ifndef IL_EXP_EMU_MASK
+#define IL_EXP_EMU_MASK 7                            // emulate elements with (j & mask) == mask
+#endif
+__device__ __forceinline__ float ex2_mixed(float x, int j) {
+  return ((j & IL_EXP_EMU_MASK) == IL_EXP_EMU_MASK) ? ex2_poly(x) : ex2(x);
+}
+
+// packed fp32x2 (FFMA2 / FADD2 on sm_100a): two elements per instruction
+__device__ __forceinline__ void ffma2(float& o0, float& o1, float a0, float a1, float s, float m) {
+  asm("{ .reg .b64 x, y, z, w; mov.b64 x, {%2, %3}; mov.b64 y, {%4, %4}; mov.b64 z, {%5, %5};\n\t"
+      "fma.rn.f32x2 w, x, y, z; mov.b64 {%0, %1}, w; }"
+      : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(s), "f"(m));
+}
+__device__ __forceinline__ void fadd2(float& s0, float& s1, float a0, float a1) {
+  asm("{ .reg .b64 x, y, w; mov.b64 x, {%0, %1}; mov.b64 y, {%2, %3};\n\t"
+      "add.rn.f32x2 w, x, y; mov.b64 {%0, %1}, w; }"
+      : "+f"(s0), "+f"(s1) : "f"(a0), "f"(a1));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));   // low half = a
@@ -189,7 +221,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 // instruction descriptor kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // A major [15] (0 = K), B major [16] (1 = MN), N >> 3 [17,23), M >> 4 [24,29)
-constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((BM >> 4) << 24);  // N = 64 keys
+constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
 constexpr uint32_t IDESC_PV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((D >> 3) << 17) | ((BM >> 4) << 24);
 
 // ------------------------------------------------------------------ work decomposition
@@ -274,8 +306,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (uint32_t s = 0; s < NSTK; ++s) { mbar_init(bar(K_FULL + s), 1); mbar_init(bar(K_FREE + s), 1); }
     static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
     for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
-    for (int x = 0; x < 4; ++x) { mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), 128); }
-    for (int x = 0; x < 2; ++x) mbar_init(bar(PV_DONE + x), 1);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), 128); mbar_init(bar(PV_DONE + x), 1);
+    }
     mbar_init(bar(O_FULL), 1); mbar_init(bar(O_FREE), SM_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
@@ -291,9 +324,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: Q tile x owns S/P columns [128x, 128x+128) as two 64-key sub-tile buffers
-  // h (columns 128x + 64h ..): the P of a sub-tile overwrites the first 32 columns of its S as
-  // packed bf16.  O_A = [256,384), O_B = [384,512).
+  // TMEM columns: S_A [0,128), S_B [128,256) (the P of a tile overwrites the first 64 columns
+  // of its S as packed bf16), O_A [256,384), O_B [384,512).
 
   if (warp == 0 || warp == 3) {
     // ============ TMA producers: warp 0 = Q tiles + K tiles, warp 3 = V tiles ============
@@ -323,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         load_info(pr, l, n, req, tgt);
         const uint32_t nblk = req == pr.a.i ? pr.a.nblk : pr.b.nblk;
         const int32_t* bt = block_table + (size_t)req * c.max_blocks;
-        const uint32_t blk = n * 4 + (lane & 3);
+        const uint32_t blk = n * 8 + (lane & 7);
         const int32_t page = blk < nblk ? __ldg(bt + blk) : __ldg(bt);
         const uint32_t s = lc % nst, u = lc / nst;
         if (lane == 0) {
@@ -332,8 +364,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_expect_tx(bar(full0 + s), KVTILE);
         }
         __syncwarp();
-        if (lane < 8) {                                  // lane = (page, column half)
-          const uint32_t p = lane & 3, h = lane >> 2;
+        if (lane < 16) {                                 // lane = (page, column half)
+          const uint32_t p = lane & 7, h = lane >> 3;
           const int row = (int)(((uint32_t)page * Hkv + pr.kh) * BS);
           tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
         }
@@ -365,55 +397,48 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
 #endif
       tc_fence_after();
-      // pending PVs per Q tile (<= 2, oldest first): (load counter, tile count)
-      uint32_t q0n = 0, q0l0 = 0, q0c0 = 0, q0l1 = 0, q0c1 = 0;
-      uint32_t q1n = 0, q1l0 = 0, q1c0 = 0, q1l1 = 0, q1c1 = 0;
+      // pending PV per Q tile (S is single-buffered: PV(n) must precede QK(n+1)):
+      // (load counter, tile count)
+      uint32_t q0n = 0, q0l = 0, q0c = 0, q1n = 0, q1l = 0, q1c = 0;
       bool first0 = true, first1 = true, o_ready = it == 0;
-      auto pv_one = [&](const uint32_t x) {           // oldest pending PV of Q tile x
-        const uint32_t pl = x ? q1l0 : q0l0, pc = x ? q1c0 : q0c0, vs = pl % NSTV;
+      auto pv_one = [&](const uint32_t x) {
+        const uint32_t pl = x ? q1l : q0l, pc = x ? q1c : q0c, vs = pl % NSTV;
         if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
-        mbar_wait(bar(P_FULL + 2 * x + (pc & 1)), (pc >> 1) & 1);
+        mbar_wait(bar(P_FULL + x), pc & 1);
         mbar_wait(bar(V_FULL + vs), (pl / NSTV) & 1);
         if (lane == 0) IL_TRACE(3, (2 * pl + x) & 4095);
         tc_fence_after();
         const uint64_t dv = dv0 + (uint64_t)((vs * KVTILE) >> 4);
-        const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x + 64 * (pc & 1);
+        const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x;
         const bool fst = x ? first1 : first0;
-        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 0, dv + 0 * 128, fst ? 0u : 1u);
-        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8, dv + 1 * 128, 1u);
-        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 16, dv + 2 * 128, 1u);
-        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 24, dv + 3 * 128, 1u);
+        // K = 128 keys in 8 steps of 16 (V tile rows; 16 keys = 2 swizzle atoms = 2048 B)
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+          mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst && k == 0) ? 0u : 1u);
         if (x) first1 = false; else first0 = false;
         commit_w(bar(PV_DONE + x));
         const uint32_t sh = 2 * (pl & 7);
         vus -= 1u << sh;
         if (((vus >> sh) & 3u) == 0) commit_w(bar(V_FREE + vs));
-        if (x) { q1l0 = q1l1; q1c0 = q1c1; --q1n; } else { q0l0 = q0l1; q0c0 = q0c1; --q0n; }
+        if (x) q1n = 0; else q0n = 0;
       };
       auto qk = [&](const uint32_t x, const uint64_t dk) {
-        if ((x ? q1n : q0n) == 2) pv_one(x);          // frees the TMEM buffer this QK overwrites
+        if (x ? q1n : q0n) pv_one(x);                 // frees the S/P columns this QK overwrites
         const uint32_t sc = x ? cnt1++ : cnt0++;
-        const uint32_t s_tmem = tmem + 128 * x + 64 * (sc & 1);
+        const uint32_t s_tmem = tmem + 128 * x;
         const uint64_t dq = x ? dqb : dqa;
-        // K = 128 (head dim) in 8 steps of 16: +32 B within a 64-column block, +CB / +KCB across
 #pragma unroll
         for (uint32_t k = 0; k < 8; ++k)
           mma_ss_w<IDESC_QK>(s_tmem, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
                              dk + (uint64_t)(((k >> 2) * KCB + (k & 3) * 32) >> 4), k ? 1u : 0u);
-        commit_w(bar(S_FULL + 2 * x + (sc & 1)));
-        if (x) {
-          if (q1n == 0) { q1l0 = lc; q1c0 = sc; } else { q1l1 = lc; q1c1 = sc; }
-          ++q1n;
-        } else {
-          if (q0n == 0) { q0l0 = lc; q0c0 = sc; } else { q0l1 = lc; q0c1 = sc; }
-          ++q0n;
-        }
+        commit_w(bar(S_FULL + x));
+        if (x) { q1l = lc; q1c = sc; q1n = 1; } else { q0l = lc; q0c = sc; q0n = 1; }
       };
       for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
         uint32_t n, req, tgt;
         load_info(pr, l, n, req, tgt);
-        if (last0 < l) while (q0n) pv_one(0);         // a Q tile whose loads ended drains its PVs
-        if (last1 < l) while (q1n) pv_one(1);
+        if (last0 < l && q0n) pv_one(0);              // a Q tile whose loads ended drains its PV
+        if (last1 < l && q1n) pv_one(1);
         const uint32_t ks = lc % NSTK;
         mbar_wait(bar(K_FULL + ks), (lc / NSTK) & 1);
         if (lane == 0) IL_TRACE(2, lc & 4095);
@@ -444,19 +469,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
       const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
       float m_used = -INFINITY, l = 0.f;
-      const uint32_t nsub = T.valid ? T.n_kv : 0;      // 64-key KV tiles
-      for (uint32_t n = 0; n < nsub; ++n, ++cnt) {
-        const uint32_t b = cnt & 1;
-        const uint32_t sb_tmem = s_tmem + 64 * b;
-        mbar_wait(bar(S_FULL + 2 * x + b), (cnt >> 1) & 1);
+      const uint32_t ntl = T.valid ? T.n_kv : 0;
+      for (uint32_t n = 0; n < ntl; ++n, ++cnt) {
+        mbar_wait(bar(S_FULL + x), cnt & 1);
         if (r == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
         tc_fence_after();
         const uint32_t key0 = n * BN;
+        const bool masked = key0 + BN - 1 > pos_q;
         float a[64];
-        tmem_ld32(sb_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
-        tmem_ld32(sb_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
+        // pass 1: row max over both 64-column halves
+        tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
+        tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
         tmem_wait_ld();
-        if (key0 + BN - 1 > pos_q) {
+        if (masked) {
 #pragma unroll
           for (int j = 0; j < 64; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
         }
@@ -465,6 +490,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int q = 0; q < 8; ++q) mxa[q] = a[q];
 #pragma unroll
         for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
+        tmem_ld32(s_tmem + 64, *reinterpret_cast<float(*)[32]>(&a[0]));
+        tmem_ld32(s_tmem + 96, *reinterpret_cast<float(*)[32]>(&a[32]));
+        tmem_wait_ld();
+        if (masked) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) if (key0 + 64 + j > pos_q) a[j] = -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
         const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float mx2 = mx * scale_log2;
@@ -479,7 +513,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           l *= factor;
         }
         if (__any_sync(~0u, need)) {
-          // lazy rescale of this warp's O rows once the previous sub-tile's PV has landed
+          // lazy rescale of this warp's O rows once the previous tile's PV has landed
           mbar_wait(bar(PV_DONE + x), (cnt - 1) & 1);
           tc_fence_after();
 #pragma unroll
@@ -495,19 +529,39 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const float negm = -m_used;
         float rsa[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[32];
+        uint32_t pk1[32], pk0[32];
+        // pass 2: keys 64..127 are in registers; then reload keys 0..63
 #pragma unroll
         for (int j = 0; j < 64; j += 2) {
-          const float p0 = ex2(fmaf(a[j], scale_log2, negm)), p1 = ex2(fmaf(a[j + 1], scale_log2, negm));
-          rsa[(j >> 1) & 3] += p0 + p1;
-          pk[j >> 1] = pack_bf16(p0, p1);
+          float x0, x1;
+          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+          const float p0 = ex2_mixed(x0, j), p1 = ex2_mixed(x1, j + 1);
+          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+          pk1[j >> 1] = pack_bf16(p0, p1);
+        }
+        tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
+        tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
+        tmem_wait_ld();
+        if (masked) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          float x0, x1;
+          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+          const float p0 = ex2_mixed(x0, j), p1 = ex2_mixed(x1, j + 1);
+          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+          pk0[j >> 1] = pack_bf16(p0, p1);
         }
         l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
-        tmem_st32u(sb_tmem, pk);                        // P (bf16 pairs) over this S's first 32 columns
+        // P (bf16 pairs, keys 0..127) overwrites TMEM columns [0, 64) of this S
+        tmem_st32u(s_tmem, pk0);
+        tmem_st32u(s_tmem + 32, pk1);
         tmem_wait_st();
         tc_fence_before();
         if (r == 0) IL_TRACE(5 + 2 * x, cnt & 4095);
-        mbar_arrive(bar(P_FULL + 2 * x + b));
+        mbar_arrive(bar(P_FULL + x));
       }
       // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
       mbar_wait(bar(O_FULL), it & 1);
@@ -546,7 +600,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // k_pair_scan: for every pair of consecutive M-tiles, how many leading KV tiles read the same
-// 4 pages for both (one warp per pair).
+// 8 pages for both (one warp per pair).
 __global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restrict__ cu_q,
                                                    const int32_t* __restrict__ prefix_len,
                                                    const int32_t* __restrict__ block_table, uint32_t TQ) {
@@ -559,17 +613,17 @@ __global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restr
     const uint32_t ntile = min(A.n_kv, Bt.n_kv);
     const int32_t* ba = block_table + (size_t)A.i * c.max_blocks;
     const int32_t* bb = block_table + (size_t)Bt.i * c.max_blocks;
-    // tile n is shared iff its 4 page ids agree (blocks past a request's end read page bt[0])
+    // tile n is shared iff its 8 page ids agree (blocks past a request's end read page bt[0])
     uint32_t n = 0;
-    for (; n < ntile; n += 8) {
-      const uint32_t tn = n + (lane >> 2), blk = tn * 4 + (lane & 3);
+    for (; n < ntile; n += 4) {
+      const uint32_t tn = n + (lane >> 3), blk = tn * 8 + (lane & 7);
       bool eq = true;
       if (tn < ntile) {
         const int32_t pa = blk < A.nblk ? ba[blk] : ba[0], pb = blk < Bt.nblk ? bb[blk] : bb[0];
         eq = pa == pb;
       }
       const uint32_t bad = __ballot_sync(~0u, !eq);
-      if (bad) { n += (__ffs(bad) - 1) >> 2; break; }
+      if (bad) { n += (__ffs(bad) - 1) >> 3; break; }
     }
     nsh = min(n, ntile);
   }
