@@ -39,6 +39,16 @@ def peaks():
     return {"hbm": 6650.0, "tc": 1590.0, "tc_sustained": 1400.0, "src": "fallback (B200_PROFILING.md)"}
 
 
+def ncu_traffic():
+    """dram read+write bytes per launch of the attention kernel from the committed ncu summary
+    (profiles/attn_ncu_summary.json, written from one `ncu --set full` capture), or None."""
+    p = os.path.join(ROOT, "profiles", "attn_ncu_summary.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    return None, None
+
+
 def workload(cfg_n: int, rank: int, world: int):
     cfg = gen.config(cfg_n)
     name, n, nt, s, seed = cfg.datasets[0]
@@ -60,13 +70,14 @@ def plan_batches(cfg, n_full: int, rank: int, world: int, ramp=(1, 64)):
 
 
 def flops_bytes(plen, hit, bt, Hq, Hkv, d):
-    """Algorithmic work of prefill attention for one batch."""
-    L = plen.astype(np.int64); P = 16 * hit.astype(np.int64); S = L - P
+    """Algorithmic work of prefill attention for one batch:
+    FLOPs = sum_i 4 d Hq (S_i P_i + S_i (S_i + 1) / 2); bytes = Q + O + K_new + V_new of the
+    suffix rows (write + read of the appended K/V) + one read of every distinct cached page."""
+    L = plen.astype(np.int64); H = hit.astype(np.int64); P = 16 * H; S = L - P
     flops = float(np.sum(4 * d * Hq * (S * P + S * (S + 1) // 2)))
-    pages = set()
-    for i in range(len(L)):
-        pages.update(bt[i, :hit[i]].tolist())
-    byts = float(np.sum(2 * d * S * (2 * Hq + 4 * Hkv))) + 4.0 * d * Hkv * 16 * len(pages)
+    mask = np.arange(bt.shape[1])[None, :] < H[:, None]
+    n_pages = len(np.unique(bt[mask]))
+    byts = float(np.sum(2 * d * S * (2 * Hq + 4 * Hkv))) + 4.0 * d * Hkv * 16 * n_pages
     return flops, byts
 
 
@@ -78,16 +89,18 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(gpu_index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = self.p.stdout.readline()          # sampling has started
         except Exception:
             self.p = None
+            self.first = ""
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
-        out = self.p.communicate()[0]
+        out = self.first + self.p.communicate()[0]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -130,55 +143,85 @@ def run_ours(args, rank, world, local_rank):
     plan = plan_batches(cfg, W + 2 * K, rank, world)
     n_ramp = len(plan) - (W + 2 * K)
     batches = [gen.make_batch(ds, s, b) for s, b in plan]
-    # device-resident inputs for the warm-up + device-timed steps
-    dev_in = []
-    for bt in batches[:n_ramp + W + K]:
-        dev_in.append((torch.from_numpy(bt.q_off.view(np.int32)).to(dev), torch.from_numpy(bt.q_tok.view(np.int32)).to(dev),
-                       torch.from_numpy(bt.q_src.view(np.int32)).to(dev), bt.B))
+
+    def to_dev(bt):
+        return (torch.from_numpy(bt.q_off.view(np.int32)).to(dev), torch.from_numpy(bt.q_tok.view(np.int32)).to(dev),
+                torch.from_numpy(bt.q_src.view(np.int32)).to(dev), bt.B)
+
+    def to_pinned(bt):
+        return tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src)) + (bt.B,)
+
+    # Timed steps alternate: even = device-timed (inputs already resident in HBM), odd = end to
+    # end (pinned host inputs copied in, refined DS / info / hits copied out inside the timed
+    # region), so both see the same part of the stream.
+    warm_in = [to_dev(bt) for bt in batches[:n_ramp + W]]
+    timed = batches[n_ramp + W:]
+    dev_in = [to_dev(bt) if j % 2 == 0 else None for j, bt in enumerate(timed)]
+    host_in = [to_pinned(bt) if j % 2 == 1 else None for j, bt in enumerate(timed)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stage_buf = (torch.zeros(cfg.B + 1, dtype=torch.int32, device=dev),
+                 torch.zeros(cfg.B * 256, dtype=torch.int32, device=dev), torch.zeros(cfg.B, dtype=torch.int32, device=dev))
+    out_fin = torch.empty(cfg.B, cfg.k, dtype=torch.int32).pin_memory()
+    out_hit = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
+    out_info = torch.empty(cfg.B, 16, dtype=torch.uint8).pin_memory()
+    # per-step accounting kept on the device (no host sync inside the timed region)
+    rec_len = torch.zeros(K, cfg.B, dtype=torch.int32, device=dev)
+    rec_hit = torch.zeros(K, cfg.B, dtype=torch.int32, device=dev)
+    rec_bt = torch.zeros(K, cfg.B, ccfg.max_blocks, dtype=torch.int32, device=dev)
 
     def set_inputs(x):
         pl.q_off, pl.q_tok, pl.q_src, pl.B = x
 
     # ---- warm-up (cold-start ramp + W full steps), not timed
     with torch.cuda.stream(stream):
-        for x in dev_in[:n_ramp + W]:
+        for x in warm_in:
             set_inputs(x)
             pl.step()
     stream.synchronize()
     pl.ctx.status_sync(stream)
 
-    # ---- device-timed steps: inputs resident in HBM, L2 flushed between steps
     stage_names = ["refine", "match", "synth", "attn", "commit"]
-    step_ms, stage_ms, attn_ms, work = [], {n: [] for n in stage_names}, [], []
-    hits = fulls = 0
+    evs, e2e_evs = [], []
+    h2d = d2h = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     t_wall = time.perf_counter()
     launches0 = pl.launches()
-    for x in dev_in[n_ramp + W:]:
-        with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):
+        for j in range(2 * K):
             flush.zero_()
-            set_inputs(x)
-            e = [ev() for _ in range(6)]
-            e[0].record(stream); pl.refine()
-            e[1].record(stream); pl.match()
-            e[2].record(stream); pl.synth()
-            e[3].record(stream); pl.attn()
-            e[4].record(stream); pl.commit()
-            e[5].record(stream)
-        e[5].synchronize()
-        step_ms.append(e[0].elapsed_time(e[5]))
-        for j, n in enumerate(stage_names):
-            stage_ms[n].append(e[j].elapsed_time(e[j + 1]))
-        B = x[3]
-        plen = pl.prompt_len[:B].cpu().numpy(); hit = pl.hit[:B].cpu().numpy()
-        bt = pl.block_table[:B].cpu().numpy()
-        work.append(flops_bytes(plen, hit, bt, cfg.Hq, cfg.Hkv, cfg.d))
-        hits += int(hit.sum()); fulls += int((plen // 16).sum())
+            if j % 2 == 0:
+                set_inputs(dev_in[j])
+                e = [ev() for _ in range(6)]
+                e[0].record(stream); pl.refine()
+                e[1].record(stream); pl.match()
+                e[2].record(stream); pl.synth()
+                e[3].record(stream); pl.attn()
+                e[4].record(stream); pl.commit()
+                e[5].record(stream)
+                evs.append(e)
+                B = dev_in[j][3]
+                rec_len[j // 2, :B].copy_(pl.prompt_len[:B]); rec_hit[j // 2, :B].copy_(pl.hit[:B])
+                rec_bt[j // 2, :B].copy_(pl.block_table[:B])
+            else:
+                qo, qt, qs, B = host_in[j]
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                stage_buf[0][:B + 1].copy_(qo, non_blocking=True)
+                stage_buf[1][:qt.numel()].copy_(qt, non_blocking=True)
+                stage_buf[2][:B].copy_(qs, non_blocking=True)
+                set_inputs(stage_buf + (B,))
+                pl.step()
+                out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
+                out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
+                out_info[:B].copy_(pl.info[:B], non_blocking=True)
+                e1.record(stream)
+                e2e_evs.append((e0, e1))
+                h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
+                d2h = 4 * B * cfg.k + 4 * B + 16 * B
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall
     clk = clocks.stop()
@@ -186,42 +229,15 @@ def run_ours(args, rank, world, local_rank):
     pl.ctx.status_sync(stream)
     if world > 1:
         dist.barrier()
-
-    # ---- end-to-end: host (pinned) inputs in, results out, every step
-    pinned = []
-    for bt in batches[n_ramp + W + K:]:
-        pinned.append(tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src))
-                      + (bt.B,))
-    out_fin = torch.empty(cfg.B, cfg.k, dtype=torch.int32).pin_memory()
-    out_hit = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
-    out_info = torch.empty(cfg.B, 16, dtype=torch.uint8).pin_memory()
-    h2d = d2h = 0
-    pl.q_off = torch.zeros(cfg.B + 1, dtype=torch.int32, device=dev)
-    pl.q_tok = torch.zeros(cfg.B * 256, dtype=torch.int32, device=dev)
-    pl.q_src = torch.zeros(cfg.B, dtype=torch.int32, device=dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e2e_ms = []
-    for qo, qt, qs, B in pinned:
-        with torch.cuda.stream(stream):
-            flush.zero_()
-            e0, e1 = ev(), ev()
-            e0.record(stream)
-            pl.q_off[:B + 1].copy_(qo, non_blocking=True)
-            pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
-            pl.q_src[:B].copy_(qs, non_blocking=True)
-            pl.B = B
-            pl.step()
-            out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
-            out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
-            out_info[:B].copy_(pl.info[:B], non_blocking=True)
-            e1.record(stream)
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-        h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
-        d2h = 4 * B * cfg.k + 4 * B + 16 * B
-    pl.ctx.status_sync(stream)
+    step_ms = [e[0].elapsed_time(e[5]) for e in evs]
+    stage_ms = {n: [e[i].elapsed_time(e[i + 1]) for e in evs] for i, n in enumerate(stage_names)}
+    e2e_ms = [a.elapsed_time(b) for a, b in e2e_evs]
+    work, hits, fulls = [], 0, 0
+    L_all, H_all, BT_all = rec_len.cpu().numpy(), rec_hit.cpu().numpy(), rec_bt.cpu().numpy()
+    for j in range(K):
+        B = dev_in[2 * j][3]
+        work.append(flops_bytes(L_all[j, :B], H_all[j, :B], BT_all[j, :B], cfg.Hq, cfg.Hkv, cfg.d))
+        hits += int(H_all[j, :B].sum()); fulls += int((L_all[j, :B] // 16).sum())
 
     # ---- reduce over ranks (max time)
     ms = float(np.mean(step_ms)); e2e = float(np.mean(e2e_ms))
@@ -254,13 +270,15 @@ def run_ours(args, rank, world, local_rank):
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
         "stage_ms": {n: float(np.mean(v)) for n, v in stage_ms.items()},
         "roofline": {"kernel": "il_prefill_attn (K/V append + attention)", "bound": bound, "achieved": achieved,
-                     "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": None,
+                     "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": ncu_traffic()[0],
+                     "traffic_src": ncu_traffic()[1],
                      "peak_src": pk["src"] + (" burst bf16" if bound == "tensor" else ""),
                      "flops_per_step": float(fl.mean()), "bytes_per_step": float(by.mean()),
                      "t_star_ms": float(np.maximum(t_tc, t_hbm).mean() * 1e3)},
         "e2e": {"value": B_all / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
         "gpu_launches": int(launches),
+        "timed_steps": {"device": K, "e2e": K, "order": "alternating"},
         "clocks": clk,
         "wall_s_timed": wall,
     }
@@ -373,8 +391,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-guard", action="store_true")
