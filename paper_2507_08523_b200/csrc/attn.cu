@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(256) k_kv_append(Ctx c, uint32_t B, const int3
 }
 
 // one CTA: tiles_i = ceil(S_i / tq); exclusive scan into tile_off; total into sc->n_tiles
-__global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, uint32_t tq) {
+// (+ cascade bookkeeping: suffix rows, dense M-tiles, shared-block bound = request 0's hits)
+__global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q,
+                                                    const int32_t* __restrict__ prefix_len, uint32_t tq,
+                                                    uint32_t cascade) {
   __shared__ uint32_t s[1024];
   const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
   uint32_t n = 0;
@@ -53,7 +56,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int
     for (uint32_t t = 0; t < nt; ++t) c.tile_req[acc + t] = i;
     acc += nt;
   }
-  if (tid == 1023) { c.tile_off[B] = s[1023]; c.sc->n_tiles = s[1023]; }
+  if (tid == 1023) {
+    c.tile_off[B] = s[1023]; c.sc->n_tiles = s[1023];
+    const uint32_t tot = (uint32_t)cu_q[B];
+    c.sc->q_total = tot;
+    c.sc->n_dense = cdiv(tot, tq);
+    c.sc->shared_blk = cascade ? (uint32_t)prefix_len[0] / BS : 0u;
+  }
 }
 
 __device__ __forceinline__ uint32_t tile_owner(const uint32_t* __restrict__ tile_off, uint32_t B, uint32_t t) {
@@ -202,7 +211,7 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
     return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
   }
   if (g * SIMPLE_TQ > 128) { set_error("bring-up attention: Hq/Hkv > 8 unsupported"); return IL_ERR_ARG; }
-  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, SIMPLE_TQ);
+  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, SIMPLE_TQ, 0u);
   const uint32_t R = SIMPLE_TQ * g;
   const size_t smem = ((size_t)R * d + SIMPLE_KC * (d + 1) + SIMPLE_KC * d) * sizeof(float);
   if (d == 128) {

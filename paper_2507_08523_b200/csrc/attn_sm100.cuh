@@ -230,14 +230,29 @@ constexpr uint32_t IDESC_PV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | 
 // pages (the instruction and often the demonstrations, P:182 / PAIR rule 1), counted by nsh
 // (k_pair_scan); a shared KV tile is loaded once and feeds both Q tiles.
 struct Tile {
-  uint32_t i, mt, P, S, r0, ntok, n_kv, nblk;
+  uint32_t i, mt, P, S, r0, ntok, kv0, n_kv, nblk;
   bool valid;
 };
+// Cascade: NC = the leading 128-key KV tiles every request of the batch reads
+// from the same cached pages (the instruction).  Phase 1 runs them once over DENSE
+// M-tiles of all suffix rows of the batch (no padding between requests, no mask: every suffix
+// position lies past the shared prefix) and leaves (O / l in `out`, m + log2 l in attn_ml);
+// phase 2 runs each request's own M-tiles over KV tiles NC.. with the softmax state
+// initialised from that partial.  NC = 0: phase 2 alone is the whole attention.
 __device__ __forceinline__ Tile decode_tile(const Ctx& c, const int32_t* __restrict__ cu_q,
-                                            const int32_t* __restrict__ prefix_len, uint32_t t, uint32_t TQ) {
+                                            const int32_t* __restrict__ prefix_len, uint32_t t, uint32_t TQ,
+                                            uint32_t phase, uint32_t NC) {
   Tile T;
+  if (phase == 1) {
+    T.valid = t < c.sc->n_dense;
+    const uint32_t tot = c.sc->q_total;
+    T.i = 0; T.mt = t; T.P = 0; T.r0 = 0; T.S = tot;
+    T.ntok = T.valid ? min(TQ, tot - t * TQ) : 0;
+    T.kv0 = 0; T.n_kv = T.valid ? NC : 0; T.nblk = 8 * NC;
+    return T;
+  }
   T.valid = t < c.sc->n_tiles;
-  if (!T.valid) { T.i = T.mt = T.P = T.S = T.r0 = T.ntok = T.n_kv = T.nblk = 0; return T; }
+  if (!T.valid) { T.i = T.mt = T.P = T.S = T.r0 = T.ntok = T.kv0 = T.n_kv = T.nblk = 0; return T; }
   const uint32_t i = c.tile_req[t];
   T.i = i;
   T.mt = t - c.tile_off[i];
@@ -245,7 +260,8 @@ __device__ __forceinline__ Tile decode_tile(const Ctx& c, const int32_t* __restr
   T.r0 = (uint32_t)cu_q[i];
   T.S = (uint32_t)cu_q[i + 1] - T.r0;
   T.ntok = min(TQ, T.S - T.mt * TQ);
-  T.n_kv = (T.P + T.mt * TQ + T.ntok - 1) / BN + 1;
+  T.kv0 = NC;
+  T.n_kv = (T.P + T.mt * TQ + T.ntok - 1) / BN + 1 - NC;
   T.nblk = cdiv(T.P + T.S, BS);
   return T;
 }
@@ -255,13 +271,13 @@ struct Pair {
 };
 __device__ __forceinline__ Pair decode_pair(const Ctx& c, const int32_t* __restrict__ cu_q,
                                             const int32_t* __restrict__ prefix_len, uint32_t w, uint32_t Hkv,
-                                            uint32_t TQ) {
+                                            uint32_t TQ, uint32_t phase, uint32_t NC) {
   Pair p;
   const uint32_t u = w / Hkv;
   p.kh = w % Hkv;
-  p.a = decode_tile(c, cu_q, prefix_len, 2 * u, TQ);
-  p.b = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ);
-  p.nsh = p.b.valid ? c.pair_nsh[u] : 0;
+  p.a = decode_tile(c, cu_q, prefix_len, 2 * u, TQ, phase, NC);
+  p.b = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ, phase, NC);
+  p.nsh = p.b.valid ? (phase == 1 ? NC : c.pair_nsh[u]) : 0;
   p.nload = p.a.n_kv + (p.b.valid ? p.b.n_kv - p.nsh : 0);
   return p;
 }
@@ -288,7 +304,7 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
 __global__ void __launch_bounds__(THREADS, 1)
     k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
                  const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                 float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
+                 float scale_log2, uint32_t g, uint32_t TQ, uint32_t phase, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -299,7 +315,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
-  const uint32_t n_items = cdiv(c.sc->n_tiles, 2) * Hkv;
+  const uint32_t NC = c.sc->shared_blk / 8;
+  // (phase 1 with NC = 0 has nothing to do: every item would have zero KV tiles)
+  const uint32_t n_items = phase == 1 ? (NC ? cdiv(c.sc->n_dense, 2) * Hkv : 0u) : cdiv(c.sc->n_tiles, 2) * Hkv;
+  const bool init_o = phase == 2 && NC > 0;             // phase 2 continues phase 1's partial
 
   if (threadIdx.x == 0) {
     mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
@@ -336,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t ring = sbase + (is_k ? OFF_K : OFF_V);
     uint32_t lc = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
       if (is_k && lane == 0) {
         if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
         const uint32_t qbytes = 2 * 128 * g * TQ;
@@ -355,7 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         load_info(pr, l, n, req, tgt);
         const uint32_t nblk = req == pr.a.i ? pr.a.nblk : pr.b.nblk;
         const int32_t* bt = block_table + (size_t)req * c.max_blocks;
-        const uint32_t blk = n * 8 + (lane & 7);
+        const uint32_t blk = (pr.a.kv0 + n) * 8 + (lane & 7);
         const int32_t page = blk < nblk ? __ldg(bt + blk) : __ldg(bt);
         const uint32_t s = lc % nst, u = lc / nst;
         if (lane == 0) {
@@ -381,7 +400,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t lc = 0, it = 0, cnt0 = 0, cnt1 = 0;
     uint32_t vus = 0;                                 // 2-bit PV-user counters per load (lc % 8)
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
       uint32_t last0 = 0, last1 = 0;
       for (uint32_t l = 0; l < pr.nload; ++l) {
         uint32_t n_, r_, t_;
@@ -400,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // pending PV per Q tile (S is single-buffered: PV(n) must precede QK(n+1)):
       // (load counter, tile count)
       uint32_t q0n = 0, q0l = 0, q0c = 0, q1n = 0, q1l = 0, q1c = 0;
-      bool first0 = true, first1 = true, o_ready = it == 0;
+      bool first0 = !init_o, first1 = !init_o, o_ready = it == 0;
       auto pv_one = [&](const uint32_t x) {
         const uint32_t pl = x ? q1l : q0l, pc = x ? q1c : q0c, vs = pl % NSTV;
         if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
@@ -451,6 +470,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit_w(bar(K_FREE + ks));
         if (l + 1 == pr.nload) commit_w(bar(Q_FREE));
       }
+      if (pr.nload == 0) commit_w(bar(Q_FREE));        // (not reached: every item has a KV tile)
       while (q0n) pv_one(0);
       while (q1n) pv_one(1);
       if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
@@ -463,19 +483,50 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t s_tmem = tmem + lane_addr + 128 * x, o_tmem = tmem + lane_addr + 256 + 128 * x;
     uint32_t it = 0, cnt = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ);
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
       const Tile& T = x ? pr.b : pr.a;
       const uint32_t t = r / g, hh = r % g;
       const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
       const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
+      const size_t orow = ((size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh);
       float m_used = -INFINITY, l = 0.f;
+      if (init_o) {
+        // continue phase 1's partial: state (m + log2 l, 1, O / l) is the same softmax state.
+        // (warp-uniform: tcgen05.st is .sync.aligned; padding rows store zeros)
+        uint4 raw[16];
+        if (valid) {
+          m_used = c.attn_ml[orow];
+          l = 1.f;
+          const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) raw[j] = src[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) raw[j] = make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t w4[4] = {raw[4 * q + j].x, raw[4 * q + j].y, raw[4 * q + j].z, raw[4 * q + j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
+              ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+            }
+          }
+          tmem_st32(o_tmem + 32 * q, ov);
+        }
+        tmem_wait_st();
+      }
       const uint32_t ntl = T.valid ? T.n_kv : 0;
       for (uint32_t n = 0; n < ntl; ++n, ++cnt) {
         mbar_wait(bar(S_FULL + x), cnt & 1);
         if (r == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
         tc_fence_after();
-        const uint32_t key0 = n * BN;
-        const bool masked = key0 + BN - 1 > pos_q;
+        const uint32_t key0 = (T.kv0 + n) * BN;
+        const bool masked = phase == 2 && key0 + BN - 1 > pos_q;
         float a[64];
         // pass 1: row max over both 64-column halves
         tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
@@ -504,7 +555,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float mx2 = mx * scale_log2;
         bool need = false;
         float factor = 1.f;
-        if (n == 0) {
+        if (m_used == -INFINITY) {
           m_used = mx2;
         } else if (mx2 > m_used + 8.f) {
           need = true;
@@ -568,7 +619,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       if (T.valid) {
         const float inv = 1.f / l;
-        const size_t orow = ((size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float ov[32];
@@ -587,7 +637,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-        if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+        if (valid && phase == 1) c.attn_ml[orow] = m_used + __log2f(l);
+        else if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
       }
       tc_fence_before();
       mbar_arrive(bar(O_FREE));
@@ -604,10 +655,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 __global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restrict__ cu_q,
                                                    const int32_t* __restrict__ prefix_len,
                                                    const int32_t* __restrict__ block_table, uint32_t TQ) {
-  const uint32_t lane = threadIdx.x & 31, nt = c.sc->n_tiles;
+  const uint32_t lane = threadIdx.x & 31, nt = c.sc->n_tiles, NC = c.sc->shared_blk / 8;
   for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < cdiv(nt, 2);
        u += (gridDim.x * blockDim.x) >> 5) {
-  const Tile A = decode_tile(c, cu_q, prefix_len, 2 * u, TQ), Bt = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ);
+  const Tile A = decode_tile(c, cu_q, prefix_len, 2 * u, TQ, 2, NC);
+  const Tile Bt = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ, 2, NC);
   uint32_t nsh = 0;
   if (Bt.valid) {
     const uint32_t ntile = min(A.n_kv, Bt.n_kv);
@@ -616,7 +668,7 @@ __global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restr
     // tile n is shared iff its 8 page ids agree (blocks past a request's end read page bt[0])
     uint32_t n = 0;
     for (; n < ntile; n += 4) {
-      const uint32_t tn = n + (lane >> 3), blk = tn * 8 + (lane & 7);
+      const uint32_t tn = n + (lane >> 3), blk = (NC + tn) * 8 + (lane & 7);
       bool eq = true;
       if (tn < ntile) {
         const int32_t pa = blk < A.nblk ? ba[blk] : ba[0], pb = blk < Bt.nblk ? bb[blk] : bb[0];
@@ -628,6 +680,26 @@ __global__ void __launch_bounds__(256) k_pair_scan(Ctx c, const int32_t* __restr
     nsh = min(n, ntile);
   }
   if (lane == 0) c.pair_nsh[u] = nsh;
+  }
+}
+
+// k_shared_scan: blocks every request shares with request 0 (same page ids, within both hit
+// ranges); sc->shared_blk starts at request 0's hit count (k_tile_scan).  Warp per request.
+__global__ void __launch_bounds__(256) k_shared_scan(Ctx c, uint32_t B, const int32_t* __restrict__ prefix_len,
+                                                     const int32_t* __restrict__ block_table) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int32_t* b0 = block_table;
+  for (uint32_t i = 1 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < B; i += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t lim = min((uint32_t)prefix_len[i] / BS, *(volatile uint32_t*)&c.sc->shared_blk);
+    const int32_t* bi = block_table + (size_t)i * c.max_blocks;
+    uint32_t n = 0;
+    for (; n < lim; n += 32) {
+      const uint32_t b = n + lane;
+      const bool ne = b < lim && bi[b] != b0[b];
+      const uint32_t bad = __ballot_sync(~0u, ne);
+      if (bad) { n += __ffs(bad) - 1; break; }
+    }
+    if (lane == 0 && n < lim) atomicMin(&c.sc->shared_blk, n);
   }
 }
 
@@ -680,17 +752,22 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { set_error("tensor map (kv) encode failed"); return IL_ERR_CUDA; }
   }
-  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, TQ);
+  const char* ce = getenv("IL_CASCADE");
+  const bool cascade = !(ce && ce[0] == '0');
+  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
+  if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
   k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
   static bool attr = false;
   if (!attr) {
     IL_CUDA(cudaFuncSetAttribute(k_attn_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
-  k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out, lse,
-                                                        scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
-  IL_LAUNCH_CHECK("k_attn_sm100");
-  c->launches += 3;
+  for (uint32_t phase = cascade ? 1 : 2; phase <= 2; ++phase) {
+    k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out,
+                                                          lse, scale * 1.4426950408889634f, g, TQ, phase, tq, tk, tv);
+    IL_LAUNCH_CHECK("k_attn_sm100");
+  }
+  c->launches += cascade ? (B > 1 ? 5 : 4) : 3;
   return IL_OK;
 }
 

@@ -340,7 +340,7 @@ static inline il_status attn_sm100s_launch(Ctx* c, uint32_t B, const int32_t* cu
       set_error("tensor map (kv) encode failed"); return IL_ERR_CUDA;
     }
   }
-  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, TQ);
+  k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, 0u);
   static bool attr = false;
   if (!attr) {
     IL_CUDA(cudaFuncSetAttribute(S::k_attn_sm100s, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES));

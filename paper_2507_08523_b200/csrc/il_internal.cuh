@@ -36,7 +36,7 @@ struct DevScalars {
   uint32_t rebuild_flag;
   uint32_t n_tiles;          // attention work items
   uint32_t instr_hits;       // per batch: leading resident (verified) instruction blocks
-  uint32_t pad0;
+  uint32_t n_dense;          // attention: dense M-tiles over all suffix rows (cascade phase 1)
   uint64_t stamp_min;        // eviction radix-select scratch
   uint64_t stamp_max;
   uint64_t sel_prefix;       // selected key prefix
@@ -44,7 +44,9 @@ struct DevScalars {
   uint32_t sel_remaining;
   uint32_t sel_shift;
   uint32_t cand;             // eviction candidates
-  uint32_t pad1[17];
+  uint32_t q_total;          // attention: suffix rows of the batch (cu_q[B])
+  uint32_t shared_blk;       // attention: blocks every request shares (same pages, all cached)
+  uint32_t pad1[15];
 };
 
 struct Ctx {
@@ -87,6 +89,7 @@ struct Ctx {
   uint32_t *tile_off;        // attention work decomposition
   uint32_t *tile_req;        // attention M-tile -> request
   uint32_t *pair_nsh;        // attention M-tile pair -> leading shared KV tiles
+  float *attn_ml;            // cascade: per row log2 softmax mass of the shared-prefix partial
   uint64_t *evicted_list;
   uint32_t *guard_prompt;    // guard: DS_current prompt rows
   // pointers remembered between calls (caller-owned)

@@ -89,3 +89,19 @@ def test_attention_long_prompts():
     sp = StreamSpec(n_logs=4096, n_templates=300, zipf=1.1, seed=4000, pool_seed=4001, k=5, B=8, n_instr=1836,
                     T=4096, C=4096, max_prompt_tokens=2560, Hq=32, Hkv=8, d=128, ramp=(1,))
     run(sp, n_batches=3, sample=3, max_rows=48)
+
+
+def _long(B, ramp=(1,)):
+    return StreamSpec(n_logs=4096, n_templates=300, zipf=1.1, seed=4000, pool_seed=4001, k=5, B=B, n_instr=1836,
+                      T=4096, C=8192, max_prompt_tokens=2560, Hq=32, Hkv=8, d=128, ramp=ramp)
+
+
+def test_attention_long_prompts_wide_batch():
+    # B = 64: the cascade's dense phase-1 M-tiles span several requests each
+    run(_long(64), n_batches=2, sample=10, max_rows=48)
+
+
+def test_attention_long_prompts_no_cascade(monkeypatch):
+    # IL_CASCADE=0: one phase over each request's whole prefix (the NC = 0 path)
+    monkeypatch.setenv("IL_CASCADE", "0")
+    run(_long(16), n_batches=2, sample=6, max_rows=48)
