@@ -10,6 +10,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libinferlog_b200.so")
+# profiling builds of the same sources (scripts/attn_variants.py) may be selected by name
+if os.environ.get("IL_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, "variants", f"libinferlog_b200_{os.environ['IL_LIB_VARIANT']}.so")
 
 IL_OK, IL_ERR_ARG, IL_ERR_CAPACITY, IL_ERR_STATE, IL_ERR_INTERNAL, IL_ERR_CUDA = range(6)
 STATUS_NAMES = {0: "IL_OK", 1: "IL_ERR_ARG", 2: "IL_ERR_CAPACITY", 3: "IL_ERR_STATE",

@@ -31,14 +31,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
     """trace=True builds libinferlog_b200_trace.so with per-tile clock64 stamps in the
-    attention kernel (profiling only; never loaded by the product path)."""
-    lib = LIB.replace(".so", "_trace.so") if trace else LIB
-    extra = ["-DIL_ATTN_TRACE"] if trace else []
-    if not force and not trace and up_to_date():
+    attention kernel; variant="name" with defines=("-DX=Y", ...) builds
+    variants/libinferlog_b200_name.so (profiling only; never loaded by the product path)."""
+    if variant:
+        os.makedirs(os.path.join(HERE, "variants"), exist_ok=True)
+        lib = os.path.join(HERE, "variants", f"libinferlog_b200_{variant}.so")
+    else:
+        lib = LIB.replace(".so", "_trace.so") if trace else LIB
+    extra = (["-DIL_ATTN_TRACE"] if trace else []) + list(defines)
+    if not force and not trace and not variant and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build_trace" if trace else "build")
+    objdir = os.path.join(HERE, f"build_{variant}" if variant else ("build_trace" if trace else "build"))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -188,7 +188,6 @@ __global__ void __launch_bounds__(256) k_attn_simple(Ctx c, uint32_t B, const in
 }  // namespace il
 
 #include "attn_sm100.cuh"
-#include "attn_sm100_single.cuh"
 
 using namespace il;
 
@@ -205,9 +204,6 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
   IL_LAUNCH_CHECK("k_kv_append");
   c->launches += 1;
   if (attn_sm100_supported(c)) {
-    const char* kv = getenv("IL_ATTN_KERNEL");
-    if (kv && kv[0] == 's')
-      return attn_sm100s_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
     return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
   }
   if (g * SIMPLE_TQ > 128) { set_error("bring-up attention: Hq/Hkv > 8 unsupported"); return IL_ERR_ARG; }
@@ -236,7 +232,7 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
 extern "C" il_status il_debug_trace(unsigned long long* out_h) {
   IL_CUDA(cudaDeviceSynchronize());
   IL_CUDA(cudaMemcpyFromSymbol(out_h, il::sm100::g_trace, sizeof(il::sm100::g_trace)));
-  IL_CUDA(cudaMemcpyFromSymbol(out_h + 8 * 4096, il::sm100::g_trace_item, sizeof(il::sm100::g_trace_item)));
+  IL_CUDA(cudaMemcpyFromSymbol(out_h + 16 * 4096, il::sm100::g_trace_item, sizeof(il::sm100::g_trace_item)));
   return IL_OK;
 }
 #endif

@@ -13,9 +13,9 @@
 //   O += P V       A = P (TMEM), B = V tile (smem, MN-major), D = O in TMEM
 // K and V stream through separate smem rings (K is released right after QK, V after its
 // last PV).  Two M-tiles share each CTA (see "work decomposition"): a KV tile both need is
-// loaded once, and their softmax warpgroups ping-pong against one tensor core.  Warp roles (persistent CTA per SM, 256 threads): warp 0 = TMA producer for Q and K,
-// warp 3 = TMA producer for V, warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
-// warps 4-11 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
+// loaded once.  Warp roles (persistent CTA per SM, 384 threads): warp 0 = TMA producer for K,
+// warp 3 = TMA producer for V, warp 1 = MMA issuer (warp-uniform, one elected lane), warp 2 =
+// TMEM allocator, then TMA producer for Q, warps 4-11 = softmax + epilogue.  Hand-offs are mbarriers; MMA completion is signalled with
 // tcgen05.commit; tcgen05.mma from one thread execute in order, which orders the reuse of S.
 // Softmax runs on two warpgroups (warps 4-7 and 8-11) that split each tile's key columns.
 #pragma once
@@ -30,10 +30,10 @@ namespace sm100 {
 
 #ifdef IL_ATTN_TRACE
 // debug build only (build.py --trace): per-tile clock64 stamps of each role in CTA 0
-__device__ unsigned long long g_trace[8][4096];
+__device__ unsigned long long g_trace[16][4096];
 __device__ unsigned int g_trace_item[1024][4];
 #define IL_TRACE(slot, idx) \
-  do { if (blockIdx.x == 0 && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
+  do { if (blockIdx.x == 0 && phase == 1 && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
 #else
 #define IL_TRACE(slot, idx) do { } while (0)
 #endif
@@ -45,19 +45,28 @@ constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf1
 constexpr uint32_t QTILE = 2 * CB;       // 128 x 128 bf16 = 32 KB
 constexpr uint32_t KCB = CB;             // one 64-column block of a 128-key K/V tile
 constexpr uint32_t KVTILE = 2 * KCB;     // 128 x 128 bf16 = 32 KB
-constexpr uint32_t NSTK = 3, NSTV = 2;   // K and V ring depths
+#ifndef IL_NSTK
+#define IL_NSTK 3
+#endif
+#ifndef IL_NSTV
+#define IL_NSTV 2
+#endif
+constexpr uint32_t NSTK = IL_NSTK, NSTV = IL_NSTV;   // K and V ring depths
 constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
 constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
 constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
 constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
-constexpr uint32_t NBAR = 20;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
+constexpr uint32_t NBAR = 10 + 2 * NSTK + 2 * NSTV;
+constexpr uint32_t OFF_XCH = OFF_BAR + 256;          // softmax half exchange: [2][2][128] fp32
+constexpr uint32_t SMEM_BYTES = OFF_XCH + 2 * 2 * 128 * 4;
 constexpr int THREADS = 384;
 constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
 // S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
-enum Bar { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = 5, V_FULL = 8, V_FREE = 10, S_FULL = 12, P_FULL = 14,
-           PV_DONE = 16, O_FULL = 18, O_FREE = 19 };
+enum Bar : uint32_t { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = K_FULL + NSTK, V_FULL = K_FREE + NSTK,
+                      V_FREE = V_FULL + NSTV, S_FULL = V_FREE + NSTV, P_FULL = S_FULL + 2, PV_DONE = P_FULL + 2,
+                      O_FULL = PV_DONE + 2, O_FREE = O_FULL + 1 };
+static_assert(O_FREE + 1 == NBAR, "barrier map");
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -71,14 +80,27 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or the
+// hint expires) instead of spinning and taking issue slots from the softmax warps on its SMSP.
+#ifndef IL_WAIT_HINT_NS
+#define IL_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done;
   do {
+#if IL_WAIT_HINT_NS > 0
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "n"(IL_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+#endif
   } while (!done);
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
@@ -175,24 +197,36 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA/ALU pipes (exp2 emulation, offloads the MUFU unit): x = j + f with j the
-// nearest integer (magic-number rounding), 2^f by a cubic on [-0.5, 0.5] (relative error
-// < 7e-5, far below the bf16 rounding of P), 2^j added to the exponent field.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;                   // 1.5 * 2^23
-  const float j = t - 12582912.f;
-  const float f = x - j;
-  float p = fmaf(f, 0.05550411f, 0.24022651f);
-  p = fmaf(p, f, 0.69314718f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-#ifndef IL_EXP_EMU_MASK
-#define IL_EXP_EMU_MASK 7                            // emulate elements with (j & mask) == mask
+// 2^x for a PAIR on the FMA pipe (exp2 emulation, offloads the MUFU unit) with packed fp32x2 ops: magic-number
+// rounding to j, cubic in f = x - j, 2^j added to the exponent field by one IMAD per element).
+#ifndef IL_EXP_EMU_PAIRS
+#define IL_EXP_EMU_PAIRS 0x4A                        // pairs (j/2) % 8 in {1, 3, 6}: 3 of 8 emulated
 #endif
-__device__ __forceinline__ float ex2_mixed(float x, int j) {
-  return ((j & IL_EXP_EMU_MASK) == IL_EXP_EMU_MASK) ? ex2_poly(x) : ex2(x);
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  uint32_t t0, t1, p0, p1;
+  asm("{ .reg .b64 x, t, j, f, p, c, m, nm, k3, k2, k1, one;\n\t"
+      "mov.b64 x, {%4, %5};\n\t"
+      "mov.b64 m, {0f4B400000, 0f4B400000};\n\t"            // 1.5 * 2^23
+      "mov.b64 nm, {0fCB400000, 0fCB400000};\n\t"
+      "add.rn.f32x2 t, x, m;\n\t"                           // t = x + M (rounds x to an integer)
+      "add.rn.f32x2 j, t, nm;\n\t"                          // j = t - M
+      "mov.b64 c, {0fBF800000, 0fBF800000};\n\t"
+      "fma.rn.f32x2 f, j, c, x;\n\t"                        // f = x - j in [-0.5, 0.5]
+      "mov.b64 k3, {0f3D61FBB0, 0f3D61FBB0};\n\t"           // minimax cubic for 2^f on [-1/2, 1/2]
+      "mov.b64 k2, {0f3E786F0F, 0f3E786F0F};\n\t"           // (relative error 7.5e-5)
+      "mov.b64 k1, {0f3F31798D, 0f3F31798D};\n\t"
+      "mov.b64 one, {0f3F7FFB49, 0f3F7FFB49};\n\t"
+      "fma.rn.f32x2 p, f, k3, k2;\n\t"
+      "fma.rn.f32x2 p, p, f, k1;\n\t"
+      "fma.rn.f32x2 p, p, f, one;\n\t"
+      "mov.b64 {%0, %1}, t;\n\t"
+      "mov.b64 {%2, %3}, p; }"
+      : "=r"(t0), "=r"(t1), "=r"(p0), "=r"(p1) : "f"(x0), "f"(x1));
+  // the low mantissa bits of t hold j + 2^22 (mod 2^9); (t << 23) = j << 23 (mod 2^32)
+  y0 = __uint_as_float(p0 + (t0 << 23));
+  y1 = __uint_as_float(p1 + (t1 << 23));
 }
 
 // packed fp32x2 (FFMA2 / FADD2 on sm_100a): two elements per instruction
@@ -236,9 +270,10 @@ struct Tile {
 // Cascade: NC = the leading 128-key KV tiles every request of the batch reads
 // from the same cached pages (the instruction).  Phase 1 runs them once over DENSE
 // M-tiles of all suffix rows of the batch (no padding between requests, no mask: every suffix
-// position lies past the shared prefix) and leaves (O / l in `out`, m + log2 l in attn_ml);
-// phase 2 runs each request's own M-tiles over KV tiles NC.. with the softmax state
-// initialised from that partial.  NC = 0: phase 2 alone is the whole attention.
+// position lies past the shared prefix).  Phase 2 runs FIRST: each request's own M-tiles over KV
+// tiles NC.. (the causal part), leaving (O / l in `out`, m + log2 l in attn_ml); phase 1 starts
+// each row from that partial (its items are long, so the extra load is amortised) and writes
+// the result.  NC = 0: phase 2 alone is the whole attention.
 __device__ __forceinline__ Tile decode_tile(const Ctx& c, const int32_t* __restrict__ cu_q,
                                             const int32_t* __restrict__ prefix_len, uint32_t t, uint32_t TQ,
                                             uint32_t phase, uint32_t NC) {
@@ -318,7 +353,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t NC = c.sc->shared_blk / 8;
   // (phase 1 with NC = 0 has nothing to do: every item would have zero KV tiles)
   const uint32_t n_items = phase == 1 ? (NC ? cdiv(c.sc->n_dense, 2) * Hkv : 0u) : cdiv(c.sc->n_tiles, 2) * Hkv;
-  const bool init_o = phase == 2 && NC > 0;             // phase 2 continues phase 1's partial
+  const bool cascade = NC > 0;                          // phase 2 leaves a partial that phase 1 merges
 
   if (threadIdx.x == 0) {
     mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
@@ -326,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
     for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
     for (int x = 0; x < 2; ++x) {
-      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), 128); mbar_init(bar(PV_DONE + x), 1);
+      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), SM_THREADS); mbar_init(bar(PV_DONE + x), 1);
     }
     mbar_init(bar(O_FULL), 1); mbar_init(bar(O_FREE), SM_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -346,8 +381,33 @@ __global__ void __launch_bounds__(THREADS, 1)
   // TMEM columns: S_A [0,128), S_B [128,256) (the P of a tile overwrites the first 64 columns
   // of its S as packed bf16), O_A [256,384), O_B [384,512).
 
+#ifndef IL_Q_WARP
+#define IL_Q_WARP 2
+#endif
+  if (IL_Q_WARP == 2 && warp == 2) {
+    // ============ Q producer: the next item's Q tiles load as soon as the last QK of the
+    // current item has read Q (the K / V producers run ahead independently) ============
+    uint32_t it = 0;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      if (lane == 0) {
+        const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
+        if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
+        const uint32_t qbytes = 2 * 128 * g * TQ;
+        mbar_expect_tx(bar(Q_FULL), pr.b.valid ? 2 * qbytes : qbytes);
+        const int ra = (int)(pr.a.r0 + pr.a.mt * TQ);
+        tma_load_3d(sbase + OFF_QA, &tm_q, 0, (int)(pr.kh * g), ra, bar(Q_FULL));
+        tma_load_3d(sbase + OFF_QA + CB, &tm_q, 64, (int)(pr.kh * g), ra, bar(Q_FULL));
+        if (pr.b.valid) {
+          const int rb = (int)(pr.b.r0 + pr.b.mt * TQ);
+          tma_load_3d(sbase + OFF_QB, &tm_q, 0, (int)(pr.kh * g), rb, bar(Q_FULL));
+          tma_load_3d(sbase + OFF_QB + CB, &tm_q, 64, (int)(pr.kh * g), rb, bar(Q_FULL));
+        }
+      }
+      __syncwarp();
+    }
+  }
   if (warp == 0 || warp == 3) {
-    // ============ TMA producers: warp 0 = Q tiles + K tiles, warp 3 = V tiles ============
+    // ============ TMA producers: warp 0 = K tiles, warp 3 = V tiles ============
     const bool is_k = warp == 0;
     const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
     const uint32_t nst = is_k ? NSTK : NSTV;
@@ -356,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t lc = 0, it = 0;
     for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      if (is_k && lane == 0) {
+      if (IL_Q_WARP == 0 && is_k && lane == 0) {        // (alternative: Q issued by the K producer)
         if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
         const uint32_t qbytes = 2 * 128 * g * TQ;
         mbar_expect_tx(bar(Q_FULL), pr.b.valid ? 2 * qbytes : qbytes);
@@ -380,9 +440,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           if (lc >= nst) mbar_wait(bar(free0 + s), (u - 1) & 1);
           IL_TRACE(is_k ? 0 : 1, lc & 4095);
+#ifdef IL_DBG_NOKVTMA
+          if (lc >= nst) mbar_arrive(bar(full0 + s)); else   // timing experiment only: stale K/V
+#endif
           mbar_expect_tx(bar(full0 + s), KVTILE);
         }
         __syncwarp();
+#ifdef IL_DBG_NOKVTMA
+        if (lc >= nst) continue;
+#endif
         if (lane < 16) {                                 // lane = (page, column half)
           const uint32_t p = lane & 7, h = lane >> 3;
           const int row = (int)(((uint32_t)page * Hkv + pr.kh) * BS);
@@ -410,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       mbar_wait(bar(Q_FULL), it & 1);
 #ifdef IL_ATTN_TRACE
-      if (blockIdx.x == 0 && it < 1024 && lane == 0) {
+      if (blockIdx.x == 0 && phase == 1 && it < 1024 && lane == 0) {
         g_trace_item[it][0] = lc; g_trace_item[it][1] = pr.nload; g_trace_item[it][2] = pr.nsh;
         g_trace_item[it][3] = pr.a.n_kv | (pr.b.n_kv << 16);
       }
@@ -419,7 +485,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // pending PV per Q tile (S is single-buffered: PV(n) must precede QK(n+1)):
       // (load counter, tile count)
       uint32_t q0n = 0, q0l = 0, q0c = 0, q1n = 0, q1l = 0, q1c = 0;
-      bool first0 = !init_o, first1 = !init_o, o_ready = it == 0;
+      bool first0 = phase != 1, first1 = phase != 1, o_ready = it == 0;   // phase 1 accumulates onto the partial
       auto pv_one = [&](const uint32_t x) {
         const uint32_t pl = x ? q1l : q0l, pc = x ? q1c : q0c, vs = pl % NSTV;
         if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
@@ -477,155 +543,213 @@ __global__ void __launch_bounds__(THREADS, 1)
       commit_w(bar(O_FULL));
     }
   } else if (warp >= 4) {
-    // ====== softmax + epilogue: warpgroup x owns Q tile x (A: warps 4-7, B: warps 8-11) ======
-    const uint32_t sm_t = threadIdx.x - 128, x = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
+    // ====== softmax + epilogue: thread = (row r, key half hc); both warpgroups work on every S tile ======
+    // Tiles are taken in the MMA warp's issue order (per load: A then B).  Each thread owns 64 of
+    // the 128 key columns of its row; the two halves exchange their partial row max through
+    // shared memory (double buffered by tile parity, one named barrier per tile), so one tile's
+    // softmax runs on all 8 warps and its latency (the critical path S -> P -> PV -> next S) halves.
+    const uint32_t sm_t = threadIdx.x - 128, hc = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
     const uint32_t lane_addr = (32 * q4) << 16;
-    const uint32_t s_tmem = tmem + lane_addr + 128 * x, o_tmem = tmem + lane_addr + 256 + 128 * x;
-    uint32_t it = 0, cnt = 0;
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      const Tile& T = x ? pr.b : pr.a;
+    float* xch = reinterpret_cast<float*>(smem + OFF_XCH);   // [2 parity][2 halves][128 rows]
+    uint32_t it = 0, cnt0 = 0, cnt1 = 0, par = 0;
+    // phase 1: the partial of an item's rows is fetched one item ahead (issued before the
+    // previous epilogue waits for its last PV) so its latency stays off the critical path
+    uint4 pf_raw[2][8];
+    float pf_m[2];
+    auto prefetch = [&](uint32_t wn) {
+      const Pair pn = decode_pair(c, cu_q, prefix_len, wn, Hkv, TQ, phase, NC);
       const uint32_t t = r / g, hh = r % g;
-      const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
-      const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
-      const size_t orow = ((size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh);
-      float m_used = -INFINITY, l = 0.f;
-      if (init_o) {
-        // continue phase 1's partial: state (m + log2 l, 1, O / l) is the same softmax state.
-        // (warp-uniform: tcgen05.st is .sync.aligned; padding rows store zeros)
-        uint4 raw[16];
-        if (valid) {
-          m_used = c.attn_ml[orow];
-          l = 1.f;
-          const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) raw[j] = src[j];
+      for (int x = 0; x < 2; ++x) {
+        const Tile& T = x ? pn.b : pn.a;
+        pf_m[x] = -INFINITY;
+        if (T.valid && r < g * TQ && t < T.ntok) {
+          const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pn.kh * g + hh;
+          pf_m[x] = c.attn_ml[orow];
+          const uint4* src = reinterpret_cast<const uint4*>(out + orow * D + 64 * hc);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pf_raw[x][j] = src[j];
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) raw[j] = make_uint4(0u, 0u, 0u, 0u);
+          for (int j = 0; j < 8; ++j) pf_raw[x][j] = make_uint4(0u, 0u, 0u, 0u);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float ov[32];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t w4[4] = {raw[4 * q + j].x, raw[4 * q + j].y, raw[4 * q + j].z, raw[4 * q + j].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
-              ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
-            }
-          }
-          tmem_st32(o_tmem + 32 * q, ov);
-        }
-        tmem_wait_st();
       }
-      const uint32_t ntl = T.valid ? T.n_kv : 0;
-      for (uint32_t n = 0; n < ntl; ++n, ++cnt) {
-        mbar_wait(bar(S_FULL + x), cnt & 1);
-        if (r == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
-        tc_fence_after();
-        const uint32_t key0 = (T.kv0 + n) * BN;
-        const bool masked = phase == 2 && key0 + BN - 1 > pos_q;
-        float a[64];
-        // pass 1: row max over both 64-column halves
-        tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
-        tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
-        tmem_wait_ld();
-        if (masked) {
+    };
+#ifndef IL_INIT_PREFETCH
+#define IL_INIT_PREFETCH 0
+#endif
+    if (phase == 1 && blockIdx.x < n_items) prefetch(blockIdx.x);
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
+      const uint32_t t = r / g, hh = r % g;
+      bool valid[2];
+      uint32_t pos_q[2];
+      size_t orow[2];
+      float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
 #pragma unroll
-          for (int j = 0; j < 64; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
-        }
-        float mxa[8];
+      for (int x = 0; x < 2; ++x) {
+        const Tile& T = x ? pr.b : pr.a;
+        valid[x] = T.valid && (r < g * TQ) && (t < T.ntok);
+        pos_q[x] = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
+        orow[x] = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh;
+      }
+      if (!IL_INIT_PREFETCH && phase == 1) prefetch(w);
+      if (phase == 1) {
+        // continue phase 2's partial of these rows (prefetched during the previous item's
+        // epilogue): the state (m + log2 l, 1, O / l) is the same softmax state (the mass 1 goes
+        // to half 0's partial sum).  Warp-uniform: tcgen05.st is .aligned; padding rows store zeros.
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mxa[q] = a[q];
+        for (int x = 0; x < 2; ++x) {
+          const Tile& T = x ? pr.b : pr.a;
+          if (!T.valid) continue;                        // uniform over the CTA
+          if (valid[x]) {
+            m_used[x] = pf_m[x];
+            l[x] = hc == 0 ? 1.f : 0.f;
+          }
 #pragma unroll
-        for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
-        tmem_ld32(s_tmem + 64, *reinterpret_cast<float(*)[32]>(&a[0]));
-        tmem_ld32(s_tmem + 96, *reinterpret_cast<float(*)[32]>(&a[32]));
-        tmem_wait_ld();
-        if (masked) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) if (key0 + 64 + j > pos_q) a[j] = -INFINITY;
-        }
-#pragma unroll
-        for (int j = 0; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
-        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-        const float mx2 = mx * scale_log2;
-        bool need = false;
-        float factor = 1.f;
-        if (m_used == -INFINITY) {
-          m_used = mx2;
-        } else if (mx2 > m_used + 8.f) {
-          need = true;
-          factor = ex2(m_used - mx2);
-          m_used = mx2;
-          l *= factor;
-        }
-        if (__any_sync(~0u, need)) {
-          // lazy rescale of this warp's O rows once the previous tile's PV has landed
-          mbar_wait(bar(PV_DONE + x), (cnt - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 2; ++q) {
             float ov[32];
-            tmem_ld32(o_tmem + 32 * q, ov);
-            tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) ov[j] *= factor;
-            tmem_st32(o_tmem + 32 * q, ov);
+            for (int j = 0; j < 4; ++j) {
+              const uint4 u = pf_raw[x][4 * q + j];
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
+                ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+              }
+            }
+            tmem_st32(tmem + lane_addr + 256 + 128 * x + 64 * hc + 32 * q, ov);
           }
-          tmem_wait_st();
         }
-        const float negm = -m_used;
-        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t pk1[32], pk0[32];
-        // pass 2: keys 64..127 are in registers; then reload keys 0..63
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          float x0, x1;
-          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
-          const float p0 = ex2_mixed(x0, j), p1 = ex2_mixed(x1, j + 1);
-          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
-          pk1[j >> 1] = pack_bf16(p0, p1);
-        }
-        tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
-        tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
-        tmem_wait_ld();
-        if (masked) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
-        }
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          float x0, x1;
-          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
-          const float p0 = ex2_mixed(x0, j), p1 = ex2_mixed(x1, j + 1);
-          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
-          pk0[j >> 1] = pack_bf16(p0, p1);
-        }
-        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
-        // P (bf16 pairs, keys 0..127) overwrites TMEM columns [0, 64) of this S
-        tmem_st32u(s_tmem, pk0);
-        tmem_st32u(s_tmem + 32, pk1);
         tmem_wait_st();
-        tc_fence_before();
-        if (r == 0) IL_TRACE(5 + 2 * x, cnt & 4095);
-        mbar_arrive(bar(P_FULL + x));
       }
-      // epilogue: O / l -> bf16 rows of `out`, natural-log LSE
+      for (uint32_t ld = 0; ld < pr.nload; ++ld) {
+        uint32_t n, req_, tgt;
+        load_info(pr, ld, n, req_, tgt);
+#pragma unroll
+        for (uint32_t x = 0; x < 2; ++x) {
+          if (!(tgt & (1u << x))) continue;
+          const Tile& T = x ? pr.b : pr.a;
+          const uint32_t cnt = x ? cnt1++ : cnt0++;
+          const uint32_t s_tmem = tmem + lane_addr + 128 * x + 64 * hc;
+          const uint32_t o_tmem = tmem + lane_addr + 256 + 128 * x + 64 * hc;
+          mbar_wait(bar(S_FULL + x), cnt & 1);
+          if (r == 0 && hc == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
+          tc_fence_after();
+#ifdef IL_DBG_NOSOFTMAX
+          if (true) { tc_fence_before(); mbar_arrive(bar(P_FULL + x)); continue; }   // timing experiment only
+#endif
+          const uint32_t key0 = (T.kv0 + n) * BN + 64 * hc;
+          const bool masked = phase == 2 && key0 + 63 > pos_q[x];
+          float a[64];
+          tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
+          tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
+          tmem_wait_ld();
+          if (r == 0 && hc == 0 && x == 0) IL_TRACE(8, cnt & 4095);
+          if (masked) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) if (key0 + j > pos_q[x]) a[j] = -INFINITY;
+          }
+          float mxa[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mxa[q] = a[q];
+#pragma unroll
+          for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
+          const float mxh = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                  fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+#ifdef IL_DBG_NOXCH
+          const float mx = mxh;                          // timing experiment only
+#else
+          xch[(par * 2 + hc) * 128 + r] = mxh;
+          named_bar_sync(1, SM_THREADS);
+          const float mx = fmaxf(mxh, xch[(par * 2 + (hc ^ 1)) * 128 + r]);
+#endif
+          par ^= 1;
+          if (r == 0 && hc == 0 && x == 0) IL_TRACE(9, cnt & 4095);
+          const float mx2 = mx * scale_log2;
+          bool need = false;
+          float factor = 1.f;
+          if (m_used[x] == -INFINITY) {
+            m_used[x] = mx2;
+          } else if (mx2 > m_used[x] + 8.f) {
+            need = true;
+            factor = ex2(m_used[x] - mx2);
+            m_used[x] = mx2;
+            l[x] *= factor;
+          }
+          if (__any_sync(~0u, need)) {
+            // lazy rescale of this thread's 64 O columns once the previous tile's PV has landed
+            mbar_wait(bar(PV_DONE + x), (cnt - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              float ov[32];
+              tmem_ld32(o_tmem + 32 * q, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) ov[j] *= factor;
+              tmem_st32(o_tmem + 32 * q, ov);
+            }
+            tmem_wait_st();
+          }
+          // a fully masked row (no key yet) keeps p = 0: exp2(-inf - 0)
+          const float negm = m_used[x] == -INFINITY ? 0.f : -m_used[x];
+          float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+          uint32_t pk[32];
+#pragma unroll
+          for (int j = 0; j < 64; j += 2) {
+            float x0, x1;
+            ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+            float p0, p1;
+#ifdef IL_DBG_NOEXP
+            if (true) { p0 = x0; p1 = x1; } else   // timing experiment only: no exponential
+#endif
+            if ((IL_EXP_EMU_PAIRS >> ((j >> 1) & 7)) & 1) {
+              ex2_poly2(x0, x1, p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+            pk[j >> 1] = pack_bf16(p0, p1);
+          }
+          l[x] += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+          if (r == 0 && hc == 0 && x == 0) IL_TRACE(10, cnt & 4095);
+          // P (bf16 pairs) of keys [64hc, 64hc + 64) -> TMEM columns [32hc, 32hc + 32) of this S
+          // (half 0 read its S columns before the exchange barrier, so half 1 may overwrite them)
+          tmem_st32u(tmem + lane_addr + 128 * x + 32 * hc, pk);
+          tmem_wait_st();
+          if (r == 0 && hc == 0 && x == 0) IL_TRACE(11, cnt & 4095);
+          tc_fence_before();
+          if (r == 0 && hc == 0) IL_TRACE(5 + 2 * x, cnt & 4095);
+          mbar_arrive(bar(P_FULL + x));
+        }
+      }
+      if (IL_INIT_PREFETCH && phase == 1 && w + gridDim.x < n_items) prefetch(w + gridDim.x);
+      // epilogue: combine the two halves' row sums, O / l -> bf16 rows of `out`, natural-log LSE
+      // (two exchange rounds with the same parity protocol as the per-tile max exchange)
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        xch[(par * 2 + hc) * 128 + r] = l[x];
+        named_bar_sync(1, SM_THREADS);
+        l[x] += xch[(par * 2 + (hc ^ 1)) * 128 + r];
+        par ^= 1;
+      }
       mbar_wait(bar(O_FULL), it & 1);
       tc_fence_after();
-      if (T.valid) {
-        const float inv = 1.f / l;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+      for (int x = 0; x < 2; ++x) {
+        const Tile& T = x ? pr.b : pr.a;
+        if (!T.valid) continue;
+        const float inv = 1.f / l[x];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
           float ov[32];
-          tmem_ld32(o_tmem + 32 * q, ov);
+          tmem_ld32(tmem + lane_addr + 256 + 128 * x + 64 * hc + 32 * q, ov);
           tmem_wait_ld();
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
+          if (valid[x]) {
+            uint4* dst = reinterpret_cast<uint4*>(out + orow[x] * D + 64 * hc + 32 * q);
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
               uint4 v;
@@ -637,8 +761,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-        if (valid && phase == 1) c.attn_ml[orow] = m_used + __log2f(l);
-        else if (valid && lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+        if (valid[x] && hc == 0) {
+          if (phase == 2 && cascade) c.attn_ml[orow[x]] = m_used[x] + __log2f(l[x]);
+          else if (lse) lse[orow[x]] = (m_used[x] + __log2f(l[x])) * 0.69314718055994531f;
+        }
       }
       tc_fence_before();
       mbar_arrive(bar(O_FREE));
@@ -762,7 +888,8 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
     IL_CUDA(cudaFuncSetAttribute(k_attn_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
-  for (uint32_t phase = cascade ? 1 : 2; phase <= 2; ++phase) {
+  for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
+    if (phase == 1 && !cascade) break;
     k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out,
                                                           lse, scale * 1.4426950408889634f, g, TQ, phase, tq, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");

@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 
 from paper_2507_08523_b200 import _lib  # noqa: E402
 
-_lib.LIB_PATH = _lib.LIB_PATH.replace(".so", "_trace.so")
+if not os.environ.get("IL_LIB_VARIANT"):          # a variant built with -DIL_ATTN_TRACE may be named instead
+    _lib.LIB_PATH = _lib.LIB_PATH.replace(".so", "_trace.so")
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -31,12 +32,12 @@ def main():
         pl.stage_batch(gen.make_batch(ds, s, b))
         pl.step()
     torch.cuda.synchronize()
-    raw = np.zeros(8 * 4096 + 1024 * 4 // 2 + 8, np.uint64)
+    raw = np.zeros(16 * 4096 + 1024 * 4 // 2 + 8, np.uint64)
     lib = _lib.load()
     lib.il_debug_trace.argtypes = [C.c_void_p]
     _lib.check(lib.il_debug_trace(raw.ctypes.data_as(C.c_void_p)), "trace")
-    tr = raw[:8 * 4096].reshape(8, 4096).astype(np.int64)
-    items = raw[8 * 4096:8 * 4096 + 2048].view(np.uint32).reshape(1024, 4)
+    tr = raw[:16 * 4096].reshape(16, 4096).astype(np.int64)
+    items = raw[16 * 4096:16 * 4096 + 2048].view(np.uint32).reshape(1024, 4)
     t0 = tr[2][0]
     rel = np.where(tr > 0, tr - t0, -1)
     n_it = int((items[:, 1] > 0).sum())
@@ -58,6 +59,10 @@ def main():
     loads = int(items[1:n_it - 1, 1].sum())
     print("cycles per load (steady):", tot_cycles / max(loads, 1))
     da = rel[5][20:400] - rel[4][20:400]; print("softmax A duration median", np.median(da))
+    seg = [("S_FULL->ld done", 4, 8), ("ld->exchange done", 8, 9), ("exchange->exp done", 9, 10),
+           ("exp->P stored", 10, 11), ("P stored->arrive", 11, 5)]
+    for name, a, b in seg:
+        print(f"  softmax A {name:22s} median {np.median(rel[b][20:400] - rel[a][20:400]):7.0f} cycles")
 
 
 if __name__ == "__main__":
