@@ -48,6 +48,8 @@ def lib():
         _lib.or_pool_load.argtypes = [P, C.c_uint32] + [u32p] * 7 + [C.c_uint32]
         _lib.or_run_batch.argtypes = ([P, C.c_uint32, u32p, u32p, u32p, u32p, u32p, i32p, u64p,
                                        u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p])
+        _lib.or_run_batch_dp.argtypes = ([C.POINTER(P), C.c_uint32, C.c_uint32, u32p, u32p, u32p, u32p, u32p, i32p,
+                                          u64p, u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p])
         _lib.or_batch_index.restype = C.c_uint64
         _lib.or_batch_index.argtypes = [P]
         _lib.or_index_size.restype = C.c_uint32
@@ -132,6 +134,29 @@ class Oracle:
                                 _p(ev, C.c_uint64), _p(nev, C.c_uint32))
         if rc:
             raise RuntimeError(f"or_run_batch rc={rc}")
+        return BatchResult(topk, fin, info, tst, plen, ptok, bh, hit, ev[:nev[0]].copy())
+
+    @staticmethod
+    def run_batch_dp(ranks: list, batch, prompt_stride: int = 4096, max_blocks: int = 256,
+                     max_evict: int = 1 << 20) -> BatchResult:
+        """One global batch over len(ranks) data-parallel oracle contexts: rank r
+        owns the r-th contiguous slice and its own prefix index; the replicated ICL Tables receive
+        every record in global admission order."""
+        G, B, k = len(ranks), batch.B, ranks[0].k
+        topk = np.zeros((B, k), np.uint32); fin = np.zeros((B, k), np.uint32)
+        info = np.zeros((B, 4), np.int32); tst = np.zeros(B, np.uint64)
+        plen = np.zeros(B, np.uint32); ptok = np.zeros((B, prompt_stride), np.uint32)
+        bh = np.zeros((B, max_blocks), np.uint64); hit = np.zeros(B, np.uint32)
+        ev = np.zeros(max_evict, np.uint64); nev = np.array([max_evict], np.uint32)
+        qo, qt, qs = _u32(batch.q_off), _u32(batch.q_tok), _u32(batch.q_src)
+        hs = (C.c_void_p * G)(*[o.h for o in ranks])
+        rc = lib().or_run_batch_dp(hs, G, B, _p(qo, C.c_uint32), _p(qt, C.c_uint32), _p(qs, C.c_uint32),
+                                   _p(topk, C.c_uint32), _p(fin, C.c_uint32), _p(info, C.c_int32),
+                                   _p(tst, C.c_uint64), _p(plen, C.c_uint32), _p(ptok, C.c_uint32),
+                                   prompt_stride, _p(bh, C.c_uint64), max_blocks, _p(hit, C.c_uint32),
+                                   _p(ev, C.c_uint64), _p(nev, C.c_uint32))
+        if rc:
+            raise RuntimeError(f"or_run_batch_dp rc={rc}")
         return BatchResult(topk, fin, info, tst, plen, ptok, bh, hit, ev[:nev[0]].copy())
 
     @property

@@ -287,23 +287,35 @@ int or_pool_load(or_state* s, u32 n, const u32* log_off, const u32* log_tok, con
   return 0;
 }
 
-int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
-                 u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
-                 u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
-                 u64* evicted, u32* n_evicted) {
-  if (!s->loaded) return 3;
-  const u32 k = s->k;
-  const u64 b = s->batch + 1;
+// The batch procedure over G data-parallel ranks; G = 1 is the one-GPU
+// procedure.  Rank r owns the contiguous admission slice [r*B/G, (r+1)*B/G) of the global batch
+// and its own prefix index st[r]->index (steps 6, 7, 9 use only that index); the ICL Table is
+// replicated: every st[r]->table starts identical and step 10 applies ALL B records in global
+// admission order to each of them.  Stamps use the global admission index i.
+static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
+                        u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
+                        u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
+                        u64* evicted, u32* n_evicted) {
+  for (u32 r = 0; r < G; ++r) {
+    if (!st[r]->loaded) return 3;
+    if (st[r]->batch != st[0]->batch || st[r]->table != st[0]->table) return 4;   // not replicated
+  }
+  const u32 k = st[0]->k;
+  const u64 b = st[0]->batch + 1;
+  std::vector<u32> owner(B);
+  for (u32 r = 0; r < G; ++r)
+    for (u32 i = (u32)((u64)r * B / G); i < (u32)((u64)(r + 1) * B / G); ++i) owner[i] = r;
   std::vector<std::vector<u32>> q(B), cur(B), prompt(B);
   std::vector<std::vector<u64>> H(B);
   std::vector<Refined> ref(B);
   std::vector<u32> h(B);
   std::vector<int> err(B, 0);
 
-  // Steps 1-6 per request against the snapshot (Z1).
+  // Steps 1-6 per request against the snapshot (Z1) of its rank.
 #pragma omp parallel for schedule(dynamic, 4)
   for (int64_t ii = 0; ii < (int64_t)B; ++ii) {
     const u32 i = (u32)ii;
+    const or_state* s = st[owner[i]];
     q[i].assign(q_tok + q_off[i], q_tok + q_off[i + 1]);
     cur[i].assign(k, 0);
     if (select_examples(s, q[i], q_src[i], cur[i].data())) { err[i] = 1; continue; }
@@ -316,35 +328,44 @@ int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u
   }
   for (u32 i = 0; i < B; ++i) if (err[i]) return err[i];
 
-  // Step 7: touch + pin the hit blocks, then evict for the pages this batch needs (Z21).
-  std::set<u64> pinned;
-  u64 need = 0;
-  for (u32 i = 0; i < B; ++i) {
-    for (u32 j = 0; j < h[i]; ++j) pinned.insert(H[i][j]);
-    need += (prompt[i].size() + BS - 1) / BS - h[i];
+  // Step 7 per rank: touch + pin the hit blocks, then evict for the pages its slice needs (Z21).
+  std::vector<std::vector<u64>> victims(G);
+  for (u32 r = 0; r < G; ++r) {
+    or_state* s = st[r];
+    std::set<u64> pinned;
+    u64 need = 0;
+    for (u32 i = 0; i < B; ++i) {
+      if (owner[i] != r) continue;
+      for (u32 j = 0; j < h[i]; ++j) pinned.insert(H[i][j]);
+      need += (prompt[i].size() + BS - 1) / BS - h[i];
+    }
+    u64 free_pages = s->C - s->index.size();
+    if (need > free_pages) {
+      struct V { u64 stamp; u32 depth; u64 hash; };
+      std::vector<V> cand;
+      for (auto& e : s->index)
+        if (!pinned.count(e.first)) cand.push_back({e.second.stamp, e.second.depth, e.first});
+      if (cand.size() < need - free_pages) return 2;  // IL_ERR_CAPACITY, state untouched
+      std::sort(cand.begin(), cand.end(), [](const V& x, const V& y) {
+        if (x.stamp != y.stamp) return x.stamp < y.stamp;   // least recently used first
+        if (x.depth != y.depth) return x.depth > y.depth;   // deeper first (keeps ancestors)
+        return x.hash < y.hash;
+      });
+      for (u64 e = 0; e < need - free_pages; ++e) victims[r].push_back(cand[e].hash);
+    }
   }
-  u64 free_pages = s->C - s->index.size();
-  std::vector<u64> victims;
-  if (need > free_pages) {
-    struct V { u64 stamp; u32 depth; u64 hash; };
-    std::vector<V> cand;
-    for (auto& e : s->index)
-      if (!pinned.count(e.first)) cand.push_back({e.second.stamp, e.second.depth, e.first});
-    if (cand.size() < need - free_pages) return 2;    // IL_ERR_CAPACITY, state untouched
-    std::sort(cand.begin(), cand.end(), [](const V& x, const V& y) {
-      if (x.stamp != y.stamp) return x.stamp < y.stamp;   // least recently used first
-      if (x.depth != y.depth) return x.depth > y.depth;   // deeper first (keeps ancestors)
-      return x.hash < y.hash;
-    });
-    for (u64 e = 0; e < need - free_pages; ++e) victims.push_back(cand[e].hash);
-  }
-  if (victims.size() > *n_evicted) return 1;
+  size_t n_vict = 0;
+  for (u32 r = 0; r < G; ++r) n_vict += victims[r].size();
+  if (n_vict > *n_evicted) return 1;
   for (u32 i = 0; i < B; ++i)
-    for (u32 j = 0; j < h[i]; ++j) s->index[H[i][j]].stamp = stamp_of(b, i);
-  for (u64 v : victims) s->index.erase(v);
+    for (u32 j = 0; j < h[i]; ++j) st[owner[i]]->index[H[i][j]].stamp = stamp_of(b, i);
+  for (u32 r = 0; r < G; ++r)
+    for (u64 v : victims[r]) st[r]->index.erase(v);
 
-  // Step 9: insert the new full blocks in admission order; first wins (Z22).
+  // Step 9: insert the new full blocks in admission order, each into its rank's index; first
+  // wins (Z22).
   for (u32 i = 0; i < B; ++i) {
+    or_state* s = st[owner[i]];
     for (u32 j = h[i]; j < H[i].size(); ++j) {
       auto it = s->index.find(H[i][j]);
       if (it != s->index.end()) {
@@ -360,23 +381,26 @@ int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u
     }
   }
 
-  // Step 10: ICL Table commit (Z2, Z3, Z14).  Rule 1 refreshes the target
-  // (its key IS final_ds); rules 2/3 and reverted requests upsert final_ds; a rule-3
-  // target keeps its position.  Then keep the T most recent entries.
-  if (s->flags & OR_F_PAIR) {
-    for (u32 i = 0; i < B; ++i) {
-      auto it = s->table.find(ref[i].final_ds);
-      if (it == s->table.end()) s->table[ref[i].final_ds] = stamp_of(b, i);
-      else it->second = std::max(it->second, stamp_of(b, i));
+  // Step 10: ICL Table commit (Z2, Z3, Z14), all B records on every rank.  Rule 1
+  // refreshes the target (its key IS final_ds); rules 2/3 and reverted requests upsert
+  // final_ds; a rule-3 target keeps its position.  Then keep the T most recent entries.
+  for (u32 r = 0; r < G; ++r) {
+    or_state* s = st[r];
+    if (s->flags & OR_F_PAIR) {
+      for (u32 i = 0; i < B; ++i) {
+        auto it = s->table.find(ref[i].final_ds);
+        if (it == s->table.end()) s->table[ref[i].final_ds] = stamp_of(b, i);
+        else it->second = std::max(it->second, stamp_of(b, i));
+      }
+      while (s->table.size() > s->T) {
+        auto oldest = s->table.begin();
+        for (auto it = s->table.begin(); it != s->table.end(); ++it)
+          if (it->second < oldest->second) oldest = it;
+        s->table.erase(oldest);
+      }
     }
-    while (s->table.size() > s->T) {
-      auto oldest = s->table.begin();
-      for (auto it = s->table.begin(); it != s->table.end(); ++it)
-        if (it->second < oldest->second) oldest = it;
-      s->table.erase(oldest);
-    }
+    s->batch = b;
   }
-  s->batch = b;
 
   // outputs
   for (u32 i = 0; i < B; ++i) {
@@ -389,9 +413,28 @@ int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u
     for (u32 j = 0; j < H[i].size(); ++j) block_hash[(size_t)i * max_blocks + j] = H[i][j];
     hit[i] = h[i];
   }
-  for (size_t e = 0; e < victims.size(); ++e) evicted[e] = victims[e];
-  *n_evicted = (u32)victims.size();
+  size_t e = 0;
+  for (u32 r = 0; r < G; ++r)
+    for (u64 v : victims[r]) evicted[e++] = v;
+  *n_evicted = (u32)n_vict;
   return 0;
+}
+
+int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
+                 u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
+                 u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
+                 u64* evicted, u32* n_evicted) {
+  return run_batch_dp(&s, 1, B, q_off, q_tok, q_src, topk, final_ds, info, target_stamp, prompt_len, prompt_tok,
+                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted);
+}
+
+int or_run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
+                    u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
+                    u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
+                    u64* evicted, u32* n_evicted) {
+  if (G == 0) return 1;
+  return run_batch_dp(st, G, B, q_off, q_tok, q_src, topk, final_ds, info, target_stamp, prompt_len, prompt_tok,
+                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted);
 }
 
 u64 or_batch_index(const or_state* s) { return s->batch; }
