@@ -138,11 +138,19 @@ def run_ours(args, rank, world, local_rank):
                   max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
                   max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
-                  head_dim=cfg.d, flags=flags)
+                  head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world)
     stream = torch.cuda.Stream(dev)
     pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
+    # N > 1: rank r runs the r-th slice of every global batch; the pool is
+    # broadcast from rank 0 and the ICL records are all-gathered (NCCL) at every commit
+    dp = None
+    if world > 1:
+        from paper_2507_08523_b200.distributed import DataParallel
+        dp = DataParallel(pl)
     with torch.cuda.stream(stream):
-        pl.load_pool(pool, instr)
+        (dp or pl).load_pool(pool, instr)
+    commit = dp.commit if dp else pl.commit
+    step = dp.step if dp else pl.step
     K, W = args.steps, args.warmup
     plan = plan_batches(cfg, W + 2 * K, rank, world)
     n_ramp = len(plan) - (W + 2 * K)
@@ -181,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         for x in warm_in:
             set_inputs(x)
-            pl.step()
+            step()
     stream.synchronize()
     pl.ctx.status_sync(stream)
 
@@ -204,7 +212,7 @@ def run_ours(args, rank, world, local_rank):
                 e[1].record(stream); pl.match()
                 e[2].record(stream); pl.synth()
                 e[3].record(stream); pl.attn()
-                e[4].record(stream); pl.commit()
+                e[4].record(stream); commit()
                 e[5].record(stream)
                 evs.append(e)
                 B = dev_in[j][3]
@@ -218,7 +226,7 @@ def run_ours(args, rank, world, local_rank):
                 stage_buf[1][:qt.numel()].copy_(qt, non_blocking=True)
                 stage_buf[2][:B].copy_(qs, non_blocking=True)
                 set_inputs(stage_buf + (B,))
-                pl.step()
+                step()
                 out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
                 out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
                 out_info[:B].copy_(pl.info[:B], non_blocking=True)
@@ -269,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
                    "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
                    "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
                    "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
-                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards)",
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards" + ("; ICL records all-gathered per batch, NCCL)" if world > 1 else ")"),
                    "stream": f"{ds.n} distinct logs, no query repeats within the run",
                    "int_dtype": "u32/u64 bit-exact", "attn": "bf16 in, fp32 accumulate"},
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),

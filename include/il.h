@@ -82,6 +82,8 @@ typedef struct {
   uint32_t metric;             /* il_sim */
   uint32_t flags;              /* IL_F_* */
   uint64_t hash_seed;          /* chain-hash root (Z17) */
+  uint32_t max_global_batch;   /* records per il_commit_records (multi-GPU: world x B); 0 = max_batch */
+  uint32_t reserved0;          /* must be 0 */
 } il_config;
 
 /* Per-request refinement outcome (SPEC S:190-193 RefinementResult). */
@@ -181,6 +183,22 @@ il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const in
  * upsert the final DS; the target of rule 3 keeps its position), then keeps the T most recent
  * entries (Z2, Z3, Z14). */
 il_status il_commit(il_ctx* ctx, il_stream s);
+
+/* ---- multi-GPU: requests shard by admission order (rank r takes the r-th
+ * contiguous slice of the global batch), every rank keeps its own KV pages and prefix index,
+ * and the ICL Table is REPLICATED: each rank refines its slice against the same table
+ * snapshot, the per-request records of all ranks (final_ds[i][0..k), il_refine_info[i]) are
+ * all-gathered in global admission order, and every rank applies all of them, so the tables
+ * stay identical and equal to a one-GPU run over the global batch (P:356-363 applied to the
+ * whole batch).
+ *   il_commit_index    the prefix-index half of il_commit (this rank's blocks only)
+ *   il_commit_records  the ICL Table half over B_global gathered records (device arrays,
+ *                      global admission order; info[].target_slot refers to the replicated
+ *                      table).  Ends the batch.  B_global <= cfg.max_global_batch.
+ * il_commit == il_commit_index + il_commit_records over this rank's own records. */
+il_status il_commit_index(il_ctx* ctx, il_stream s);
+il_status il_commit_records(il_ctx* ctx, uint32_t B_global, const uint32_t* final_ds_all,
+                            const il_refine_info* info_all, il_stream s);
 
 /* ---- bench / test helper (not part of the method): deterministic bf16 Q, K, V for the
  * suffix rows from (seed, token, absolute position, head, dim) — the counter-based

@@ -49,7 +49,7 @@ def lib():
         _lib.or_run_batch.argtypes = ([P, C.c_uint32, u32p, u32p, u32p, u32p, u32p, i32p, u64p,
                                        u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p])
         _lib.or_run_batch_dp.argtypes = ([C.POINTER(P), C.c_uint32, C.c_uint32, u32p, u32p, u32p, u32p, u32p, i32p,
-                                          u64p, u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p])
+                                          u64p, u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p, u32p])
         _lib.or_batch_index.restype = C.c_uint64
         _lib.or_batch_index.argtypes = [P]
         _lib.or_index_size.restype = C.c_uint32
@@ -150,14 +150,18 @@ class Oracle:
         ev = np.zeros(max_evict, np.uint64); nev = np.array([max_evict], np.uint32)
         qo, qt, qs = _u32(batch.q_off), _u32(batch.q_tok), _u32(batch.q_src)
         hs = (C.c_void_p * G)(*[o.h for o in ranks])
+        nrank = np.zeros(G, np.uint32)
         rc = lib().or_run_batch_dp(hs, G, B, _p(qo, C.c_uint32), _p(qt, C.c_uint32), _p(qs, C.c_uint32),
                                    _p(topk, C.c_uint32), _p(fin, C.c_uint32), _p(info, C.c_int32),
                                    _p(tst, C.c_uint64), _p(plen, C.c_uint32), _p(ptok, C.c_uint32),
                                    prompt_stride, _p(bh, C.c_uint64), max_blocks, _p(hit, C.c_uint32),
-                                   _p(ev, C.c_uint64), _p(nev, C.c_uint32))
+                                   _p(ev, C.c_uint64), _p(nev, C.c_uint32), _p(nrank, C.c_uint32))
         if rc:
             raise RuntimeError(f"or_run_batch_dp rc={rc}")
-        return BatchResult(topk, fin, info, tst, plen, ptok, bh, hit, ev[:nev[0]].copy())
+        res = BatchResult(topk, fin, info, tst, plen, ptok, bh, hit, ev[:nev[0]].copy())
+        off = np.concatenate([[0], np.cumsum(nrank.astype(np.int64))])
+        res.evicted_rank = [res.evicted[off[r]:off[r + 1]] for r in range(G)]
+        return res
 
     @property
     def batch_index(self) -> int:

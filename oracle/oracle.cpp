@@ -295,7 +295,7 @@ int or_pool_load(or_state* s, u32 n, const u32* log_off, const u32* log_tok, con
 static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
                         u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
                         u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
-                        u64* evicted, u32* n_evicted) {
+                        u64* evicted, u32* n_evicted, u32* n_evicted_rank) {
   for (u32 r = 0; r < G; ++r) {
     if (!st[r]->loaded) return 3;
     if (st[r]->batch != st[0]->batch || st[r]->table != st[0]->table) return 4;   // not replicated
@@ -357,8 +357,12 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
   size_t n_vict = 0;
   for (u32 r = 0; r < G; ++r) n_vict += victims[r].size();
   if (n_vict > *n_evicted) return 1;
+  // index stamps use the admission index within the rank's slice (its LRU order); table stamps
+  // (step 10) use the global admission index
+  std::vector<u32> lo(G + 1);
+  for (u32 r = 0; r <= G; ++r) lo[r] = (u32)((u64)r * B / G);
   for (u32 i = 0; i < B; ++i)
-    for (u32 j = 0; j < h[i]; ++j) st[owner[i]]->index[H[i][j]].stamp = stamp_of(b, i);
+    for (u32 j = 0; j < h[i]; ++j) st[owner[i]]->index[H[i][j]].stamp = stamp_of(b, i - lo[owner[i]]);
   for (u32 r = 0; r < G; ++r)
     for (u64 v : victims[r]) st[r]->index.erase(v);
 
@@ -366,16 +370,17 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
   // wins (Z22).
   for (u32 i = 0; i < B; ++i) {
     or_state* s = st[owner[i]];
+    const u32 il = i - lo[owner[i]];
     for (u32 j = h[i]; j < H[i].size(); ++j) {
       auto it = s->index.find(H[i][j]);
       if (it != s->index.end()) {
-        it->second.stamp = std::max(it->second.stamp, stamp_of(b, i));
+        it->second.stamp = std::max(it->second.stamp, stamp_of(b, il));
       } else {
         Block blk;
         blk.parent = j == 0 ? root_hash(s->seed) : H[i][j - 1];
         std::memcpy(blk.tok, &prompt[i][j * BS], sizeof(blk.tok));
         blk.depth = j;
-        blk.stamp = stamp_of(b, i);
+        blk.stamp = stamp_of(b, il);
         s->index[H[i][j]] = blk;
       }
     }
@@ -414,8 +419,10 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     hit[i] = h[i];
   }
   size_t e = 0;
-  for (u32 r = 0; r < G; ++r)
+  for (u32 r = 0; r < G; ++r) {
     for (u64 v : victims[r]) evicted[e++] = v;
+    if (n_evicted_rank) n_evicted_rank[r] = (u32)victims[r].size();
+  }
   *n_evicted = (u32)n_vict;
   return 0;
 }
@@ -425,16 +432,16 @@ int or_run_batch(or_state* s, u32 B, const u32* q_off, const u32* q_tok, const u
                  u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
                  u64* evicted, u32* n_evicted) {
   return run_batch_dp(&s, 1, B, q_off, q_tok, q_src, topk, final_ds, info, target_stamp, prompt_len, prompt_tok,
-                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted);
+                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted, nullptr);
 }
 
 int or_run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32* q_tok, const u32* q_src,
                     u32* topk, u32* final_ds, int32_t* info, u64* target_stamp, u32* prompt_len,
                     u32* prompt_tok, u32 prompt_stride, u64* block_hash, u32 max_blocks, u32* hit,
-                    u64* evicted, u32* n_evicted) {
+                    u64* evicted, u32* n_evicted, u32* n_evicted_rank) {
   if (G == 0) return 1;
   return run_batch_dp(st, G, B, q_off, q_tok, q_src, topk, final_ds, info, target_stamp, prompt_len, prompt_tok,
-                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted);
+                      prompt_stride, block_hash, max_blocks, hit, evicted, n_evicted, n_evicted_rank);
 }
 
 u64 or_batch_index(const or_state* s) { return s->batch; }

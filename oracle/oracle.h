@@ -47,14 +47,16 @@ int or_run_batch(or_state*, uint32_t B, const uint32_t* q_off, const uint32_t* q
 
 /* The same batch over G data-parallel ranks: rank r owns the admission slice
  * [r*B/G, (r+1)*B/G) and its own prefix index st[r]; the ICL Tables of all st[] must be
- * identical on entry and receive all B records in global admission order.  Outputs as
- * or_run_batch for the global batch (hits from the owning rank's index; evictions rank-major).
- * Returns 4 if the tables differ on entry.  G = 1 is or_run_batch. */
+ * identical on entry and receive all B records in global admission order (table stamps use the
+ * global admission index, a rank's index stamps the index within its slice).  Outputs as
+ * or_run_batch for the global batch (hits from the owning rank's index; evictions rank-major,
+ * n_evicted_rank[G] per rank, may be NULL).  Returns 4 if the tables differ on entry.  G = 1 is
+ * or_run_batch. */
 int or_run_batch_dp(or_state** st, uint32_t G, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
                     const uint32_t* q_src, uint32_t* topk, uint32_t* final_ds, int32_t* info,
                     uint64_t* target_stamp, uint32_t* prompt_len, uint32_t* prompt_tok,
                     uint32_t prompt_stride, uint64_t* block_hash, uint32_t max_blocks,
-                    uint32_t* hit, uint64_t* evicted, uint32_t* n_evicted);
+                    uint32_t* hit, uint64_t* evicted, uint32_t* n_evicted, uint32_t* n_evicted_rank);
 
 uint64_t or_batch_index(const or_state*);           /* b of the last committed batch */
 uint32_t or_index_size(const or_state*);

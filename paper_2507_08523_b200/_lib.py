@@ -23,7 +23,8 @@ IL_F_PAIR, IL_F_GUARD, IL_F_EXCLUDE_SELF, IL_F_VERIFY = 1, 2, 4, 8
 # every symbol include/il.h declares (checked by tests/test_abi.py)
 EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "il_stats_sync",
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
-           "il_commit", "il_synth_qkv", "il_index_dump", "il_table_dump", "il_evicted_dump"]
+           "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
+           "il_table_dump", "il_evicted_dump"]
 
 
 class ILError(RuntimeError):
@@ -38,7 +39,7 @@ class il_config(C.Structure):
                 ("max_pool_tokens", C.c_uint32), ("max_log_tokens", C.c_uint32),
                 ("max_suffix_tokens", C.c_uint32), ("n_q_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
                 ("head_dim", C.c_uint32), ("metric", C.c_uint32), ("flags", C.c_uint32),
-                ("hash_seed", C.c_uint64)]
+                ("hash_seed", C.c_uint64), ("max_global_batch", C.c_uint32), ("reserved0", C.c_uint32)]
 
 
 class il_refine_info(C.Structure):
@@ -79,6 +80,8 @@ def load():
         "il_prefix_match": [P, U32, P, P, P, P, P, P, P, P],
         "il_prefill_attn": [P, U32, P, P, P, P, P, P, P, P, P, P, F32, P],
         "il_commit": [P, P],
+        "il_commit_index": [P, P],
+        "il_commit_records": [P, U32, P, P, P],
         "il_synth_qkv": [P, U32, P, P, P, U64, F32, P, P, P, P],
         "il_index_dump": [P, P, P, P, P, P, P],
         "il_table_dump": [P, P, P, P],

@@ -31,6 +31,7 @@ class Config:
     metric: int = L.IL_SIM_COSINE
     flags: int = L.IL_F_PAIR | L.IL_F_VERIFY
     hash_seed: int = 0
+    max_global_batch: int = 0           # multi-GPU: world * max_batch records per table commit
 
     @property
     def max_blocks(self) -> int:
@@ -41,7 +42,7 @@ class Config:
         return L.il_config(self.k, self.table_capacity, self.kv_pages, self.max_batch,
                            self.max_prompt_tokens, self.max_pool, self.max_pool_tokens,
                            self.max_log_tokens, m, self.n_q_heads, self.n_kv_heads, self.head_dim,
-                           self.metric, self.flags, self.hash_seed)
+                           self.metric, self.flags, self.hash_seed, self.max_global_batch, 0)
 
 
 def _p(t) -> C.c_void_p:
@@ -107,6 +108,13 @@ class Context:
 
     def commit(self, stream=None):
         L.check(self.lib.il_commit(self.h, _stream(stream)), "il_commit")
+
+    def commit_index(self, stream=None):
+        L.check(self.lib.il_commit_index(self.h, _stream(stream)), "il_commit_index")
+
+    def commit_records(self, B_global, final_ds_all, info_all, stream=None):
+        L.check(self.lib.il_commit_records(self.h, B_global, _p(final_ds_all), _p(info_all), _stream(stream)),
+                "il_commit_records")
 
     def synth_qkv(self, B, prompt_tok, cu_q, prefix_len, seed, q_scale, q, k_new, v_new, stream=None):
         L.check(self.lib.il_synth_qkv(self.h, B, _p(prompt_tok), _p(cu_q), _p(prefix_len), int(seed),

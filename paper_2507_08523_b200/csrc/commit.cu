@@ -1,3 +1,4 @@
+#include <algorithm>
 // commit.cu — il_commit (K8): prefix-index insert in admission order (first request owns the
 // page, duplicates and partial pages are freed; Z22, Z23) + tombstone compaction, and the
 // ICL-Table commit (keyed upsert in admission order, keep the T most recent; Z2, Z3, Z14).
@@ -359,44 +360,86 @@ __global__ void __launch_bounds__(1024) k_tab_commit(Ctx c, uint32_t B, uint64_t
 
 using namespace il;
 
-extern "C" il_status il_commit(il_ctx* c, il_stream s) {
-  if (!c->matched) { set_error("il_commit before il_prefix_match"); return IL_ERR_STATE; }
-  const bool pair = (c->cfg.flags & IL_F_PAIR) != 0;
-  if (pair && !c->refined) { set_error("il_commit before il_refine_batch"); return IL_ERR_STATE; }
-  cudaStream_t st = (cudaStream_t)s;
+// index half of the commit (this context's blocks), stamps of batch b_cur
+static il_status commit_index(Ctx* c, cudaStream_t st, uint64_t b_cur) {
   const uint32_t B = c->last_B;
-  const uint64_t b_cur = c->batch + 1;
   if (B) {
     const uint32_t g = cdiv(B * 32, 256);
     k_commit_probe<<<g, 256, 0, st>>>(*c, B, b_cur);
     k_commit_insert<<<g, 256, 0, st>>>(*c, B, b_cur);
     k_commit_own<<<g, 256, 0, st>>>(*c, B);
   }
-  {
-    static int rb_blocks = -1;
-    if (rb_blocks < 0) {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0);
-      rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
-    }
-    Ctx cc = *c;
-    void* args[] = {&cc};
-    IL_CUDA(cudaLaunchCooperativeKernel((void*)k_rebuild, dim3(rb_blocks), dim3(512), args, 0, st));
+  static int rb_blocks = -1;
+  if (rb_blocks < 0) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0);
+    rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
   }
-  if (pair && B) {
-    k_tab_key<<<cdiv(B, 256), 256, 0, st>>>(*c, B);
-    k_tab_find<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B);
-    const size_t smem = (size_t)c->cfg.table_capacity * 8;
-    static bool attr = false;
-    if (!attr) {
-      IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
-      attr = true;
-    }
-    k_tab_commit<<<1, 1024, smem, st>>>(*c, B, b_cur);
+  Ctx cc = *c;
+  void* args[] = {&cc};
+  IL_CUDA(cudaLaunchCooperativeKernel((void*)k_rebuild, dim3(rb_blocks), dim3(512), args, 0, st));
+  IL_LAUNCH_CHECK("il_commit (index)");
+  c->launches += (B ? 3 : 0) + 1;
+  return IL_OK;
+}
+
+// table half: B records (final DS + refine info) in admission order, stamps (b_cur, i)
+static il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, const il_refine_info* info,
+                              cudaStream_t st, uint64_t b_cur) {
+  if (!B) return IL_OK;
+  c->final_ds = final_ds;
+  c->info = info;
+  k_tab_key<<<cdiv(B, 256), 256, 0, st>>>(*c, B);
+  k_tab_find<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B);
+  const size_t smem = (size_t)c->cfg.table_capacity * 8;
+  static bool attr = false;
+  if (!attr) {
+    IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+    attr = true;
   }
-  IL_LAUNCH_CHECK("il_commit");
-  c->launches += (B ? 3 : 0) + 1 + ((pair && B) ? 3 : 0);
-  c->batch = b_cur;
-  c->refined = c->matched = false;
+  k_tab_commit<<<1, 1024, smem, st>>>(*c, B, b_cur);
+  IL_LAUNCH_CHECK("il_commit (table)");
+  c->launches += 3;
+  return IL_OK;
+}
+
+static void end_batch(Ctx* c) {
+  c->batch += 1;
+  c->refined = c->matched = c->index_done = false;
+}
+
+extern "C" il_status il_commit(il_ctx* c, il_stream s) {
+  if (!c->matched || c->index_done) { set_error("il_commit before il_prefix_match"); return IL_ERR_STATE; }
+  const bool pair = (c->cfg.flags & IL_F_PAIR) != 0;
+  if (pair && !c->refined) { set_error("il_commit before il_refine_batch"); return IL_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)s;
+  const uint64_t b_cur = c->batch + 1;
+  il_status r = commit_index(c, st, b_cur);
+  if (r != IL_OK) return r;
+  if (pair) {
+    r = commit_table(c, c->last_B, c->final_ds, c->info, st, b_cur);
+    if (r != IL_OK) return r;
+  }
+  end_batch(c);
+  return IL_OK;
+}
+
+extern "C" il_status il_commit_index(il_ctx* c, il_stream s) {
+  if (!c->matched || c->index_done) { set_error("il_commit_index before il_prefix_match"); return IL_ERR_STATE; }
+  il_status r = commit_index(c, (cudaStream_t)s, c->batch + 1);
+  if (r != IL_OK) return r;
+  c->index_done = true;
+  return IL_OK;
+}
+
+extern "C" il_status il_commit_records(il_ctx* c, uint32_t B_global, const uint32_t* final_ds_all,
+                                       const il_refine_info* info_all, il_stream s) {
+  if (!c->index_done) { set_error("il_commit_records before il_commit_index"); return IL_ERR_STATE; }
+  if (!(c->cfg.flags & IL_F_PAIR)) { set_error("il_commit_records needs IL_F_PAIR"); return IL_ERR_STATE; }
+  if (B_global > c->max_records) { set_error("B_global > max_global_batch"); return IL_ERR_ARG; }
+  if (B_global && (!final_ds_all || !info_all)) { set_error("null records"); return IL_ERR_ARG; }
+  il_status r = commit_table(c, B_global, final_ds_all, info_all, (cudaStream_t)s, c->batch + 1);
+  if (r != IL_OK) return r;
+  end_batch(c);
   return IL_OK;
 }

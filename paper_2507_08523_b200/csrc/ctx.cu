@@ -61,11 +61,13 @@ static size_t carve(Ctx* c, void* ws) {
   c->need_off = w.take<uint32_t>(B + 1);
   c->occ = w.take<uint32_t>(B * MB);
   c->hist = w.take<uint32_t>(4096);
-  c->tab_find = w.take<int32_t>(B); c->tab_last = w.take<uint32_t>(B); c->tab_hash = w.take<uint64_t>(B);
-  c->tab_slot = w.take<uint32_t>(B);
+  const size_t R = std::max<size_t>(B, g.max_global_batch);   // table-commit records
+  c->max_records = (uint32_t)R;
+  c->tab_find = w.take<int32_t>(R); c->tab_last = w.take<uint32_t>(R); c->tab_hash = w.take<uint64_t>(R);
+  c->tab_slot = w.take<uint32_t>(R);
   {
     uint32_t n = 64;
-    while (n < 2 * B) n <<= 1;
+    while (n < 2 * R) n <<= 1;
     c->dd_mask = n - 1;
     c->dd_key = w.take<uint64_t>(n); c->dd_max = w.take<uint32_t>(n);
   }
@@ -84,6 +86,8 @@ static il_status validate(const il_config* g) {
   if (g->table_capacity < 1 || g->table_capacity > 8192) { set_error("table_capacity in 1..8192"); return IL_ERR_ARG; }
   if (g->kv_pages < 1) { set_error("kv_pages >= 1"); return IL_ERR_ARG; }
   if (g->max_batch < 1 || g->max_batch > 8192) { set_error("max_batch in 1..8192"); return IL_ERR_ARG; }
+  if (g->max_global_batch > 8192) { set_error("max_global_batch <= 8192"); return IL_ERR_ARG; }
+  if (g->reserved0 != 0) { set_error("il_config.reserved0 must be 0"); return IL_ERR_ARG; }
   if (g->max_prompt_tokens < 16 || (g->max_prompt_tokens % 16)) { set_error("max_prompt_tokens: multiple of 16"); return IL_ERR_ARG; }
   if (g->max_pool < g->k) { set_error("max_pool < k"); return IL_ERR_ARG; }
   if (g->max_log_tokens < 1 || g->max_log_tokens > 256) { set_error("max_log_tokens in 1..256"); return IL_ERR_ARG; }
@@ -340,7 +344,7 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   c->n_instr = n_instr;
   c->n_instr_blocks = n_instr / BS;
   c->pool_loaded = true;
-  c->refined = c->matched = false;
+  c->refined = c->matched = c->index_done = false;
   c->batch = 0;
   return IL_OK;
 }

@@ -53,7 +53,8 @@ struct Ctx {
   il_config cfg;
   uint32_t max_blocks = 0, n_slots = 0, slot_mask = 0;
   uint32_t n_demos = 0, n_instr = 0, n_instr_blocks = 0;
-  bool pool_loaded = false, refined = false, matched = false;
+  bool pool_loaded = false, refined = false, matched = false, index_done = false;
+  uint32_t max_records = 0;    // max(max_batch, max_global_batch): table-commit scratch size
   uint32_t last_B = 0;
   uint64_t batch = 0;        // b of the last committed batch
   // workspace carve

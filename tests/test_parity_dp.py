@@ -1,0 +1,86 @@
+"""Multi-GPU data parallelism vs the oracle's run_batch_dp, bit-exact.
+
+Only one GPU exists on the test box, so the G ranks are G independent library contexts on the
+same device; the per-batch record all-gather is what DataParallel.commit feeds to
+il_commit_records (rank-major concatenation = global admission order; the collective itself is
+covered over gloo in test_distributed_gloo.py).  Checked per rank after every batch: topk,
+final DS, rule/PMC/guard, prompts, block hashes, hits, evictions, the rank's prefix index, and
+the replicated ICL Table."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests.parity_util import StreamSpec, batch_plan, compare_batch, compare_state, make_stream
+from workload import gen
+
+pytestmark = pytest.mark.gpu
+
+
+def _rank_pipeline(sp, pool, instr, G):
+    from paper_2507_08523_b200 import Config, Pipeline
+    cfg = Config(k=sp.k, table_capacity=sp.T, kv_pages=sp.C, max_batch=sp.B // G,
+                 max_prompt_tokens=sp.max_prompt_tokens, max_pool=sp.M,
+                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                 n_q_heads=sp.Hq, n_kv_heads=sp.Hkv, head_dim=sp.d, metric=sp.metric, flags=sp.flags,
+                 hash_seed=sp.hash_seed, max_global_batch=sp.B)
+    pl = Pipeline(cfg, "cuda")
+    pl.load_pool(pool, instr)
+    return pl
+
+
+class _Slice:
+    """Rows [lo, hi) of a global oracle result, shaped like a one-rank BatchResult."""
+    def __init__(self, r, lo, hi, evicted):
+        for f in ("topk", "final_ds", "info", "target_stamp", "prompt_len", "prompt_tok", "block_hash", "hit"):
+            setattr(self, f, getattr(r, f)[lo:hi])
+        self.evicted = evicted
+
+
+def run_dp(sp: StreamSpec, G: int, n_batches: int, attention: bool = False):
+    ds, pool, instr = make_stream(sp)
+    ranks_o = []
+    for _ in range(G):
+        o = O.Oracle(sp.k, sp.T, sp.C, metric=sp.metric, flags=sp.flags, hash_seed=sp.hash_seed)
+        o.pool_load(pool, instr)
+        ranks_o.append(o)
+    pls = [_rank_pipeline(sp, pool, instr, G) for _ in range(G)]
+    k = sp.k
+    fds_all = torch.zeros(sp.B, k, dtype=torch.int32, device="cuda")
+    info_all = torch.zeros(sp.B, 16, dtype=torch.uint8, device="cuda")
+    sp.n_batches = n_batches
+    for b, (start, B) in enumerate(batch_plan(sp, ds.n)):
+        assert B % G == 0
+        batch = gen.make_batch(ds, start, B)
+        r = O.Oracle.run_batch_dp(ranks_o, batch, prompt_stride=sp.max_prompt_tokens,
+                                  max_blocks=(sp.max_prompt_tokens + 15) // 16)
+        n = B // G
+        for g, pl in enumerate(pls):
+            pl.stage_batch(gen.make_batch(ds, start + g * n, n))
+            pl.refine(); pl.match()
+            if attention:
+                pl.synth(); pl.attn()
+            pl.ctx.commit_index()
+        # the all-gather: rank-major rows = global admission order
+        torch.cat([pl.final_ds[:n] for pl in pls], out=fds_all[:B])
+        torch.cat([pl.info[:n] for pl in pls], out=info_all[:B])
+        for pl in pls:
+            pl.ctx.commit_records(B, fds_all, info_all)
+        for g, pl in enumerate(pls):
+            pl.ctx.status_sync()
+            compare_batch(_Slice(r, g * n, (g + 1) * n, r.evicted_rank[g]), pl, n, sp, where=f"batch {b} rank {g}")
+            compare_state(ranks_o[g], pl, where=f"batch {b} rank {g}")
+    return pls
+
+
+def test_dp2_no_guard():
+    run_dp(StreamSpec(B=96, C=1500, n_logs=2000), G=2, n_batches=10)
+
+
+def test_dp2_guard():
+    run_dp(StreamSpec(B=96, C=1500, n_logs=2000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD), G=2, n_batches=10)
+
+
+def test_dp4_eviction_pressure_with_attention():
+    sp = StreamSpec(B=64, C=700, n_logs=3000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4, 16))
+    run_dp(sp, G=4, n_batches=14, attention=True)
