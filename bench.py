@@ -172,8 +172,6 @@ def run_ours(args, rank, world, local_rank):
     host_in = [to_pinned(bt) if j % 2 == 1 else None for j, bt in enumerate(timed)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    stage_buf = (torch.zeros(cfg.B + 1, dtype=torch.int32, device=dev),
-                 torch.zeros(cfg.B * 256, dtype=torch.int32, device=dev), torch.zeros(cfg.B, dtype=torch.int32, device=dev))
     out_fin = torch.empty(cfg.B, cfg.k, dtype=torch.int32).pin_memory()
     out_hit = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
     out_info = torch.empty(cfg.B, 16, dtype=torch.uint8).pin_memory()
@@ -183,7 +181,7 @@ def run_ours(args, rank, world, local_rank):
     rec_bt = torch.zeros(K, cfg.B, ccfg.max_blocks, dtype=torch.int32, device=dev)
 
     def set_inputs(x):
-        pl.q_off, pl.q_tok, pl.q_src, pl.B = x
+        pl.load_inputs(*x)                             # device-to-device into the resident buffers
 
     # ---- warm-up (cold-start ramp + W full steps), not timed
     with torch.cuda.stream(stream):
@@ -194,6 +192,28 @@ def run_ours(args, rank, world, local_rank):
     pl.ctx.status_sync(stream)
 
     stage_names = ["refine", "match", "synth", "attn", "commit"]
+    # CUDA graphs: each stage captured once for B (one replay per stage, no per-kernel launch
+    # gaps); with N > 1 the commit (NCCL all-gather inside) stays eager
+    graphs, per_step_launches = None, None
+    if not args.no_graph:
+        l0 = pl.launches()
+        with torch.cuda.stream(stream):
+            graphs = pl.capture(cfg.B, stages=stage_names if dp is None else stage_names[:-1])
+        per_step_launches = pl.launches() - l0
+        stream.synchronize()
+
+    def run_stage(name):
+        if graphs is not None and name in graphs:
+            graphs[name].replay()
+        elif name == "commit":
+            commit()
+        else:
+            getattr(pl, name)()
+
+    def run_step():
+        for n in stage_names:
+            run_stage(n)
+
     evs, e2e_evs = [], []
     h2d = d2h = 0
     if world > 1:
@@ -208,11 +228,9 @@ def run_ours(args, rank, world, local_rank):
             if j % 2 == 0:
                 set_inputs(dev_in[j])
                 e = [ev() for _ in range(6)]
-                e[0].record(stream); pl.refine()
-                e[1].record(stream); pl.match()
-                e[2].record(stream); pl.synth()
-                e[3].record(stream); pl.attn()
-                e[4].record(stream); commit()
+                for i, n in enumerate(stage_names):
+                    e[i].record(stream)
+                    run_stage(n)
                 e[5].record(stream)
                 evs.append(e)
                 B = dev_in[j][3]
@@ -222,11 +240,11 @@ def run_ours(args, rank, world, local_rank):
                 qo, qt, qs, B = host_in[j]
                 e0, e1 = ev(), ev()
                 e0.record(stream)
-                stage_buf[0][:B + 1].copy_(qo, non_blocking=True)
-                stage_buf[1][:qt.numel()].copy_(qt, non_blocking=True)
-                stage_buf[2][:B].copy_(qs, non_blocking=True)
-                set_inputs(stage_buf + (B,))
-                step()
+                pl.q_off[:B + 1].copy_(qo, non_blocking=True)        # pinned host -> resident buffers
+                pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
+                pl.q_src[:B].copy_(qs, non_blocking=True)
+                pl.B = B
+                run_step()
                 out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
                 out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
                 out_info[:B].copy_(pl.info[:B], non_blocking=True)
@@ -238,6 +256,8 @@ def run_ours(args, rank, world, local_rank):
     wall = time.perf_counter() - t_wall
     clk = clocks.stop()
     launches = pl.launches() - launches0
+    if graphs is not None:                             # replays do not pass through the host counter
+        launches += per_step_launches * 2 * K
     pl.ctx.status_sync(stream)
     if world > 1:
         dist.barrier()
@@ -291,7 +311,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": B_all / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
         "gpu_launches": int(launches),
-        "timed_steps": {"device": K, "e2e": K, "order": "alternating"},
+        "timed_steps": {"device": K, "e2e": K, "order": "alternating",
+                        "launch": "eager" if graphs is None else "per-stage CUDA graphs"},
         "clocks": clk,
         "wall_s_timed": wall,
     }
@@ -412,6 +433,7 @@ def main():
     ap.add_argument("--no-guard", action="store_true")
     ap.add_argument("--naive", action="store_true", help="PAIR off (naive prefix caching)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
     ap.add_argument("--cpu-attn-sample", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -85,9 +85,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 #ifndef IL_WAIT_HINT_NS
 #define IL_WAIT_HINT_NS 1000000
 #endif
+// A wait that has not completed after ~2^34 cycles (~9 s) traps (a launch error the host
+// reports) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done;
+  long long t0 = 0;
   do {
+    if (t0 == 0) t0 = clock64();
+    else if (clock64() - t0 > (1ll << 34)) __trap();
 #if IL_WAIT_HINT_NS > 0
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"

@@ -20,7 +20,8 @@ __device__ __forceinline__ void push_free(const Ctx& c, uint32_t page) {
 
 // Phase A: blocks j in [h_i, F_i) that are resident now (only the Z20-capped block can be)
 // get their stamp refreshed and the request's page freed; the rest become insert candidates.
-__global__ void __launch_bounds__(256) k_commit_probe(Ctx c, uint32_t B, uint64_t b_cur) {
+__global__ void __launch_bounds__(256) k_commit_probe(Ctx c, uint32_t B, uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= B) return;
   const uint32_t L = c.prompt_len[i], h = c.hit[i], F = L / BS;
@@ -40,7 +41,8 @@ __global__ void __launch_bounds__(256) k_commit_probe(Ctx c, uint32_t B, uint64_
 // Phase B: lock-free insert-or-find of every candidate key (CAS into EMPTY slots, linear
 // probing past tombstones), then claim = min admission index, cstamp = max stamp over the
 // requests presenting the key (order-independent, hence deterministic).
-__global__ void __launch_bounds__(256) k_commit_insert(Ctx c, uint32_t B, uint64_t b_cur) {
+__global__ void __launch_bounds__(256) k_commit_insert(Ctx c, uint32_t B, uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= B) return;
   const uint32_t L = c.prompt_len[i], h = c.hit[i], F = L / BS;
@@ -211,7 +213,8 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32
 // k_tab_commit (one CTA of 1024 threads, T <= 8192 slots, B <= 8192 requests).
 // The recency order after the batch is: untouched old entries (stamps of earlier batches),
 // then the batch's keys ordered by their last request.  Keep the T most recent.
-__global__ void __launch_bounds__(1024) k_tab_commit(Ctx c, uint32_t B, uint64_t b_cur) {
+__global__ void __launch_bounds__(1024) k_tab_commit(Ctx c, uint32_t B, uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   extern __shared__ uint64_t s_old[];                  // old stamps, compacted [n_old]
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_hist[256];
@@ -403,9 +406,15 @@ static il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, cons
   return IL_OK;
 }
 
-static void end_batch(Ctx* c) {
+__global__ void k_end_batch(Ctx c) { c.sc->batch_done += 1; }
+
+static il_status end_batch(Ctx* c, cudaStream_t st) {
+  k_end_batch<<<1, 1, 0, st>>>(*c);
+  IL_LAUNCH_CHECK("il_commit (end of batch)");
+  c->launches += 1;
   c->batch += 1;
   c->refined = c->matched = c->index_done = false;
+  return IL_OK;
 }
 
 extern "C" il_status il_commit(il_ctx* c, il_stream s) {
@@ -420,8 +429,7 @@ extern "C" il_status il_commit(il_ctx* c, il_stream s) {
     r = commit_table(c, c->last_B, c->final_ds, c->info, st, b_cur);
     if (r != IL_OK) return r;
   }
-  end_batch(c);
-  return IL_OK;
+  return end_batch(c, st);
 }
 
 extern "C" il_status il_commit_index(il_ctx* c, il_stream s) {
@@ -438,8 +446,8 @@ extern "C" il_status il_commit_records(il_ctx* c, uint32_t B_global, const uint3
   if (!(c->cfg.flags & IL_F_PAIR)) { set_error("il_commit_records needs IL_F_PAIR"); return IL_ERR_STATE; }
   if (B_global > c->max_records) { set_error("B_global > max_global_batch"); return IL_ERR_ARG; }
   if (B_global && (!final_ds_all || !info_all)) { set_error("null records"); return IL_ERR_ARG; }
-  il_status r = commit_table(c, B_global, final_ds_all, info_all, (cudaStream_t)s, c->batch + 1);
+  cudaStream_t st = (cudaStream_t)s;
+  il_status r = commit_table(c, B_global, final_ds_all, info_all, st, c->batch + 1);
   if (r != IL_OK) return r;
-  end_batch(c);
-  return IL_OK;
+  return end_batch(c, st);
 }

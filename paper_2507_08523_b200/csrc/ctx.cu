@@ -302,7 +302,7 @@ il_status il_stats_sync(il_ctx* c, il_stream s, il_stats* out) {
   DevScalars h;
   IL_CUDA(cudaMemcpyAsync(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)s));
   IL_CUDA(cudaStreamSynchronize((cudaStream_t)s));
-  out->batch = c->batch;
+  out->batch = h.batch_done;
   out->resident_blocks = h.resident;
   out->free_pages = h.n_free;
   out->table_entries = h.table_entries;

@@ -41,6 +41,7 @@ struct DevScalars {
   uint64_t stamp_max;
   uint64_t sel_prefix;       // selected key prefix
   uint64_t sel_key;          // final threshold key
+  uint64_t batch_done;       // committed batches (device copy: CUDA-graph replays advance it)
   uint32_t sel_remaining;
   uint32_t sel_shift;
   uint32_t cand;             // eviction candidates

@@ -15,7 +15,8 @@ namespace il {
 __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
                                                     const uint32_t* __restrict__ prompt_len,
                                                     uint64_t* __restrict__ block_hash, uint32_t* __restrict__ hit,
-                                                    int32_t* __restrict__ block_table, uint64_t b_cur) {
+                                                    int32_t* __restrict__ block_table, uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= B) return;
   const uint32_t L = prompt_len[i];
@@ -44,7 +45,8 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
 __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
                                                      const uint32_t* __restrict__ hit,
                                                      int32_t* __restrict__ prefix_len, int32_t* __restrict__ cu_q,
-                                                     uint64_t b_cur) {
+                                                     uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   __shared__ uint32_t s_need[1024], s_suf[1024];
   __shared__ int32_t s_top[1025];
   const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
@@ -126,7 +128,8 @@ __device__ __forceinline__ uint64_t ev_key(const Ctx& c, uint32_t p, uint64_t b_
   return (((st >> 32) - b_min) << 25) | ((st & 0x1FFFull) << 12) | (uint64_t)(4095u - min(c.pg_depth[p], 4095u));
 }
 
-__global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t b_cur) {
+__global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
+  const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t s_hist[EV_BINS];
   __shared__ uint64_t s_red;

@@ -96,8 +96,39 @@ class Pipeline:
                               self.k_pages, self.v_pages, self.out, self.lse if lse else None, self.scale,
                               stream=self.stream)
 
-    def commit(self) -> None:
+    def commit(self, B=None) -> None:
         self.ctx.commit(stream=self.stream)
+
+    # -------------------------------------------------------------- CUDA graphs
+    STAGES = ("refine", "match", "synth", "attn", "commit")
+
+    def capture(self, B: int, stages=STAGES) -> dict:
+        """Capture each stage for batch size B as a CUDA graph (one replay per stage removes the
+        per-kernel launch gaps).  The graphs read the pipeline's own input buffers (stage the
+        batch with stage_batch / load_inputs first) and every device state they touch (batch
+        counter, index, table) lives on the device, so replays advance the stream like eager
+        calls.  Call after at least one eager step (one-time function attributes)."""
+        own = self.stream
+        s = own if own is not None else torch.cuda.Stream(self.device)   # capture needs a side stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        self.stream = s                                 # the library launches on the capture stream
+        self.graphs = {}
+        try:
+            for name in stages:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    getattr(self, name)(B)
+                self.graphs[name] = g
+        finally:
+            self.stream = own
+        return self.graphs
+
+    def load_inputs(self, q_off: torch.Tensor, q_tok: torch.Tensor, q_src: torch.Tensor, B: int) -> None:
+        """Device-to-device copy of one batch's query CSR into the resident input buffers."""
+        self.q_off[:B + 1].copy_(q_off[:B + 1], non_blocking=True)
+        self.q_tok[:q_tok.numel()].copy_(q_tok, non_blocking=True)
+        self.q_src[:B].copy_(q_src[:B], non_blocking=True)
+        self.B = B
 
     def launches(self) -> int:
         """Kernels this context has launched so far (host-side counter in the library)."""

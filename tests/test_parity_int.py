@@ -69,3 +69,31 @@ def test_long_instruction_c3_shape():
                     n_instr=1836, T=4096, C=6000, max_prompt_tokens=2560, n_batches=8, ramp=(1, 8),
                     flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
     run_stream(sp, state_every=4)
+
+
+def test_graph_replay_stream_bit_exact():
+    """Per-stage CUDA-graph replays (bench's launch mode) advance the device state exactly like
+    eager calls: batch counter, index, table (all on the device)."""
+    import torch
+    sp = StreamSpec(B=64, C=1200, n_logs=2000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(64,))
+    ds, pool, instr = make_stream(sp)
+    o = oracle_for(sp, pool, instr)
+    pl = gpu_pipeline(sp, pool, instr)
+    sp.n_batches = 12
+    plan = batch_plan(sp, ds.n)
+    for b, (start, B) in enumerate(plan):
+        batch = gen.make_batch(ds, start, B)
+        r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=(sp.max_prompt_tokens + 15) // 16)
+        pl.stage_batch(batch)
+        if b == 0:
+            pl.step(attention=False)                   # eager once (one-time attributes)
+        else:
+            if b == 1:
+                graphs = pl.capture(B, stages=("refine", "match", "commit"))
+            for n in ("refine", "match", "commit"):
+                graphs[n].replay()
+        torch.cuda.synchronize()
+        pl.ctx.status_sync()
+        compare_batch(r, pl, B, sp, where=f"graph batch {b}")
+        compare_state(o, pl, where=f"graph batch {b}")
+    assert pl.ctx.stats()["batch"] == len(plan)
