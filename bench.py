@@ -356,9 +356,11 @@ def oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn: int, n_step
 def cpu_baseline(args, cfg, ds, pool, instr, plan, n_warm, flags):
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    v, t_int, n_int, t_att, n_att = oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn=args.cpu_attn_sample)
+    v, t_int, n_int, t_att, n_att = oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags,
+                                                  n_attn=max(1, args.cpu_baseline_attn // args.cpu_baseline_batches),
+                                                  n_steps=args.cpu_baseline_batches)
     return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"integer path of {n_int} requests (one full batch after {n_warm} warm-up batches) in {t_int:.2f} s "
+            "sample": f"integer path of {n_int} requests ({args.cpu_baseline_batches} full batches after {n_warm} warm-up batches) in {t_int:.2f} s "
                       f"+ fp64 attention of {n_att} sampled requests in {t_att:.2f} s; requests/s = 1 / per-request time",
             "cpu": cpu_model()}
 
@@ -434,7 +436,9 @@ def main():
     ap.add_argument("--naive", action="store_true", help="PAIR off (naive prefix caching)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
-    ap.add_argument("--cpu-attn-sample", type=int, default=8)
+    ap.add_argument("--cpu-attn-sample", type=int, default=8, help="--impl reference: fp64 attention requests per step")
+    ap.add_argument("--cpu-baseline-attn", type=int, default=400, help="cpu_baseline: fp64 attention requests sampled")
+    ap.add_argument("--cpu-baseline-batches", type=int, default=4, help="cpu_baseline: full batches of the integer path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

@@ -33,7 +33,10 @@ namespace sm100 {
 __device__ unsigned long long g_trace[16][4096];
 __device__ unsigned int g_trace_item[1024][4];
 #define IL_TRACE(slot, idx) \
-  do { if (blockIdx.x == 0 && phase == 1 && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
+  do { if (blockIdx.x == 0 && phase == IL_TRACE_PHASE && (idx) < 4096) g_trace[slot][idx] = clock64(); } while (0)
+#ifndef IL_TRACE_PHASE
+#define IL_TRACE_PHASE 1
+#endif
 #else
 #define IL_TRACE(slot, idx) do { } while (0)
 #endif
@@ -479,9 +482,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t_ & 1u) last0 = l;
         if (t_ & 2u) last1 = l;
       }
+      if (lane == 0) IL_TRACE(12, it & 4095);          // item decoded
       mbar_wait(bar(Q_FULL), it & 1);
+      if (lane == 0) IL_TRACE(13, it & 4095);          // Q landed
 #ifdef IL_ATTN_TRACE
-      if (blockIdx.x == 0 && phase == 1 && it < 1024 && lane == 0) {
+      if (blockIdx.x == 0 && phase == IL_TRACE_PHASE && it < 1024 && lane == 0) {
         g_trace_item[it][0] = lc; g_trace_item[it][1] = pr.nload; g_trace_item[it][2] = pr.nsh;
         g_trace_item[it][3] = pr.a.n_kv | (pr.b.n_kv << 16);
       }
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       while (q1n) pv_one(1);
       if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
       commit_w(bar(O_FULL));
+      if (lane == 0) IL_TRACE(14, it & 4095);          // last PV issued
     }
   } else if (warp >= 4) {
     // ====== softmax + epilogue: thread = (row r, key half hc); both warpgroups work on every S tile ======
@@ -772,6 +778,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tc_fence_before();
+      if (r == 0 && hc == 0) IL_TRACE(15, it & 4095);  // epilogue done
       mbar_arrive(bar(O_FREE));
     }
   }

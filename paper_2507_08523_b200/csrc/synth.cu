@@ -1,7 +1,8 @@
 // synth.cu — il_synth_qkv (bench / test helper, not the method): bf16 Q, K, V of suffix rows
 // from the counter-based generator of DESIGN.md Z28:
-//   u = mix(mix(mix(seed_t ^ token) ^ position) ^ (head * 256 + dim)),
-//   x = (int(u >> 40) - 2^23) / 2^23 * scale, rounded to bf16 (RNE),
+//   row key r = mix(mix(seed_t ^ token) ^ position)                     (64-bit, once per row)
+//   v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), e = head * 256 + dim   (32-bit, per element)
+//   x = (int(v >> 8) - 2^23) / 2^23 * scale, rounded to bf16 (RNE),
 // seed_t = mix((seed << 8) ^ salt), salt = 'Q' / 'K' / 'V'.
 #include <cuda_bf16.h>
 
@@ -10,10 +11,12 @@
 
 namespace il {
 
-__device__ __forceinline__ __nv_bfloat16 synth_val(uint64_t row_key, uint32_t hd, float mul) {
-  const uint64_t u = mix64(row_key ^ (uint64_t)hd);
-  const float x = (float)((int32_t)(u >> 40) - (1 << 23)) * mul;
-  return __float2bfloat16_rn(x);
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; return h ^ (h >> 16);
+}
+__device__ __forceinline__ float synth_val(uint64_t row_key, uint32_t e, float mul) {
+  const uint32_t v = fmix32(((uint32_t)row_key ^ (e * 0x9E3779B9u)) + (uint32_t)(row_key >> 32));
+  return (float)((int32_t)(v >> 8) - (1 << 23)) * mul;
 }
 
 // One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
@@ -46,10 +49,13 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
       if (h < Hq) { key = kq; mul = qmul; hh = h; dst = q + ((size_t)r * Hq + h) * D + x0; }
       else if (h < Hq + Hkv) { key = kk; mul = kvmul; hh = h - Hq; dst = kn + ((size_t)r * Hkv + hh) * D + x0; }
       else { key = kv; mul = kvmul; hh = h - Hq - Hkv; dst = vn + ((size_t)r * Hkv + hh) * D + x0; }
-      __align__(16) __nv_bfloat16 v[8];
+      uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = synth_val(key, hh * 256 + x0 + j, mul);
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+      for (int j = 0; j < 4; ++j) {
+        const float a = synth_val(key, hh * 256 + x0 + 2 * j, mul), b = synth_val(key, hh * 256 + x0 + 2 * j + 1, mul);
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(b), "f"(a));   // low half = a (RNE)
+      }
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }

@@ -59,6 +59,13 @@ def main():
     loads = int(items[1:n_it - 1, 1].sum())
     print("cycles per load (steady):", tot_cycles / max(loads, 1))
     da = rel[5][20:400] - rel[4][20:400]; print("softmax A duration median", np.median(da))
+    it_dec, it_q, it_last, it_epi = rel[12][:n_it], rel[13][:n_it], rel[14][:n_it], rel[15][:n_it]
+    print("per item (cycles): decoded->Q landed, Q->last PV issued, last PV->epilogue done, epilogue->next decoded")
+    for k in range(2, min(12, n_it - 1)):
+        print(f"  item {k:3d} nload {int(items[k, 1]):3d}: {it_q[k] - it_dec[k]:7d} {it_last[k] - it_q[k]:7d} "
+              f"{it_epi[k] - it_last[k]:7d} {it_dec[k + 1] - it_epi[k]:7d}")
+    span = it_dec[n_it - 1] - it_dec[1]
+    print("mean cycles per item:", span / max(n_it - 2, 1), " mean loads per item:", float(items[1:n_it - 1, 1].mean()))
     seg = [("S_FULL->ld done", 4, 8), ("ld->exchange done", 8, 9), ("exchange->exp done", 9, 10),
            ("exp->P stored", 10, 11), ("P stored->arrive", 11, 5)]
     for name, a, b in seg:

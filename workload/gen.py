@@ -236,16 +236,31 @@ def tensor_seed(seed: int, which: str) -> int:
     return int(_mix(np.array([(seed << 8) ^ QKV_TENSOR_SALT[which]], dtype=np.uint64))[0])
 
 
+def _fmix32(h: np.ndarray) -> np.ndarray:
+    """murmur3 32-bit finaliser (uint32 arrays, wrapping)."""
+    h = h ^ (h >> np.uint32(16))
+    h = (h * np.uint32(0x85EBCA6B)).astype(np.uint32)
+    h = h ^ (h >> np.uint32(13))
+    h = (h * np.uint32(0xC2B2AE35)).astype(np.uint32)
+    return h ^ (h >> np.uint32(16))
+
+
 def synth_bf16_bits(seed: int, which: str, tokens: np.ndarray, positions: np.ndarray,
                     n_heads: int, d: int, scale: float = 1.0) -> np.ndarray:
-    """[n][n_heads][d] uint16 bf16 bit patterns: x = (i32(u>>40) - 2^23)/2^23 * scale, RNE."""
+    """[n][n_heads][d] uint16 bf16 bit patterns (Z28): per (token, position) a 64-bit
+    row key r = mix(mix(seed_t ^ token) ^ position); per element (e = head * 256 + dim)
+    v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), x = (i32(v >> 8) - 2^23) / 2^23 * scale, RNE."""
     s = np.uint64(tensor_seed(seed, which))
     t = tokens.astype(np.uint64)[:, None, None]
     p = positions.astype(np.uint64)[:, None, None]
-    hd = (np.arange(n_heads, dtype=np.uint64)[None, :, None] * np.uint64(256)
-          + np.arange(d, dtype=np.uint64)[None, None, :])
-    u = _mix(_mix(_mix(s ^ t) ^ p) ^ hd)
-    x = ((u >> np.uint64(40)).astype(np.int64) - (1 << 23)).astype(np.float32)
+    r = _mix(_mix(s ^ t) ^ p)
+    lo = (r & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    hi = (r >> np.uint64(32)).astype(np.uint32)
+    e = (np.arange(n_heads, dtype=np.uint32)[None, :, None] * np.uint32(256)
+         + np.arange(d, dtype=np.uint32)[None, None, :])
+    with np.errstate(over="ignore"):
+        v = _fmix32(((lo ^ (e * np.uint32(0x9E3779B9)).astype(np.uint32)) + hi).astype(np.uint32))
+    x = ((v >> np.uint32(8)).astype(np.int64) - (1 << 23)).astype(np.float32)
     x = x * np.float32(scale / float(1 << 23))
     b = x.view(np.uint32).astype(np.uint64)
     rnd = ((b >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)
