@@ -63,6 +63,29 @@ constexpr uint32_t NBAR = 10 + 2 * NSTK + 2 * NSTV;
 constexpr uint32_t OFF_XCH = OFF_BAR + 256;          // softmax half exchange: [2][2][128] fp32
 constexpr uint32_t SMEM_BYTES = OFF_XCH + 2 * 2 * 128 * 4;
 constexpr int THREADS = 384;
+// IL_SM_PER_TILE = 1: softmax warpgroup x owns Q tile x (thread = one full 128-key row, no max
+// exchange); the two tiles' softmaxes run concurrently, so one's row max / bookkeeping overlaps the
+// other's exponentials on the MUFU pipe.  0: both warpgroups split every tile's key columns.
+#ifndef IL_SM_PER_TILE
+#define IL_SM_PER_TILE 1
+#endif
+#ifndef IL_SETMAXNREG
+#define IL_SETMAXNREG IL_SM_PER_TILE
+#endif
+#ifndef IL_REG_PROD
+#define IL_REG_PROD 56
+#endif
+#ifndef IL_REG_SM
+#define IL_REG_SM 224
+#endif
+// producers / MMA issuer need few registers; the softmax warps hold a 128-column row
+#if IL_SETMAXNREG
+#define IL_REGS_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IL_REG_PROD))
+#define IL_REGS_INC() asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IL_REG_SM))
+#else
+#define IL_REGS_DEC() do { } while (0)
+#define IL_REGS_INC() do { } while (0)
+#endif
 constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
 // S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
@@ -369,7 +392,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
     for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
     for (int x = 0; x < 2; ++x) {
-      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), SM_THREADS); mbar_init(bar(PV_DONE + x), 1);
+      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), IL_SM_PER_TILE ? 128 : SM_THREADS);
+      mbar_init(bar(PV_DONE + x), 1);
     }
     mbar_init(bar(O_FULL), 1); mbar_init(bar(O_FREE), SM_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -392,6 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #ifndef IL_Q_WARP
 #define IL_Q_WARP 2
 #endif
+  if (warp == 2) IL_REGS_DEC();
   if (IL_Q_WARP == 2 && warp == 2) {
     // ============ Q producer: the next item's Q tiles load as soon as the last QK of the
     // current item has read Q (the K / V producers run ahead independently) ============
@@ -416,6 +441,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == 0 || warp == 3) {
     // ============ TMA producers: warp 0 = K tiles, warp 3 = V tiles ============
+    IL_REGS_DEC();
     const bool is_k = warp == 0;
     const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
     const uint32_t nst = is_k ? NSTK : NSTV;
@@ -469,6 +495,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // Per Q tile x the 64-key tiles n = 0, 1, 2, ... alternate TMEM buffers n & 1; QK of tile
     // n+2 reuses the buffer of n, so it is issued right after PV(n) (tcgen05 ops from one
     // thread execute in order).  The two Q tiles' chains interleave on the tensor pipe.
+    IL_REGS_DEC();
     const uint64_t dqa = sdesc(sbase + OFF_QA, 16, 1024), dqb = sdesc(sbase + OFF_QB, 16, 1024);
     const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024), dv0 = sdesc(sbase + OFF_V, KCB, 1024);
     uint32_t lc = 0, it = 0, cnt0 = 0, cnt1 = 0;
@@ -552,6 +579,155 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
       commit_w(bar(O_FULL));
       if (lane == 0) IL_TRACE(14, it & 4095);          // last PV issued
+    }
+  } else if (warp >= 4 && IL_SM_PER_TILE) {
+    // ====== softmax + epilogue, one warpgroup per Q tile: thread = row r of tile xo ======
+    IL_REGS_INC();
+    const uint32_t sm_t = threadIdx.x - 128, xo = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
+    const uint32_t lane_addr = (32 * q4) << 16;
+    const uint32_t s_tmem = tmem + lane_addr + 128 * xo, o_tmem = tmem + lane_addr + 256 + 128 * xo;
+    uint32_t it = 0, cnt = 0;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
+      const Tile& T = xo ? pr.b : pr.a;
+      const uint32_t t = r / g, hh = r % g;
+      const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
+      const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
+      const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh;
+      float m_used = -INFINITY, l = 0.f;
+      if (phase == 1 && T.valid) {
+        // continue phase 2's partial (m + log2 l, O / l) of these rows: state (m + log2 l, 1, O / l).
+        // Warp-uniform (tcgen05.st is .aligned); padding rows store zeros.
+        if (valid) { m_used = c.attn_ml[orow]; l = 1.f; }
+        const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
+        uint4 raw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[j] = valid ? src[j] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 u = raw[4 * q + j];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
+              ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+            }
+          }
+          tmem_st32(o_tmem + 32 * q, ov);
+        }
+        tmem_wait_st();
+      }
+      for (uint32_t ld = 0; ld < pr.nload; ++ld) {
+        uint32_t n, req_, tgt;
+        load_info(pr, ld, n, req_, tgt);
+        if (!(tgt & (1u << xo))) continue;
+        mbar_wait(bar(S_FULL + xo), cnt & 1);
+        tc_fence_after();
+        const uint32_t key0 = (T.kv0 + n) * BN;
+        float a[128];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_ld32(s_tmem + 32 * q, *reinterpret_cast<float(*)[32]>(&a[32 * q]));
+        tmem_wait_ld();
+        if (phase == 2 && key0 + BN - 1 > pos_q) {
+#pragma unroll
+          for (int j = 0; j < 128; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
+        }
+        float mxa[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mxa[q] = a[q];
+#pragma unroll
+        for (int j = 8; j < 128; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float mx2 = mx * scale_log2;
+        bool need = false;
+        float factor = 1.f;
+        if (m_used == -INFINITY) {
+          m_used = mx2;
+        } else if (mx2 > m_used + 8.f) {
+          need = true;
+          factor = ex2(m_used - mx2);
+          m_used = mx2;
+          l *= factor;
+        }
+        if (__any_sync(~0u, need)) {
+          // lazy rescale of this row's O once the previous tile's PV has landed
+          mbar_wait(bar(PV_DONE + xo), (cnt - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float ov[32];
+            tmem_ld32(o_tmem + 32 * q, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] *= factor;
+            tmem_st32(o_tmem + 32 * q, ov);
+          }
+          tmem_wait_st();
+        }
+        // a fully masked row (no key yet) keeps p = 0: exp2(-inf - 0)
+        const float negm = m_used == -INFINITY ? 0.f : -m_used;
+        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int jj = 0; jj < 64; jj += 2) {
+            const int j = 64 * h + jj;
+            float x0, x1;
+            ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+            float p0, p1;
+            if ((IL_EXP_EMU_PAIRS >> ((j >> 1) & 7)) & 1) {
+              ex2_poly2(x0, x1, p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+            pk[jj >> 1] = pack_bf16(p0, p1);
+          }
+          // P (bf16 pairs) of keys [64h, 64h + 64) -> TMEM columns [32h, 32h + 32) of this S
+          tmem_st32u(s_tmem + 32 * h, pk);
+        }
+        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar(P_FULL + xo));
+        ++cnt;
+      }
+      // epilogue: O / l -> bf16 row of `out`, natural-log LSE (or the phase-2 partial)
+      mbar_wait(bar(O_FULL), it & 1);
+      tc_fence_after();
+      if (T.valid) {
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+          tmem_ld32(o_tmem + 32 * q, ov);
+          tmem_wait_ld();
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              uint4 v;
+              v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
+              v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
+              v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
+              v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
+              dst[ch] = v;
+            }
+          }
+        }
+        if (valid) {
+          if (phase == 2 && cascade) c.attn_ml[orow] = m_used + __log2f(l);
+          else if (lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(O_FREE));
     }
   } else if (warp >= 4) {
     // ====== softmax + epilogue: thread = (row r, key half hc); both warpgroups work on every S tile ======
