@@ -59,18 +59,20 @@ constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
 constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
 constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
 constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
-constexpr uint32_t NBAR = 10 + 2 * NSTK + 2 * NSTV;
-constexpr uint32_t OFF_XCH = OFF_BAR + 256;          // softmax half exchange: [2][2][128] fp32
-constexpr uint32_t SMEM_BYTES = OFF_XCH + 2 * 2 * 128 * 4;
+constexpr uint32_t NBAR = 14 + 2 * NSTK + 2 * NSTV;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
 constexpr int THREADS = 384;
-// IL_SM_PER_TILE = 1: softmax warpgroup x owns Q tile x (thread = one full 128-key row, no max
-// exchange); the two tiles' softmaxes run concurrently, so one's row max / bookkeeping overlaps the
-// other's exponentials on the MUFU pipe.  0: both warpgroups split every tile's key columns.
-#ifndef IL_SM_PER_TILE
-#define IL_SM_PER_TILE 1
+// Softmax warpgroup x owns Q tile x (thread = one full 128-key row, no max exchange); the two
+// tiles' softmaxes run concurrently, so one's row max / bookkeeping overlaps the other's
+// exponentials.  (Round-1 history: both warpgroups splitting every tile's key columns with a
+// row-max exchange through smem was 8% slower, git 11b8cd7.)
+// IL_P_SPLIT = 1: P is released in two 64-key halves, so the first half's PV MMAs overlap the
+// second half's exponentials.
+#ifndef IL_P_SPLIT
+#define IL_P_SPLIT 1
 #endif
 #ifndef IL_SETMAXNREG
-#define IL_SETMAXNREG IL_SM_PER_TILE
+#define IL_SETMAXNREG 1
 #endif
 #ifndef IL_REG_PROD
 #define IL_REG_PROD 56
@@ -86,13 +88,12 @@ constexpr int THREADS = 384;
 #define IL_REGS_DEC() do { } while (0)
 #define IL_REGS_INC() do { } while (0)
 #endif
-constexpr uint32_t SM_THREADS = 256;     // two softmax warpgroups
 
 // S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
 enum Bar : uint32_t { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = K_FULL + NSTK, V_FULL = K_FREE + NSTK,
                       V_FREE = V_FULL + NSTV, S_FULL = V_FREE + NSTV, P_FULL = S_FULL + 2, PV_DONE = P_FULL + 2,
-                      O_FULL = PV_DONE + 2, O_FREE = O_FULL + 1 };
-static_assert(O_FREE + 1 == NBAR, "barrier map");
+                      O_FULL = PV_DONE + 2, O_FREE = O_FULL + 2, P_HALF = O_FREE + 2 };
+static_assert(P_HALF + 2 == NBAR, "barrier map");
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -392,10 +393,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
     for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
     for (int x = 0; x < 2; ++x) {
-      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), IL_SM_PER_TILE ? 128 : SM_THREADS);
-      mbar_init(bar(PV_DONE + x), 1);
+      mbar_init(bar(S_FULL + x), 1); mbar_init(bar(P_FULL + x), 128);
+      mbar_init(bar(PV_DONE + x), 1); mbar_init(bar(P_HALF + x), 128);
+      mbar_init(bar(O_FULL + x), 1); mbar_init(bar(O_FREE + x), 128);
     }
-    mbar_init(bar(O_FULL), 1); mbar_init(bar(O_FREE), SM_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_k) : "memory");
@@ -521,12 +522,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       // pending PV per Q tile (S is single-buffered: PV(n) must precede QK(n+1)):
       // (load counter, tile count)
-      uint32_t q0n = 0, q0l = 0, q0c = 0, q1n = 0, q1l = 0, q1c = 0;
-      bool first0 = phase != 1, first1 = phase != 1, o_ready = it == 0;   // phase 1 accumulates onto the partial
+      // (+ item-local load index, so the last PV of a tile commits that tile's O_FULL: the two
+      // tiles' epilogues and the next item's first PVs then proceed per tile)
+      uint32_t q0n = 0, q0l = 0, q0c = 0, q0i = 0, q1n = 0, q1l = 0, q1c = 0, q1i = 0;
+      bool first0 = phase != 1, first1 = phase != 1;   // phase 1 accumulates onto the partial
+      bool o_ready0 = it == 0, o_ready1 = it == 0;
       auto pv_one = [&](const uint32_t x) {
         const uint32_t pl = x ? q1l : q0l, pc = x ? q1c : q0c, vs = pl % NSTV;
-        if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
-        mbar_wait(bar(P_FULL + x), pc & 1);
+        if (!(x ? o_ready1 : o_ready0)) {                // the previous item's epilogue of tile x is done
+          mbar_wait(bar(O_FREE + x), (it - 1) & 1);
+          if (x) o_ready1 = true; else o_ready0 = true;
+        }
+        mbar_wait(bar((IL_P_SPLIT ? P_HALF : P_FULL) + x), pc & 1);
         mbar_wait(bar(V_FULL + vs), (pl / NSTV) & 1);
         if (lane == 0) IL_TRACE(3, (2 * pl + x) & 4095);
         tc_fence_after();
@@ -535,16 +542,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool fst = x ? first1 : first0;
         // K = 128 keys in 8 steps of 16 (V tile rows; 16 keys = 2 swizzle atoms = 2048 B)
 #pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
+        for (uint32_t k = 0; k < 8; ++k) {
+          // IL_P_SPLIT: keys 0-63 of P are released first; their MMAs run while the softmax
+          // computes keys 64-127
+          if (IL_P_SPLIT && k == 4) { mbar_wait(bar(P_FULL + x), pc & 1); tc_fence_after(); }
           mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst && k == 0) ? 0u : 1u);
+        }
         if (x) first1 = false; else first0 = false;
         commit_w(bar(PV_DONE + x));
+        if ((x ? q1i : q0i) == (x ? last1 : last0)) commit_w(bar(O_FULL + x));
         const uint32_t sh = 2 * (pl & 7);
         vus -= 1u << sh;
         if (((vus >> sh) & 3u) == 0) commit_w(bar(V_FREE + vs));
         if (x) q1n = 0; else q0n = 0;
       };
-      auto qk = [&](const uint32_t x, const uint64_t dk) {
+      auto qk = [&](const uint32_t x, const uint64_t dk, const uint32_t li) {
         if (x ? q1n : q0n) pv_one(x);                 // frees the S/P columns this QK overwrites
         const uint32_t sc = x ? cnt1++ : cnt0++;
         const uint32_t s_tmem = tmem + 128 * x;
@@ -554,7 +566,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_ss_w<IDESC_QK>(s_tmem, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
                              dk + (uint64_t)(((k >> 2) * KCB + (k & 3) * 32) >> 4), k ? 1u : 0u);
         commit_w(bar(S_FULL + x));
-        if (x) { q1l = lc; q1c = sc; q1n = 1; } else { q0l = lc; q0c = sc; q0n = 1; }
+        if (x) { q1l = lc; q1c = sc; q1i = li; q1n = 1; } else { q0l = lc; q0c = sc; q0i = li; q0n = 1; }
       };
       for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
         uint32_t n, req, tgt;
@@ -568,19 +580,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t sh = 2 * (lc & 7);
         vus = (vus & ~(3u << sh)) | (((tgt == 3) ? 2u : 1u) << sh);
         const uint64_t dk = dk0 + (uint64_t)((ks * KVTILE) >> 4);
-        if (tgt & 1u) qk(0, dk);
-        if (tgt & 2u) qk(1, dk);
+        if (tgt & 1u) qk(0, dk, l);
+        if (tgt & 2u) qk(1, dk, l);
         commit_w(bar(K_FREE + ks));
         if (l + 1 == pr.nload) commit_w(bar(Q_FREE));
       }
       if (pr.nload == 0) commit_w(bar(Q_FREE));        // (not reached: every item has a KV tile)
       while (q0n) pv_one(0);
       while (q1n) pv_one(1);
-      if (!o_ready) { mbar_wait(bar(O_FREE), (it - 1) & 1); o_ready = true; }
-      commit_w(bar(O_FULL));
+      if (!pr.b.valid) commit_w(bar(O_FULL + 1));     // (tile A always has a KV tile)
       if (lane == 0) IL_TRACE(14, it & 4095);          // last PV issued
     }
-  } else if (warp >= 4 && IL_SM_PER_TILE) {
+  } else if (warp >= 4) {
     // ====== softmax + epilogue, one warpgroup per Q tile: thread = row r of tile xo ======
     IL_REGS_INC();
     const uint32_t sm_t = threadIdx.x - 128, xo = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
@@ -625,12 +636,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         load_info(pr, ld, n, req_, tgt);
         if (!(tgt & (1u << xo))) continue;
         mbar_wait(bar(S_FULL + xo), cnt & 1);
+        if (r == 0) IL_TRACE(4 + 2 * xo, cnt & 4095);
         tc_fence_after();
         const uint32_t key0 = (T.kv0 + n) * BN;
         float a[128];
 #pragma unroll
         for (int q = 0; q < 4; ++q) tmem_ld32(s_tmem + 32 * q, *reinterpret_cast<float(*)[32]>(&a[32 * q]));
         tmem_wait_ld();
+        if (r == 0 && xo == 0) IL_TRACE(8, cnt & 4095);
         if (phase == 2 && key0 + BN - 1 > pos_q) {
 #pragma unroll
           for (int j = 0; j < 128; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
@@ -642,6 +655,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 8; j < 128; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
         const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        if (r == 0 && xo == 0) IL_TRACE(9, cnt & 4095);
         const float mx2 = mx * scale_log2;
         bool need = false;
         float factor = 1.f;
@@ -691,15 +705,23 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           // P (bf16 pairs) of keys [64h, 64h + 64) -> TMEM columns [32h, 32h + 32) of this S
           tmem_st32u(s_tmem + 32 * h, pk);
+          if (IL_P_SPLIT && h == 0) {                    // first half of P -> its PV MMAs may start
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(bar(P_HALF + xo));
+          }
         }
         l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        if (r == 0 && xo == 0) IL_TRACE(10, cnt & 4095);
         tmem_wait_st();
+        if (r == 0 && xo == 0) IL_TRACE(11, cnt & 4095);
         tc_fence_before();
+        if (r == 0) IL_TRACE(5 + 2 * xo, cnt & 4095);
         mbar_arrive(bar(P_FULL + xo));
         ++cnt;
       }
       // epilogue: O / l -> bf16 row of `out`, natural-log LSE (or the phase-2 partial)
-      mbar_wait(bar(O_FULL), it & 1);
+      mbar_wait(bar(O_FULL + xo), it & 1);
       tc_fence_after();
       if (T.valid) {
         const float inv = 1.f / l;
@@ -727,235 +749,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(bar(O_FREE));
-    }
-  } else if (warp >= 4) {
-    // ====== softmax + epilogue: thread = (row r, key half hc); both warpgroups work on every S tile ======
-    // Tiles are taken in the MMA warp's issue order (per load: A then B).  Each thread owns 64 of
-    // the 128 key columns of its row; the two halves exchange their partial row max through
-    // shared memory (double buffered by tile parity, one named barrier per tile), so one tile's
-    // softmax runs on all 8 warps and its latency (the critical path S -> P -> PV -> next S) halves.
-    const uint32_t sm_t = threadIdx.x - 128, hc = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
-    const uint32_t lane_addr = (32 * q4) << 16;
-    float* xch = reinterpret_cast<float*>(smem + OFF_XCH);   // [2 parity][2 halves][128 rows]
-    uint32_t it = 0, cnt0 = 0, cnt1 = 0, par = 0;
-    // phase 1: the partial of an item's rows is fetched one item ahead (issued before the
-    // previous epilogue waits for its last PV) so its latency stays off the critical path
-    uint4 pf_raw[2][8];
-    float pf_m[2];
-    auto prefetch = [&](uint32_t wn) {
-      const Pair pn = decode_pair(c, cu_q, prefix_len, wn, Hkv, TQ, phase, NC);
-      const uint32_t t = r / g, hh = r % g;
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const Tile& T = x ? pn.b : pn.a;
-        pf_m[x] = -INFINITY;
-        if (T.valid && r < g * TQ && t < T.ntok) {
-          const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pn.kh * g + hh;
-          pf_m[x] = c.attn_ml[orow];
-          const uint4* src = reinterpret_cast<const uint4*>(out + orow * D + 64 * hc);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) pf_raw[x][j] = src[j];
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) pf_raw[x][j] = make_uint4(0u, 0u, 0u, 0u);
-        }
-      }
-    };
-#ifndef IL_INIT_PREFETCH
-#define IL_INIT_PREFETCH 0
-#endif
-    if (phase == 1 && blockIdx.x < n_items) prefetch(blockIdx.x);
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      const uint32_t t = r / g, hh = r % g;
-      bool valid[2];
-      uint32_t pos_q[2];
-      size_t orow[2];
-      float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const Tile& T = x ? pr.b : pr.a;
-        valid[x] = T.valid && (r < g * TQ) && (t < T.ntok);
-        pos_q[x] = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
-        orow[x] = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh;
-      }
-      if (!IL_INIT_PREFETCH && phase == 1) prefetch(w);
-      if (phase == 1) {
-        // continue phase 2's partial of these rows (prefetched during the previous item's
-        // epilogue): the state (m + log2 l, 1, O / l) is the same softmax state (the mass 1 goes
-        // to half 0's partial sum).  Warp-uniform: tcgen05.st is .aligned; padding rows store zeros.
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-          const Tile& T = x ? pr.b : pr.a;
-          if (!T.valid) continue;                        // uniform over the CTA
-          if (valid[x]) {
-            m_used[x] = pf_m[x];
-            l[x] = hc == 0 ? 1.f : 0.f;
-          }
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            float ov[32];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint4 u = pf_raw[x][4 * q + j];
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
-                ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
-              }
-            }
-            tmem_st32(tmem + lane_addr + 256 + 128 * x + 64 * hc + 32 * q, ov);
-          }
-        }
-        tmem_wait_st();
-      }
-      for (uint32_t ld = 0; ld < pr.nload; ++ld) {
-        uint32_t n, req_, tgt;
-        load_info(pr, ld, n, req_, tgt);
-#pragma unroll
-        for (uint32_t x = 0; x < 2; ++x) {
-          if (!(tgt & (1u << x))) continue;
-          const Tile& T = x ? pr.b : pr.a;
-          const uint32_t cnt = x ? cnt1++ : cnt0++;
-          const uint32_t s_tmem = tmem + lane_addr + 128 * x + 64 * hc;
-          const uint32_t o_tmem = tmem + lane_addr + 256 + 128 * x + 64 * hc;
-          mbar_wait(bar(S_FULL + x), cnt & 1);
-          if (r == 0 && hc == 0) IL_TRACE(4 + 2 * x, cnt & 4095);
-          tc_fence_after();
-#ifdef IL_DBG_NOSOFTMAX
-          if (true) { tc_fence_before(); mbar_arrive(bar(P_FULL + x)); continue; }   // timing experiment only
-#endif
-          const uint32_t key0 = (T.kv0 + n) * BN + 64 * hc;
-          const bool masked = phase == 2 && key0 + 63 > pos_q[x];
-          float a[64];
-          tmem_ld32(s_tmem, *reinterpret_cast<float(*)[32]>(&a[0]));
-          tmem_ld32(s_tmem + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
-          tmem_wait_ld();
-          if (r == 0 && hc == 0 && x == 0) IL_TRACE(8, cnt & 4095);
-          if (masked) {
-#pragma unroll
-            for (int j = 0; j < 64; ++j) if (key0 + j > pos_q[x]) a[j] = -INFINITY;
-          }
-          float mxa[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) mxa[q] = a[q];
-#pragma unroll
-          for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
-          const float mxh = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                  fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-#ifdef IL_DBG_NOXCH
-          const float mx = mxh;                          // timing experiment only
-#else
-          xch[(par * 2 + hc) * 128 + r] = mxh;
-          named_bar_sync(1, SM_THREADS);
-          const float mx = fmaxf(mxh, xch[(par * 2 + (hc ^ 1)) * 128 + r]);
-#endif
-          par ^= 1;
-          if (r == 0 && hc == 0 && x == 0) IL_TRACE(9, cnt & 4095);
-          const float mx2 = mx * scale_log2;
-          bool need = false;
-          float factor = 1.f;
-          if (m_used[x] == -INFINITY) {
-            m_used[x] = mx2;
-          } else if (mx2 > m_used[x] + 8.f) {
-            need = true;
-            factor = ex2(m_used[x] - mx2);
-            m_used[x] = mx2;
-            l[x] *= factor;
-          }
-          if (__any_sync(~0u, need)) {
-            // lazy rescale of this thread's 64 O columns once the previous tile's PV has landed
-            mbar_wait(bar(PV_DONE + x), (cnt - 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              float ov[32];
-              tmem_ld32(o_tmem + 32 * q, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) ov[j] *= factor;
-              tmem_st32(o_tmem + 32 * q, ov);
-            }
-            tmem_wait_st();
-          }
-          // a fully masked row (no key yet) keeps p = 0: exp2(-inf - 0)
-          const float negm = m_used[x] == -INFINITY ? 0.f : -m_used[x];
-          float rsa[4] = {0.f, 0.f, 0.f, 0.f};
-          uint32_t pk[32];
-#pragma unroll
-          for (int j = 0; j < 64; j += 2) {
-            float x0, x1;
-            ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
-            float p0, p1;
-#ifdef IL_DBG_NOEXP
-            if (true) { p0 = x0; p1 = x1; } else   // timing experiment only: no exponential
-#endif
-            if ((IL_EXP_EMU_PAIRS >> ((j >> 1) & 7)) & 1) {
-              ex2_poly2(x0, x1, p0, p1);
-            } else {
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-            }
-            fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
-            pk[j >> 1] = pack_bf16(p0, p1);
-          }
-          l[x] += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
-          if (r == 0 && hc == 0 && x == 0) IL_TRACE(10, cnt & 4095);
-          // P (bf16 pairs) of keys [64hc, 64hc + 64) -> TMEM columns [32hc, 32hc + 32) of this S
-          // (half 0 read its S columns before the exchange barrier, so half 1 may overwrite them)
-          tmem_st32u(tmem + lane_addr + 128 * x + 32 * hc, pk);
-          tmem_wait_st();
-          if (r == 0 && hc == 0 && x == 0) IL_TRACE(11, cnt & 4095);
-          tc_fence_before();
-          if (r == 0 && hc == 0) IL_TRACE(5 + 2 * x, cnt & 4095);
-          mbar_arrive(bar(P_FULL + x));
-        }
-      }
-      if (IL_INIT_PREFETCH && phase == 1 && w + gridDim.x < n_items) prefetch(w + gridDim.x);
-      // epilogue: combine the two halves' row sums, O / l -> bf16 rows of `out`, natural-log LSE
-      // (two exchange rounds with the same parity protocol as the per-tile max exchange)
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        xch[(par * 2 + hc) * 128 + r] = l[x];
-        named_bar_sync(1, SM_THREADS);
-        l[x] += xch[(par * 2 + (hc ^ 1)) * 128 + r];
-        par ^= 1;
-      }
-      mbar_wait(bar(O_FULL), it & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const Tile& T = x ? pr.b : pr.a;
-        if (!T.valid) continue;
-        const float inv = 1.f / l[x];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          float ov[32];
-          tmem_ld32(tmem + lane_addr + 256 + 128 * x + 64 * hc + 32 * q, ov);
-          tmem_wait_ld();
-          if (valid[x]) {
-            uint4* dst = reinterpret_cast<uint4*>(out + orow[x] * D + 64 * hc + 32 * q);
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-              uint4 v;
-              v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
-              v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
-              v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
-              v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
-              dst[ch] = v;
-            }
-          }
-        }
-        if (valid[x] && hc == 0) {
-          if (phase == 2 && cascade) c.attn_ml[orow[x]] = m_used[x] + __log2f(l[x]);
-          else if (lse) lse[orow[x]] = (m_used[x] + __log2f(l[x])) * 0.69314718055994531f;
-        }
-      }
-      tc_fence_before();
-      if (r == 0 && hc == 0) IL_TRACE(15, it & 4095);  // epilogue done
-      mbar_arrive(bar(O_FREE));
+      if (r == 0 && xo == 0) IL_TRACE(15, it & 4095);  // epilogue done
+      mbar_arrive(bar(O_FREE + xo));
     }
   }
   tc_fence_before();
