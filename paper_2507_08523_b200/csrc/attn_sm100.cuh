@@ -59,7 +59,7 @@ constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
 constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
 constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
 constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
-constexpr uint32_t NBAR = 14 + 2 * NSTK + 2 * NSTV;
+constexpr uint32_t NBAR = 16 + 2 * NSTK + 2 * NSTV;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
 constexpr int THREADS = 384;
 // Softmax warpgroup x owns Q tile x (thread = one full 128-key row, no max exchange); the two
@@ -75,10 +75,10 @@ constexpr int THREADS = 384;
 #define IL_SETMAXNREG 1
 #endif
 #ifndef IL_REG_PROD
-#define IL_REG_PROD 56
+#define IL_REG_PROD 72
 #endif
 #ifndef IL_REG_SM
-#define IL_REG_SM 224
+#define IL_REG_SM 216
 #endif
 // producers / MMA issuer need few registers; the softmax warps hold a 128-column row
 #if IL_SETMAXNREG
@@ -89,8 +89,8 @@ constexpr int THREADS = 384;
 #define IL_REGS_INC() do { } while (0)
 #endif
 
-// S_FULL / P_FULL are per (Q tile x, sub-tile buffer h): index + 2 * x + h
-enum Bar : uint32_t { Q_FULL = 0, Q_FREE = 1, K_FULL = 2, K_FREE = K_FULL + NSTK, V_FULL = K_FREE + NSTK,
+// Q_*, S_FULL, P_*, PV_DONE, O_* are per Q tile (stream) x: index + x
+enum Bar : uint32_t { Q_FULL = 0, Q_FREE = 2, K_FULL = 4, K_FREE = K_FULL + NSTK, V_FULL = K_FREE + NSTK,
                       V_FREE = V_FULL + NSTV, S_FULL = V_FREE + NSTV, P_FULL = S_FULL + 2, PV_DONE = P_FULL + 2,
                       O_FULL = PV_DONE + 2, O_FREE = O_FULL + 2, P_HALF = O_FREE + 2 };
 static_assert(P_HALF + 2 == NBAR, "barrier map");
@@ -146,6 +146,12 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+// L2 prefetch of a TMA box (no smem, no barrier): warms L2 for a later tma_load_3d
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"((uint64_t)map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -232,7 +238,7 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x for a PAIR on the FMA pipe (exp2 emulation, offloads the MUFU unit) with packed fp32x2 ops: magic-number
 // rounding to j, cubic in f = x - j, 2^j added to the exponent field by one IMAD per element).
 #ifndef IL_EXP_EMU_PAIRS
-#define IL_EXP_EMU_PAIRS 0x4A                        // pairs (j/2) % 8 in {1, 3, 6}: 3 of 8 emulated
+#define IL_EXP_EMU_PAIRS 0                           // bit (j/2) % 8 set: that pair emulated (0x4A, 3 of 8, was best with split softmax)
 #endif
 __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   x0 = fmaxf(x0, -125.f);
@@ -364,9 +370,96 @@ __device__ __forceinline__ void load_info(const Pair& p, uint32_t l, uint32_t& n
   if (ra > rb) { n = p.nsh + j; req = p.a.i; tgt = 1; } else { n = p.nsh + j; req = p.b.i; tgt = 2; }
 }
 
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
+// One KV tile load of the CTA's load sequence: absolute KV tile kvt of request req (its block
+// table row, nblk blocks), kv head kh, target mask tgt (bit x = Q tile / stream x), and per
+// target stream whether this is the first / last load of the stream's current item and that
+// item's index among the stream's items (barrier parities).
+struct Load {
+  uint32_t kvt, req, nblk, kh, tgt, first, last;
+  uint32_t ix[2];
+};
+// The CTA's load sequence, walked identically by the K producer, the V producer and the MMA
+// issuer.  Pair mode (phase 1): items are pairs (A, B) of one kv head and a KV tile both need is
+// loaded once (load_info order).  Stream mode (phase 2, short items that share few tiles): the
+// A tiles and the B tiles of the CTA's items are two independent streams whose loads alternate
+// (A, B, A, B, ..., then the rest of the longer one), so one stream's item boundary (final PV,
+// epilogue, next Q) never waits for the other stream's item to end.
+struct LoadSeq {
+  const Ctx* c;
+  const int32_t* cu_q;
+  const int32_t* prefix_len;
+  uint32_t Hkv, TQ, phase, NC, n_items, stride;
+  bool streams;
+  uint32_t w, l, it, seen0, seen1;                     // pair mode
+  Pair pr;
+  uint32_t sw[2], sl[2], six[2], lastx;                 // stream mode
+  Tile st[2];
+  bool act[2];
+
+  template <uint32_t X>
+  __device__ __forceinline__ void seek() {
+    while (sw[X] < n_items) {
+      st[X] = decode_tile(*c, cu_q, prefix_len, 2 * (sw[X] / Hkv) + X, TQ, phase, NC);
+      if (st[X].valid && st[X].n_kv > 0) break;
+      sw[X] += stride;
+    }
+    act[X] = sw[X] < n_items;
+    sl[X] = 0;
+  }
+  template <uint32_t X>
+  __device__ __forceinline__ void stream_load(Load& L) {
+    lastx = X;
+    const Tile& T = st[X];
+    L.kvt = T.kv0 + sl[X]; L.req = T.i; L.nblk = T.nblk; L.kh = sw[X] % Hkv; L.tgt = 1u << X;
+    L.first = sl[X] == 0 ? L.tgt : 0u;
+    L.last = sl[X] + 1 == T.n_kv ? L.tgt : 0u;
+    L.ix[0] = six[0]; L.ix[1] = six[1];
+    if (++sl[X] == T.n_kv) { ++six[X]; sw[X] += stride; seek<X>(); }
+  }
+  __device__ __forceinline__ void init(const Ctx* c_, const int32_t* cu_q_, const int32_t* prefix_len_, uint32_t Hkv_,
+                                       uint32_t TQ_, uint32_t phase_, uint32_t NC_, uint32_t n_items_, bool streams_) {
+    c = c_; cu_q = cu_q_; prefix_len = prefix_len_; Hkv = Hkv_; TQ = TQ_; phase = phase_; NC = NC_;
+    n_items = n_items_; stride = gridDim.x; streams = streams_;
+    if (streams) {
+      sw[0] = sw[1] = blockIdx.x; six[0] = six[1] = 0;
+      seek<0>(); seek<1>();
+      lastx = 1;
+    } else {
+      w = blockIdx.x; l = 0; it = 0; seen0 = seen1 = 0;
+      if (w < n_items) pr = decode_pair(*c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
+    }
+  }
+  __device__ __forceinline__ bool next(Load& L) {
+    if (streams) {
+      // alternate A, B, A, B, ...; an exhausted stream leaves its turns to the other
+      const bool pick1 = lastx == 0 ? act[1] : !act[0];
+      if (pick1 ? !act[1] : !act[0]) return false;
+      if (pick1) stream_load<1>(L); else stream_load<0>(L);
+      return true;
+    }
+    if (w >= n_items) return false;
+    uint32_t n, req, tgt;
+    load_info(pr, l, n, req, tgt);
+    L.kvt = pr.a.kv0 + n; L.req = req; L.nblk = req == pr.a.i ? pr.a.nblk : pr.b.nblk; L.kh = pr.kh; L.tgt = tgt;
+    L.first = L.last = 0;
+    if (tgt & 1u) { L.first |= seen0 == 0 ? 1u : 0u; L.last |= seen0 + 1 == pr.a.n_kv ? 1u : 0u; ++seen0; }
+    if (tgt & 2u) { L.first |= seen1 == 0 ? 2u : 0u; L.last |= seen1 + 1 == pr.b.n_kv ? 2u : 0u; ++seen1; }
+    L.ix[0] = L.ix[1] = it;    // (an invalid B tile only occurs in the CTA's last items)
+    if (++l == pr.nload) {
+      w += stride; ++it; l = 0; seen0 = seen1 = 0;
+      if (w < n_items) pr = decode_pair(*c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
+    }
+    return true;
+  }
+  // a stream that has no further loads
+  __device__ __forceinline__ bool done(uint32_t x) const { return streams && !act[x]; }
+};
+#ifndef IL_Q_PREFETCH
+#define IL_Q_PREFETCH 1
+#endif
+#ifndef IL_STREAMS
+#define IL_STREAMS 0
+#endif
 
 __global__ void __launch_bounds__(THREADS, 1)
     k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
@@ -386,9 +479,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // (phase 1 with NC = 0 has nothing to do: every item would have zero KV tiles)
   const uint32_t n_items = phase == 1 ? (NC ? cdiv(c.sc->n_dense, 2) * Hkv : 0u) : cdiv(c.sc->n_tiles, 2) * Hkv;
   const bool cascade = NC > 0;                          // phase 2 leaves a partial that phase 1 merges
+  const bool streams = IL_STREAMS && phase == 2;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar(Q_FULL), 1); mbar_init(bar(Q_FREE), 1);
+    for (uint32_t x = 0; x < 2; ++x) { mbar_init(bar(Q_FULL + x), 1); mbar_init(bar(Q_FREE + x), 1); }
     for (uint32_t s = 0; s < NSTK; ++s) { mbar_init(bar(K_FULL + s), 1); mbar_init(bar(K_FREE + s), 1); }
     static_assert(K_FREE == K_FULL + NSTK && V_FULL == K_FREE + NSTK && V_FREE == V_FULL + NSTV, "barrier map");
     for (uint32_t s = 0; s < NSTV; ++s) { mbar_init(bar(V_FULL + s), 1); mbar_init(bar(V_FREE + s), 1); }
@@ -414,33 +508,44 @@ __global__ void __launch_bounds__(THREADS, 1)
   // TMEM columns: S_A [0,128), S_B [128,256) (the P of a tile overwrites the first 64 columns
   // of its S as packed bf16), O_A [256,384), O_B [384,512).
 
-#ifndef IL_Q_WARP
-#define IL_Q_WARP 2
-#endif
-  if (warp == 2) IL_REGS_DEC();
-  if (IL_Q_WARP == 2 && warp == 2) {
-    // ============ Q producer: the next item's Q tiles load as soon as the last QK of the
-    // current item has read Q (the K / V producers run ahead independently) ============
-    uint32_t it = 0;
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      if (lane == 0) {
-        const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-        if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
-        const uint32_t qbytes = 2 * 128 * g * TQ;
-        mbar_expect_tx(bar(Q_FULL), pr.b.valid ? 2 * qbytes : qbytes);
-        const int ra = (int)(pr.a.r0 + pr.a.mt * TQ);
-        tma_load_3d(sbase + OFF_QA, &tm_q, 0, (int)(pr.kh * g), ra, bar(Q_FULL));
-        tma_load_3d(sbase + OFF_QA + CB, &tm_q, 64, (int)(pr.kh * g), ra, bar(Q_FULL));
-        if (pr.b.valid) {
-          const int rb = (int)(pr.b.r0 + pr.b.mt * TQ);
-          tma_load_3d(sbase + OFF_QB, &tm_q, 0, (int)(pr.kh * g), rb, bar(Q_FULL));
-          tma_load_3d(sbase + OFF_QB + CB, &tm_q, 64, (int)(pr.kh * g), rb, bar(Q_FULL));
+  if (warp == 2) {
+    // ============ Q producer, lane x = Q tile (stream) x: the tile of the stream's next item
+    // loads as soon as the last QK of its current item has read Q (K / V run ahead independently)
+    IL_REGS_DEC();
+    if (lane < 2) {
+      // Q rows live in HBM (the whole batch's Q exceeds L2): the stream's NEXT Q tile is
+      // prefetched into L2 when the current one is loaded, so the load at the item boundary hits L2
+      const uint32_t x = lane, qbytes = 2 * 128 * g * TQ;
+      auto seek = [&](uint32_t& w, Tile& T) {
+        for (; w < n_items; w += gridDim.x) {
+          T = decode_tile(c, cu_q, prefix_len, 2 * (w / Hkv) + x, TQ, phase, NC);
+          if (T.valid) break;
         }
+      };
+      uint32_t w = blockIdx.x, ix = 0;
+      Tile T;
+      seek(w, T);
+      while (w < n_items) {
+        uint32_t wn = w + gridDim.x;
+        Tile Tn;
+        seek(wn, Tn);
+        if (ix >= 1) mbar_wait(bar(Q_FREE + x), (ix - 1) & 1);
+        mbar_expect_tx(bar(Q_FULL + x), qbytes);
+        const int row = (int)(T.r0 + T.mt * TQ), hq = (int)((w % Hkv) * g);
+        tma_load_3d(sbase + OFF_QA + x * QTILE, &tm_q, 0, hq, row, bar(Q_FULL + x));
+        tma_load_3d(sbase + OFF_QA + x * QTILE + CB, &tm_q, 64, hq, row, bar(Q_FULL + x));
+        if (IL_Q_PREFETCH && wn < n_items) {
+          const int rown = (int)(Tn.r0 + Tn.mt * TQ), hqn = (int)((wn % Hkv) * g);
+          tma_prefetch_3d(&tm_q, 0, hqn, rown);
+          tma_prefetch_3d(&tm_q, 64, hqn, rown);
+        }
+        ++ix;
+        w = wn;
+        T = Tn;
       }
-      __syncwarp();
     }
-  }
-  if (warp == 0 || warp == 3) {
+    __syncwarp();
+  } else if (warp == 0 || warp == 3) {
     // ============ TMA producers: warp 0 = K tiles, warp 3 = V tiles ============
     IL_REGS_DEC();
     const bool is_k = warp == 0;
@@ -448,149 +553,105 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t nst = is_k ? NSTK : NSTV;
     const uint32_t full0 = is_k ? K_FULL : V_FULL, free0 = is_k ? K_FREE : V_FREE;
     const uint32_t ring = sbase + (is_k ? OFF_K : OFF_V);
-    uint32_t lc = 0, it = 0;
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      if (IL_Q_WARP == 0 && is_k && lane == 0) {        // (alternative: Q issued by the K producer)
-        if (it >= 1) mbar_wait(bar(Q_FREE), (it - 1) & 1);
-        const uint32_t qbytes = 2 * 128 * g * TQ;
-        mbar_expect_tx(bar(Q_FULL), pr.b.valid ? 2 * qbytes : qbytes);
-        const int ra = (int)(pr.a.r0 + pr.a.mt * TQ);
-        tma_load_3d(sbase + OFF_QA, &tm_q, 0, (int)(pr.kh * g), ra, bar(Q_FULL));
-        tma_load_3d(sbase + OFF_QA + CB, &tm_q, 64, (int)(pr.kh * g), ra, bar(Q_FULL));
-        if (pr.b.valid) {
-          const int rb = (int)(pr.b.r0 + pr.b.mt * TQ);
-          tma_load_3d(sbase + OFF_QB, &tm_q, 0, (int)(pr.kh * g), rb, bar(Q_FULL));
-          tma_load_3d(sbase + OFF_QB + CB, &tm_q, 64, (int)(pr.kh * g), rb, bar(Q_FULL));
-        }
+    LoadSeq seq;
+    seq.init(&c, cu_q, prefix_len, Hkv, TQ, phase, NC, n_items, streams);
+    Load L;
+    for (uint32_t lc = 0; seq.next(L); ++lc) {
+      const int32_t* bt = block_table + (size_t)L.req * c.max_blocks;
+      const uint32_t blk = L.kvt * 8 + (lane & 7);
+      const int32_t page = blk < L.nblk ? __ldg(bt + blk) : __ldg(bt);
+      const uint32_t s = lc % nst, u = lc / nst;
+      if (lane == 0) {
+        if (lc >= nst) mbar_wait(bar(free0 + s), (u - 1) & 1);
+        IL_TRACE(is_k ? 0 : 1, lc & 4095);
+        mbar_expect_tx(bar(full0 + s), KVTILE);
       }
-      for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
-        uint32_t n, req, tgt;
-        load_info(pr, l, n, req, tgt);
-        const uint32_t nblk = req == pr.a.i ? pr.a.nblk : pr.b.nblk;
-        const int32_t* bt = block_table + (size_t)req * c.max_blocks;
-        const uint32_t blk = (pr.a.kv0 + n) * 8 + (lane & 7);
-        const int32_t page = blk < nblk ? __ldg(bt + blk) : __ldg(bt);
-        const uint32_t s = lc % nst, u = lc / nst;
-        if (lane == 0) {
-          if (lc >= nst) mbar_wait(bar(free0 + s), (u - 1) & 1);
-          IL_TRACE(is_k ? 0 : 1, lc & 4095);
-#ifdef IL_DBG_NOKVTMA
-          if (lc >= nst) mbar_arrive(bar(full0 + s)); else   // timing experiment only: stale K/V
-#endif
-          mbar_expect_tx(bar(full0 + s), KVTILE);
-        }
-        __syncwarp();
-#ifdef IL_DBG_NOKVTMA
-        if (lc >= nst) continue;
-#endif
-        if (lane < 16) {                                 // lane = (page, column half)
-          const uint32_t p = lane & 7, h = lane >> 3;
-          const int row = (int)(((uint32_t)page * Hkv + pr.kh) * BS);
-          tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
-        }
+      __syncwarp();
+      if (lane < 16) {                                 // lane = (page, column half)
+        const uint32_t p = lane & 7, h = lane >> 3;
+        const int row = (int)(((uint32_t)page * Hkv + L.kh) * BS);
+        tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer: warp-uniform loop, one elected lane issues ==============
-    // Per Q tile x the 64-key tiles n = 0, 1, 2, ... alternate TMEM buffers n & 1; QK of tile
-    // n+2 reuses the buffer of n, so it is issued right after PV(n) (tcgen05 ops from one
-    // thread execute in order).  The two Q tiles' chains interleave on the tensor pipe.
+    // Per Q tile x: S_x = Q_x K^T, then (after the softmax) O_x += P_x V.  S_x is single
+    // buffered, so PV of a tile is issued right before the next QK of the same Q tile
+    // (tcgen05 ops from one thread execute in order); the two Q tiles' chains interleave on
+    // the tensor pipe.
     IL_REGS_DEC();
-    const uint64_t dqa = sdesc(sbase + OFF_QA, 16, 1024), dqb = sdesc(sbase + OFF_QB, 16, 1024);
+    const uint64_t dq0 = sdesc(sbase + OFF_QA, 16, 1024);
     const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024), dv0 = sdesc(sbase + OFF_V, KCB, 1024);
-    uint32_t lc = 0, it = 0, cnt0 = 0, cnt1 = 0;
+    uint32_t cnt[2] = {0, 0};
     uint32_t vus = 0;                                 // 2-bit PV-user counters per load (lc % 8)
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      uint32_t last0 = 0, last1 = 0;
-      for (uint32_t l = 0; l < pr.nload; ++l) {
-        uint32_t n_, r_, t_;
-        load_info(pr, l, n_, r_, t_);
-        if (t_ & 1u) last0 = l;
-        if (t_ & 2u) last1 = l;
-      }
-      if (lane == 0) IL_TRACE(12, it & 4095);          // item decoded
-      mbar_wait(bar(Q_FULL), it & 1);
-      if (lane == 0) IL_TRACE(13, it & 4095);          // Q landed
-#ifdef IL_ATTN_TRACE
-      if (blockIdx.x == 0 && phase == IL_TRACE_PHASE && it < 1024 && lane == 0) {
-        g_trace_item[it][0] = lc; g_trace_item[it][1] = pr.nload; g_trace_item[it][2] = pr.nsh;
-        g_trace_item[it][3] = pr.a.n_kv | (pr.b.n_kv << 16);
-      }
-#endif
+    // pending PV per Q tile: flag, load counter, tile count, last tile of its item
+    uint32_t pn[2] = {0, 0}, pl[2] = {0, 0}, pc[2] = {0, 0}, pf[2] = {0, 0}, pix[2] = {0, 0};
+    bool fst[2] = {true, true}, ordy[2] = {true, true};
+    auto pv_one = [&](const uint32_t x) {
+      const uint32_t vs = pl[x] % NSTV;
+      if (!ordy[x]) { mbar_wait(bar(O_FREE + x), (pix[x] - 1) & 1); ordy[x] = true; }   // epilogue of the previous item
+      mbar_wait(bar((IL_P_SPLIT ? P_HALF : P_FULL) + x), pc[x] & 1);
+      mbar_wait(bar(V_FULL + vs), (pl[x] / NSTV) & 1);
+      if (lane == 0) IL_TRACE(3, (2 * pl[x] + x) & 4095);
       tc_fence_after();
-      // pending PV per Q tile (S is single-buffered: PV(n) must precede QK(n+1)):
-      // (load counter, tile count)
-      // (+ item-local load index, so the last PV of a tile commits that tile's O_FULL: the two
-      // tiles' epilogues and the next item's first PVs then proceed per tile)
-      uint32_t q0n = 0, q0l = 0, q0c = 0, q0i = 0, q1n = 0, q1l = 0, q1c = 0, q1i = 0;
-      bool first0 = phase != 1, first1 = phase != 1;   // phase 1 accumulates onto the partial
-      bool o_ready0 = it == 0, o_ready1 = it == 0;
-      auto pv_one = [&](const uint32_t x) {
-        const uint32_t pl = x ? q1l : q0l, pc = x ? q1c : q0c, vs = pl % NSTV;
-        if (!(x ? o_ready1 : o_ready0)) {                // the previous item's epilogue of tile x is done
-          mbar_wait(bar(O_FREE + x), (it - 1) & 1);
-          if (x) o_ready1 = true; else o_ready0 = true;
-        }
-        mbar_wait(bar((IL_P_SPLIT ? P_HALF : P_FULL) + x), pc & 1);
-        mbar_wait(bar(V_FULL + vs), (pl / NSTV) & 1);
-        if (lane == 0) IL_TRACE(3, (2 * pl + x) & 4095);
-        tc_fence_after();
-        const uint64_t dv = dv0 + (uint64_t)((vs * KVTILE) >> 4);
-        const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x;
-        const bool fst = x ? first1 : first0;
-        // K = 128 keys in 8 steps of 16 (V tile rows; 16 keys = 2 swizzle atoms = 2048 B)
+      const uint64_t dv = dv0 + (uint64_t)((vs * KVTILE) >> 4);
+      const uint32_t o_tmem = tmem + 256 + 128 * x, p_tmem = tmem + 128 * x;
+      // K = 128 keys in 8 steps of 16 (V tile rows; 16 keys = 2 swizzle atoms = 2048 B)
 #pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-          // IL_P_SPLIT: keys 0-63 of P are released first; their MMAs run while the softmax
-          // computes keys 64-127
-          if (IL_P_SPLIT && k == 4) { mbar_wait(bar(P_FULL + x), pc & 1); tc_fence_after(); }
-          mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst && k == 0) ? 0u : 1u);
+      for (uint32_t k = 0; k < 8; ++k) {
+        // IL_P_SPLIT: keys 0-63 of P are released first; their MMAs run while the softmax
+        // computes keys 64-127
+        if (IL_P_SPLIT && k == 4) { mbar_wait(bar(P_FULL + x), pc[x] & 1); tc_fence_after(); }
+        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst[x] && k == 0) ? 0u : 1u);
+      }
+      fst[x] = false;
+      commit_w(bar(PV_DONE + x));
+      if (pf[x]) commit_w(bar(O_FULL + x));          // the item's last PV of this tile: epilogue may start
+      const uint32_t sh = 2 * (pl[x] & 7);
+      vus -= 1u << sh;
+      if (((vus >> sh) & 3u) == 0) commit_w(bar(V_FREE + vs));
+      pn[x] = 0;
+    };
+    LoadSeq seq;
+    seq.init(&c, cu_q, prefix_len, Hkv, TQ, phase, NC, n_items, streams);
+    Load L;
+    for (uint32_t lc = 0; seq.next(L); ++lc) {
+#pragma unroll
+      for (uint32_t x = 0; x < 2; ++x)                 // a tile whose item has no more loads here drains its PV
+        if (!((L.tgt >> x) & 1u) && pn[x] && pf[x] && (!streams || seq.done(x))) pv_one(x);
+      const uint32_t ks = lc % NSTK;
+      mbar_wait(bar(K_FULL + ks), (lc / NSTK) & 1);
+      if (lane == 0) IL_TRACE(2, lc & 4095);
+      tc_fence_after();
+      const uint32_t sh = 2 * (lc & 7);
+      vus = (vus & ~(3u << sh)) | ((uint32_t)__popc(L.tgt) << sh);
+      const uint64_t dk = dk0 + (uint64_t)((ks * KVTILE) >> 4);
+#pragma unroll
+      for (uint32_t x = 0; x < 2; ++x) {
+        if (!((L.tgt >> x) & 1u)) continue;
+        if (pn[x]) pv_one(x);                          // frees the S/P columns this QK overwrites
+        if ((L.first >> x) & 1u) {                     // a new item of this Q tile
+          mbar_wait(bar(Q_FULL + x), L.ix[x] & 1);
+          if (lane == 0 && x == 0) IL_TRACE(13, L.ix[0] & 4095);
+          tc_fence_after();
+          fst[x] = phase != 1;                         // phase 1 accumulates onto the partial
+          ordy[x] = L.ix[x] == 0;
+          pix[x] = L.ix[x];
         }
-        if (x) first1 = false; else first0 = false;
-        commit_w(bar(PV_DONE + x));
-        if ((x ? q1i : q0i) == (x ? last1 : last0)) commit_w(bar(O_FULL + x));
-        const uint32_t sh = 2 * (pl & 7);
-        vus -= 1u << sh;
-        if (((vus >> sh) & 3u) == 0) commit_w(bar(V_FREE + vs));
-        if (x) q1n = 0; else q0n = 0;
-      };
-      auto qk = [&](const uint32_t x, const uint64_t dk, const uint32_t li) {
-        if (x ? q1n : q0n) pv_one(x);                 // frees the S/P columns this QK overwrites
-        const uint32_t sc = x ? cnt1++ : cnt0++;
-        const uint32_t s_tmem = tmem + 128 * x;
-        const uint64_t dq = x ? dqb : dqa;
+        const uint64_t dq = dq0 + (uint64_t)((x * QTILE) >> 4);
 #pragma unroll
         for (uint32_t k = 0; k < 8; ++k)
-          mma_ss_w<IDESC_QK>(s_tmem, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
+          mma_ss_w<IDESC_QK>(tmem + 128 * x, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
                              dk + (uint64_t)(((k >> 2) * KCB + (k & 3) * 32) >> 4), k ? 1u : 0u);
         commit_w(bar(S_FULL + x));
-        if (x) { q1l = lc; q1c = sc; q1i = li; q1n = 1; } else { q0l = lc; q0c = sc; q0i = li; q0n = 1; }
-      };
-      for (uint32_t l = 0; l < pr.nload; ++l, ++lc) {
-        uint32_t n, req, tgt;
-        load_info(pr, l, n, req, tgt);
-        if (last0 < l && q0n) pv_one(0);              // a Q tile whose loads ended drains its PV
-        if (last1 < l && q1n) pv_one(1);
-        const uint32_t ks = lc % NSTK;
-        mbar_wait(bar(K_FULL + ks), (lc / NSTK) & 1);
-        if (lane == 0) IL_TRACE(2, lc & 4095);
-        tc_fence_after();
-        const uint32_t sh = 2 * (lc & 7);
-        vus = (vus & ~(3u << sh)) | (((tgt == 3) ? 2u : 1u) << sh);
-        const uint64_t dk = dk0 + (uint64_t)((ks * KVTILE) >> 4);
-        if (tgt & 1u) qk(0, dk, l);
-        if (tgt & 2u) qk(1, dk, l);
-        commit_w(bar(K_FREE + ks));
-        if (l + 1 == pr.nload) commit_w(bar(Q_FREE));
+        pn[x] = 1; pl[x] = lc; pc[x] = cnt[x]++; pf[x] = (L.last >> x) & 1u;
+        if (pf[x]) commit_w(bar(Q_FREE + x));          // the item's last QK of this tile has read Q
       }
-      if (pr.nload == 0) commit_w(bar(Q_FREE));        // (not reached: every item has a KV tile)
-      while (q0n) pv_one(0);
-      while (q1n) pv_one(1);
-      if (!pr.b.valid) commit_w(bar(O_FULL + 1));     // (tile A always has a KV tile)
-      if (lane == 0) IL_TRACE(14, it & 4095);          // last PV issued
+      commit_w(bar(K_FREE + ks));
     }
+#pragma unroll
+    for (uint32_t x = 0; x < 2; ++x)
+      if (pn[x]) pv_one(x);
   } else if (warp >= 4) {
     // ====== softmax + epilogue, one warpgroup per Q tile: thread = row r of tile xo ======
     IL_REGS_INC();
@@ -598,15 +659,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_addr = (32 * q4) << 16;
     const uint32_t s_tmem = tmem + lane_addr + 128 * xo, o_tmem = tmem + lane_addr + 256 + 128 * xo;
     uint32_t it = 0, cnt = 0;
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const Pair pr = decode_pair(c, cu_q, prefix_len, w, Hkv, TQ, phase, NC);
-      const Tile& T = xo ? pr.b : pr.a;
+    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Tile T = decode_tile(c, cu_q, prefix_len, 2 * (w / Hkv) + xo, TQ, phase, NC);
+      if (!T.valid) continue;                          // (uniform over the warpgroup)
+      const uint32_t kh = w % Hkv;
       const uint32_t t = r / g, hh = r % g;
       const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
       const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
-      const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + pr.kh * g + hh;
+      const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + kh * g + hh;
       float m_used = -INFINITY, l = 0.f;
-      if (phase == 1 && T.valid) {
+      if (phase == 1) {
         // continue phase 2's partial (m + log2 l, O / l) of these rows: state (m + log2 l, 1, O / l).
         // Warp-uniform (tcgen05.st is .aligned); padding rows store zeros.
         if (valid) { m_used = c.attn_ml[orow]; l = 1.f; }
@@ -631,10 +693,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tmem_wait_st();
       }
-      for (uint32_t ld = 0; ld < pr.nload; ++ld) {
-        uint32_t n, req_, tgt;
-        load_info(pr, ld, n, req_, tgt);
-        if (!(tgt & (1u << xo))) continue;
+      for (uint32_t n = 0; n < T.n_kv; ++n) {        // this tile's KV tiles in load order
         mbar_wait(bar(S_FULL + xo), cnt & 1);
         if (r == 0) IL_TRACE(4 + 2 * xo, cnt & 4095);
         tc_fence_after();
@@ -644,9 +703,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int q = 0; q < 4; ++q) tmem_ld32(s_tmem + 32 * q, *reinterpret_cast<float(*)[32]>(&a[32 * q]));
         tmem_wait_ld();
         if (r == 0 && xo == 0) IL_TRACE(8, cnt & 4095);
-        if (phase == 2 && key0 + BN - 1 > pos_q) {
+        // causal mask: keys key0 + j with j >= nv are in this row's future.  Per 32-key chunk: all
+        // valid (no work), all masked (constant), or the one boundary chunk (per-element select)
+        // causal mask: keys key0 + j with j >= nv are in this row's future; 32-key chunks valid
+        // for the whole warp need no select (warp-uniform branches)
+        const int nv = (int)pos_q - (int)key0 + 1;
+        if (phase == 2 && __any_sync(~0u, nv < (int)BN)) {
 #pragma unroll
-          for (int j = 0; j < 128; ++j) if (key0 + j > pos_q) a[j] = -INFINITY;
+          for (int q = 0; q < 4; ++q) {
+            if (__all_sync(~0u, 32 * q + 32 <= nv)) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[32 * q + j] = 32 * q + j < nv ? a[32 * q + j] : -INFINITY;
+          }
         }
         float mxa[8];
 #pragma unroll
@@ -723,7 +791,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // epilogue: O / l -> bf16 row of `out`, natural-log LSE (or the phase-2 partial)
       mbar_wait(bar(O_FULL + xo), it & 1);
       tc_fence_after();
-      if (T.valid) {
+      {
         const float inv = 1.f / l;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -751,6 +819,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       if (r == 0 && xo == 0) IL_TRACE(15, it & 4095);  // epilogue done
       mbar_arrive(bar(O_FREE + xo));
+      ++it;
     }
   }
   tc_fence_before();

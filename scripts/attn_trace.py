@@ -36,6 +36,8 @@ def main():
     lib = _lib.load()
     lib.il_debug_trace.argtypes = [C.c_void_p]
     _lib.check(lib.il_debug_trace(raw.ctypes.data_as(C.c_void_p)), "trace")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    np.save(os.path.join(ROOT, "gpurun_out", f"trace_{os.environ.get('IL_LIB_VARIANT', 'trace')}.npy"), raw)
     tr = raw[:16 * 4096].reshape(16, 4096).astype(np.int64)
     items = raw[16 * 4096:16 * 4096 + 2048].view(np.uint32).reshape(1024, 4)
     t0 = tr[2][0]
