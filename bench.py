@@ -222,6 +222,11 @@ def run_ours(args, rank, world, local_rank):
     clocks = ClockSampler(local_rank)
     t_wall = time.perf_counter()
     launches0 = pl.launches()
+    prof = None
+    if os.environ.get("IL_BENCH_PROFILE"):             # diagnostics only: kernel timeline of the timed loop
+        from torch.profiler import ProfilerActivity, profile
+        prof = profile(activities=[ProfilerActivity.CUDA])
+        prof.__enter__()
     with torch.cuda.stream(stream):
         for j in range(2 * K):
             flush.zero_()
@@ -254,6 +259,15 @@ def run_ours(args, rank, world, local_rank):
                 d2h = 4 * B * cfg.k + 4 * B + 16 * B
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall
+    if prof is not None:
+        prof.__exit__(None, None, None)
+        evs_p = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+        t0p, prev = evs_p[0].time_range.start, None
+        for e in evs_p[-int(os.environ.get("IL_BENCH_PROFILE_N", "90")):]:
+            gap = (e.time_range.start - prev) if prev else 0
+            print(f"{e.time_range.start - t0p:10.1f} us dur {e.time_range.elapsed_us():8.1f} gap {gap:7.1f} {e.name[:60]}",
+                  file=sys.stderr)
+            prev = e.time_range.end
     clk = clocks.stop()
     launches = pl.launches() - launches0
     if graphs is not None:                             # replays do not pass through the host counter

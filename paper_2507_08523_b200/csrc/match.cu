@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t s_hist[EV_BINS];
   __shared__ uint64_t s_red;
+  __shared__ uint32_t s_wsum[EV_THREADS / 32];
   DevScalars* sc = c.sc;
   const uint32_t m = sc->evict_m;
   const uint32_t epoch = (uint32_t)b_cur, C = c.cfg.kv_pages;
@@ -170,15 +171,40 @@ __global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
     for (uint32_t x = threadIdx.x; x < EV_BINS; x += blockDim.x)
       if (s_hist[x]) atomicAdd(&ghist[x], s_hist[x]);
     grid.sync();
-    // every CTA scans the global histogram identically (2048 bins, cheap)
-    if (threadIdx.x == 0) {
-      uint32_t acc = 0, bin = 0;
-      for (bin = 0; bin < EV_BINS; ++bin) {
-        const uint32_t h = ghist[bin];
-        if (acc + h >= remaining) break;
-        acc += h;
+    // every CTA finds the bin holding the remaining-th smallest key identically: a block-wide
+    // prefix sum over the 2048 bins (4 per thread; L1 bypassed: other CTAs wrote them)
+    {
+      constexpr uint32_t PER = EV_BINS / EV_THREADS;
+      uint32_t v[PER], sum = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < PER; ++k) { v[k] = __ldcg(&ghist[threadIdx.x * PER + k]); sum += v[k]; }
+      const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
       }
-      s_red = ((uint64_t)bin << 32) | (remaining - acc);
+      if (lane == 31) s_wsum[wid] = inc;
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t t = lane < EV_THREADS / 32 ? s_wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(~0u, t, o);
+          if (lane >= (uint32_t)o) t += y;
+        }
+        if (lane < EV_THREADS / 32) s_wsum[lane] = t;      // inclusive warp-total scan
+      }
+      __syncthreads();
+      uint32_t acc = inc - sum + (wid ? s_wsum[wid - 1] : 0u);   // exclusive prefix of this thread's bins
+      if (acc < remaining && remaining <= acc + sum) {
+#pragma unroll
+        for (uint32_t k = 0; k < PER; ++k) {
+          if (acc + v[k] >= remaining) { s_red = ((uint64_t)(threadIdx.x * PER + k) << 32) | (remaining - acc); break; }
+          acc += v[k];
+        }
+      }
     }
     __syncthreads();
     const uint32_t bin = (uint32_t)(s_red >> 32);
@@ -189,6 +215,8 @@ __global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
       for (uint32_t x = threadIdx.x; x < EV_BINS; x += blockDim.x) c.hist[((pass + 1) & 1) * EV_BINS + x] = 0;
     grid.sync();
   }
+  // both histogram buffers are dead now (every CTA read the last one before the pass's sync)
+  for (uint32_t x = gtid; x < 2 * EV_BINS; x += gstride) c.hist[x] = 0;
   // prefix is now the exact m-th smallest key; evict every candidate with key <= prefix
   const uint64_t kstar = prefix;
   uint32_t ev = 0;
@@ -210,8 +238,6 @@ __global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
   if ((threadIdx.x & 31) == 0 && ev) atomicSub(&sc->resident, ev);
   grid.sync();
   if (gtid == 0) {
-    c.hist[0] = 0;                                      // leave both buffers clean
-    for (uint32_t x = 0; x < 2 * EV_BINS; ++x) c.hist[x] = 0;
     if (sc->evicted != m) latch(sc, IL_ERR_INTERNAL);
   }
 }
@@ -228,6 +254,8 @@ __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uin
   int32_t* bt = block_table + (size_t)i * c.max_blocks;
   for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
 }
+// (a kernel rather than a memset node: keeps the captured match graph all-kernel)
+__global__ void k_match_begin(Ctx c) { c.sc->pinned = 0; }
 __global__ void k_alloc_commit(Ctx c) {
   DevScalars* sc = c.sc;
   if (sc->status != IL_ERR_CAPACITY) sc->n_free -= sc->need_total;
@@ -244,7 +272,7 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)s;
   const uint64_t b_cur = c->batch + 1;
-  IL_CUDA(cudaMemsetAsync(&c->sc->pinned, 0, 4, st));
+  k_match_begin<<<1, 1, 0, st>>>(*c);
   k_instr_probe<<<1, 256, 0, st>>>(*c);
   if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
   k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q, b_cur);
@@ -263,7 +291,7 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
   k_alloc_commit<<<1, 1, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_prefix_match");
-  c->launches += B ? 6 : 4;
+  c->launches += B ? 7 : 5;
   c->prompt_tok = prompt_tok;
   c->prompt_len = prompt_len;
   c->block_hash = block_hash;

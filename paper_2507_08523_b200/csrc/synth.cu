@@ -1,8 +1,9 @@
 // synth.cu — il_synth_qkv (bench / test helper, not the method): bf16 Q, K, V of suffix rows
 // from the counter-based generator of DESIGN.md Z28:
 //   row key r = mix(mix(seed_t ^ token) ^ position)                     (64-bit, once per row)
-//   v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), e = head * 256 + dim   (32-bit, per element)
-//   x = (int(v >> 8) - 2^23) / 2^23 * scale, rounded to bf16 (RNE),
+//   v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), e = head * 128 + dim / 2   (one per dim pair)
+//   u = low 16 bits of v (even dim) / high 16 bits (odd dim), f = 1 + u / 2^16 (built from bits)
+//   x = (f - 1.5) * (2 * scale) in fp32 (no contraction), rounded to bf16 (RNE),
 // seed_t = mix((seed << 8) ^ salt), salt = 'Q' / 'K' / 'V'.
 #include <cuda_bf16.h>
 
@@ -14,9 +15,15 @@ namespace il {
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; return h ^ (h >> 16);
 }
-__device__ __forceinline__ float synth_val(uint64_t row_key, uint32_t e, float mul) {
+// the two elements (even dim, odd dim) of one dim pair
+__device__ __forceinline__ uint32_t synth_pair(uint64_t row_key, uint32_t e, float mul) {
   const uint32_t v = fmix32(((uint32_t)row_key ^ (e * 0x9E3779B9u)) + (uint32_t)(row_key >> 32));
-  return (float)((int32_t)(v >> 8) - (1 << 23)) * mul;
+  const float fa = __uint_as_float(0x3F800000u | ((v & 0xFFFFu) << 7));
+  const float fb = __uint_as_float(0x3F800000u | ((v >> 16) << 7));
+  const float a = __fmul_rn(__fsub_rn(fa, 1.5f), mul), b = __fmul_rn(__fsub_rn(fb, 1.5f), mul);
+  uint32_t w;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w) : "f"(b), "f"(a));   // low half = a (RNE)
+  return w;
 }
 
 // One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
@@ -51,10 +58,7 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
       else { key = kv; mul = kvmul; hh = h - Hq - Hkv; dst = vn + ((size_t)r * Hkv + hh) * D + x0; }
       uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float a = synth_val(key, hh * 256 + x0 + 2 * j, mul), b = synth_val(key, hh * 256 + x0 + 2 * j + 1, mul);
-        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(b), "f"(a));   // low half = a (RNE)
-      }
+      for (int j = 0; j < 4; ++j) w[j] = synth_pair(key, hh * 128 + x0 / 2 + j, mul);
       *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
@@ -69,7 +73,7 @@ extern "C" il_status il_synth_qkv(il_ctx* c, uint32_t B, const uint32_t* prompt_
                                   il_bf16* k_new, il_bf16* v_new, il_stream s) {
   if (B == 0) return IL_OK;
   auto tseed = [&](uint64_t salt) { return mix64((seed << 8) ^ salt); };
-  const float unit = 1.0f / 8388608.0f;
+  const float unit = 2.0f;                             // x = (f - 1.5) * 2 * scale
   const uint32_t d = c->cfg.head_dim;
   if (d == 128)
     k_synth<128><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),

@@ -15,7 +15,8 @@ from workload import gen  # noqa: E402
 
 
 def main():
-    cfg, ds, pool, instr = bench.workload(3, 0, 1, 20000)
+    NB = int(os.environ.get('PROBE_BATCHES', '12'))
+    cfg, ds, pool, instr = bench.workload(3, 0, 1, (NB + 2) * 1024)
     c = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B, max_prompt_tokens=cfg.max_prompt_tokens,
                max_pool=cfg.M, max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16,
                max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv, head_dim=cfg.d,
@@ -24,13 +25,23 @@ def main():
     pl = Pipeline(c, "cuda", stream=s)
     with torch.cuda.stream(s):
         pl.load_pool(pool, instr)
-        plan = bench.plan_batches(cfg, 12, 0, 1)
+        plan = bench.plan_batches(cfg, NB, 0, 1)
         for st, b in plan[:-3]:
             pl.stage_batch(gen.make_batch(ds, st, b)); pl.step()
         torch.cuda.synchronize()
+        graphs = None
+        if "--graph" in sys.argv:                      # per-stage CUDA graphs, as bench.py replays them
+            pl.stage_batch(gen.make_batch(ds, *plan[-4])); pl.step()
+            graphs = pl.capture(cfg.B)
+            torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             for st, b in plan[-3:]:
-                pl.stage_batch(gen.make_batch(ds, st, b)); pl.step()
+                pl.stage_batch(gen.make_batch(ds, st, b))
+                if graphs is None:
+                    pl.step()
+                else:
+                    for n in pl.STAGES:
+                        graphs[n].replay()
             torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ev.sort(key=lambda e: e.time_range.start)
