@@ -10,25 +10,29 @@
 namespace il {
 
 // K7a: suffix row r of request i at absolute position p goes to page block_table[i][p/16],
-// slot p%16, for every kv head: pages are [C][Hkv][16][d].
+// slot p%16, for every kv head: pages are [C][Hkv][16][d].  One warp per suffix row (the row's
+// owner and page are looked up once); lanes move 16-byte vectors of K and V.
 __global__ void __launch_bounds__(256) k_kv_append(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q,
                                                    const int32_t* __restrict__ prefix_len,
                                                    const int32_t* __restrict__ block_table,
                                                    const uint4* __restrict__ k_new, const uint4* __restrict__ v_new,
                                                    uint4* __restrict__ k_pages, uint4* __restrict__ v_pages) {
-  const uint32_t Hkv = c.cfg.n_kv_heads, d = c.cfg.head_dim;
-  const uint32_t vec_per_row = Hkv * d / 8;           // uint4 = 8 bf16
-  const uint32_t total = (uint32_t)cu_q[B];
-  const uint64_t n = (uint64_t)total * vec_per_row;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = (uint32_t)(e / vec_per_row), v = (uint32_t)(e % vec_per_row);
+  const uint32_t Hkv = c.cfg.n_kv_heads, vph = c.cfg.head_dim / 8;   // uint4 = 8 bf16
+  const uint32_t vec_per_row = Hkv * vph;
+  const uint32_t total = (uint32_t)cu_q[B], lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = gw; r < total; r += nw) {
     const uint32_t i = row_owner(cu_q, B, r);
     const uint32_t p = (uint32_t)prefix_len[i] + r - (uint32_t)cu_q[i];
     const uint32_t page = (uint32_t)block_table[(size_t)i * c.max_blocks + p / BS];
-    const uint32_t h = v / (d / 8), x = v % (d / 8);
-    const size_t dst = (((size_t)page * Hkv + h) * BS + (p % BS)) * (d / 8) + x;
-    k_pages[dst] = k_new[e];
-    v_pages[dst] = v_new[e];
+    const size_t src0 = (size_t)r * vec_per_row;
+    for (uint32_t v = lane; v < vec_per_row; v += 32) {
+      const uint32_t h = v / vph, x = v % vph;
+      const size_t dst = (((size_t)page * Hkv + h) * BS + (p % BS)) * vph + x;
+      const uint4 kk = k_new[src0 + v], vv = v_new[src0 + v];
+      k_pages[dst] = kk;
+      v_pages[dst] = vv;
+    }
   }
 }
 

@@ -1,9 +1,9 @@
 // synth.cu — il_synth_qkv (bench / test helper, not the method): bf16 Q, K, V of suffix rows
 // from the counter-based generator of DESIGN.md Z28:
 //   row key r = mix(mix(seed_t ^ token) ^ position)                     (64-bit, once per row)
-//   v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), e = head * 128 + dim / 2   (one per dim pair)
-//   u = low 16 bits of v (even dim) / high 16 bits (odd dim), f = 1 + u / 2^16 (built from bits)
-//   x = (f - 1.5) * (2 * scale) in fp32 (no contraction), rounded to bf16 (RNE),
+//   v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)), e = head * 64 + dim / 4  (one per 4 dims)
+//   u = byte (dim % 4) of v, f = 1 + u / 256 (built from bits), x = (f - 1.5) * (2 * scale)
+//   in fp32 (no contraction) -- exact in bf16: (u - 128) / 128 * scale,
 // seed_t = mix((seed << 8) ^ salt), salt = 'Q' / 'K' / 'V'.
 #include <cuda_bf16.h>
 
@@ -15,15 +15,15 @@ namespace il {
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; return h ^ (h >> 16);
 }
-// the two elements (even dim, odd dim) of one dim pair
-__device__ __forceinline__ uint32_t synth_pair(uint64_t row_key, uint32_t e, float mul) {
+// the four elements (dims 4e .. 4e+3) of one mix, as two packed bf16 pairs
+__device__ __forceinline__ void synth_quad(uint64_t row_key, uint32_t e, float mul, uint32_t& w0, uint32_t& w1) {
   const uint32_t v = fmix32(((uint32_t)row_key ^ (e * 0x9E3779B9u)) + (uint32_t)(row_key >> 32));
-  const float fa = __uint_as_float(0x3F800000u | ((v & 0xFFFFu) << 7));
-  const float fb = __uint_as_float(0x3F800000u | ((v >> 16) << 7));
-  const float a = __fmul_rn(__fsub_rn(fa, 1.5f), mul), b = __fmul_rn(__fsub_rn(fb, 1.5f), mul);
-  uint32_t w;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w) : "f"(b), "f"(a));   // low half = a (RNE)
-  return w;
+  float x[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    x[j] = __fmul_rn(__fsub_rn(__uint_as_float(0x3F800000u | (((v >> (8 * j)) & 0xFFu) << 15)), 1.5f), mul);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w0) : "f"(x[1]), "f"(x[0]));   // low half = dim 4e
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w1) : "f"(x[3]), "f"(x[2]));
 }
 
 // One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
       else if (h < Hq + Hkv) { key = kk; mul = kvmul; hh = h - Hq; dst = kn + ((size_t)r * Hkv + hh) * D + x0; }
       else { key = kv; mul = kvmul; hh = h - Hq - Hkv; dst = vn + ((size_t)r * Hkv + hh) * D + x0; }
       uint32_t w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) w[j] = synth_pair(key, hh * 128 + x0 / 2 + j, mul);
+      synth_quad(key, hh * 64 + x0 / 4, mul, w[0], w[1]);
+      synth_quad(key, hh * 64 + x0 / 4 + 1, mul, w[2], w[3]);
       *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }

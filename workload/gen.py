@@ -248,9 +248,9 @@ def _fmix32(h: np.ndarray) -> np.ndarray:
 def synth_bf16_bits(seed: int, which: str, tokens: np.ndarray, positions: np.ndarray,
                     n_heads: int, d: int, scale: float = 1.0) -> np.ndarray:
     """[n][n_heads][d] uint16 bf16 bit patterns (Z28): per (token, position) a 64-bit
-    row key r = mix(mix(seed_t ^ token) ^ position); per dim pair (e = head * 128 + dim // 2)
-    v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)); u = low (even dim) / high (odd dim) 16 bits
-    of v; f = 1 + u / 2^16; x = (f - 1.5) * (2 * scale) in float32; RNE to bf16."""
+    row key r = mix(mix(seed_t ^ token) ^ position); per 4 dims (e = head * 64 + dim // 4)
+    v = fmix32((lo32(r) ^ e * 0x9E3779B9) + hi32(r)); u = byte dim % 4 of v; f = 1 + u / 256;
+    x = (f - 1.5) * (2 * scale) in float32 (= (u - 128) / 128 * scale, exact in bf16); RNE to bf16."""
     s = np.uint64(tensor_seed(seed, which))
     t = tokens.astype(np.uint64)[:, None, None]
     p = positions.astype(np.uint64)[:, None, None]
@@ -258,11 +258,11 @@ def synth_bf16_bits(seed: int, which: str, tokens: np.ndarray, positions: np.nda
     lo = (r & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     hi = (r >> np.uint64(32)).astype(np.uint32)
     dim = np.arange(d, dtype=np.uint32)
-    e = (np.arange(n_heads, dtype=np.uint32)[None, :, None] * np.uint32(128) + (dim // np.uint32(2))[None, None, :])
+    e = (np.arange(n_heads, dtype=np.uint32)[None, :, None] * np.uint32(64) + (dim // np.uint32(4))[None, None, :])
     with np.errstate(over="ignore"):
         v = _fmix32(((lo ^ (e * np.uint32(0x9E3779B9)).astype(np.uint32)) + hi).astype(np.uint32))
-    u = np.where((dim & np.uint32(1)).astype(bool)[None, None, :], v >> np.uint32(16), v & np.uint32(0xFFFF))
-    f = (np.uint32(0x3F800000) | (u.astype(np.uint32) << np.uint32(7))).view(np.float32)
+    u = (v >> (np.uint32(8) * (dim & np.uint32(3)))[None, None, :]) & np.uint32(0xFF)
+    f = (np.uint32(0x3F800000) | (u.astype(np.uint32) << np.uint32(15))).view(np.float32)
     x = (f - np.float32(1.5)) * np.float32(2.0 * scale)
     b = x.view(np.uint32).astype(np.uint64)
     rnd = ((b >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)
