@@ -26,6 +26,31 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {   // a ra
   const uint64_t l = a.num * b.den, r = b.num * a.den;                   // < 2^48: exact in u64
   return l > r || (l == r && a.idx < b.idx);
 }
+// k rounds of warp argmax over the lanes' sorted lists (get(q) = the lane's q-th best, n of
+// them); the winning lane pops its head.  `better` is a strict total order (index breaks score
+// ties), so the result does not depend on lane order.  Picks go to out[0..n) best first.
+template <class Get>
+__device__ __forceinline__ uint32_t warp_merge(Get get, uint32_t n, uint32_t k, uint32_t lane, Cand* out) {
+  uint32_t head = 0, npick = 0;
+  for (uint32_t r = 0; r < k; ++r) {
+    Cand w;
+    uint32_t wl = NONE32;
+    if (head < n) { w = get(head); wl = lane; } else { w.num = 0; w.den = 1; w.idx = NONE32; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      Cand o_;
+      o_.num = __shfl_xor_sync(~0u, w.num, o); o_.den = __shfl_xor_sync(~0u, w.den, o);
+      o_.idx = __shfl_xor_sync(~0u, w.idx, o);
+      const uint32_t ol = __shfl_xor_sync(~0u, wl, o);
+      if (ol != NONE32 && (wl == NONE32 || better(o_, w))) { w = o_; wl = ol; }
+    }
+    if (wl == NONE32) break;                             // (uniform: every lane holds the winner)
+    if (lane == 0) out[r] = w;
+    if (lane == wl) ++head;
+    ++npick;
+  }
+  return npick;
+}
 __device__ __forceinline__ uint32_t qslot(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 9); }
 
 __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
@@ -33,10 +58,12 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
                                                           const uint32_t* __restrict__ q_src,
                                                           uint32_t* __restrict__ topk) {
   __shared__ uint32_t s_key[QHASH], s_cnt[QHASH];
-  __shared__ Cand s_best[SIM_THREADS / 32];
+  __shared__ uint64_t s_lnum[MAXK][SIM_THREADS];
+  __shared__ uint32_t s_lden[MAXK][SIM_THREADS], s_lidx[MAXK][SIM_THREADS];
+  __shared__ Cand s_wl[SIM_THREADS / 32][MAXK];
+  __shared__ uint32_t s_wn[SIM_THREADS / 32];
   __shared__ uint32_t s_nq, s_nuq, s_win;
   __shared__ Cand s_sel[MAXK];
-  __shared__ uint32_t s_btid[SIM_THREADS / 32];
   const uint32_t i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t k = c.cfg.k;
   for (uint32_t x = tid; x < QHASH; x += SIM_THREADS) { s_key[x] = NONE32; s_cnt[x] = 0; }
@@ -71,7 +98,10 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
   const bool excl = (c.cfg.flags & IL_F_EXCLUDE_SELF) != 0;
   const uint32_t my_src = (excl && q_src) ? q_src[i] : NONE32;
 
+  // private sorted list, always MAXK long: padded with a sentinel every real candidate beats
   Cand top[MAXK];
+#pragma unroll
+  for (int q = 0; q < MAXK; ++q) { top[q].num = 0; top[q].den = 1; top[q].idx = NONE32; }
   uint32_t ntop = 0;
   for (uint32_t m = tid; m < c.n_demos; m += SIM_THREADS) {
     if (excl && c.src[m] == my_src) continue;
@@ -99,73 +129,51 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
       if (nq == 0 || nm == 0) { x.num = 0; x.den = 1; }                   // zero norm (Z5)
       else { x.num = (uint64_t)dot * dot; x.den = nm; }
     }
-    // insert into the private sorted list (k <= 8; m increases, so equal scores go after)
-    bool ins = ntop < k;
-    if (!ins) {
+    // insert into the private sorted list: position q takes x if x ranks before its old
+    // entry, else keeps it; entries below shift down one (static register indices only)
+    Cand prev = top[0];
+    bool bprev = better(x, prev);
+    if (bprev) top[0] = x;
 #pragma unroll
-      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == k - 1) ins = better(x, top[q]);
+    for (int q = 1; q < MAXK; ++q) {
+      const Cand cur = top[q];
+      const bool bq = better(x, cur);
+      if (bq) top[q] = bprev ? prev : x;
+      prev = cur;
+      bprev = bq;
     }
-    if (ins) {
-      uint32_t pos = ntop < k ? ntop : k - 1;
-#pragma unroll
-      for (int q = MAXK - 1; q > 0; --q) {
-        if ((uint32_t)q <= pos && better(x, top[q - 1])) { top[q] = top[q - 1]; pos = q - 1; }
-      }
-#pragma unroll
-      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == pos) top[q] = x;
-      if (ntop < k) ++ntop;
-    }
+    ntop = min(ntop + 1, (uint32_t)MAXK);
   }
-  // block merge: k rounds of argmax over every thread's current head
-  uint32_t head = 0;
-  for (uint32_t r = 0; r < k; ++r) {
-    Cand h;
-    bool have = head < ntop;
-    if (have) {
+  ntop = min(ntop, k);
+  // merge: every thread's sorted list goes to shared memory (static register indices), each
+  // warp merges its lanes' lists (k rounds of warp argmax; the winning lane pops its head), then
+  // warp 0 merges the 8 warp lists the same way (no block-wide rounds)
 #pragma unroll
-      for (int q = 0; q < MAXK; ++q) if ((uint32_t)q == head) h = top[q];
-    } else {
-      h.num = 0; h.den = 1; h.idx = NONE32;
-    }
-    // warp argmax (NONE32 idx = absent)
-    Cand w = h;
-    uint32_t wtid = have ? tid : NONE32;
-    for (int o = 16; o; o >>= 1) {
-      Cand o_;
-      o_.num = __shfl_xor_sync(~0u, w.num, o); o_.den = __shfl_xor_sync(~0u, w.den, o);
-      o_.idx = __shfl_xor_sync(~0u, w.idx, o);
-      const uint32_t ot = __shfl_xor_sync(~0u, wtid, o);
-      const bool take = (ot != NONE32) && (wtid == NONE32 || better(o_, w));
-      if (take) { w = o_; wtid = ot; }
-    }
-    if (lane == 0) { s_best[wid] = w; s_btid[wid] = wtid; }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t bt = NONE32;
-      Cand b;
-      for (uint32_t q = 0; q < SIM_THREADS / 32; ++q) {
-        if (s_btid[q] == NONE32) continue;
-        if (bt == NONE32 || better(s_best[q], b)) { b = s_best[q]; bt = s_btid[q]; }
-      }
-      s_win = bt;
-      if (bt != NONE32) s_sel[r] = b;
-      else latch(c.sc, IL_ERR_ARG);                       // fewer than k candidates
-    }
-    __syncthreads();
-    if (s_win == tid) ++head;
-    if (s_win == NONE32) return;
+  for (int q = 0; q < MAXK; ++q)
+    if ((uint32_t)q < ntop) { s_lnum[q][tid] = top[q].num; s_lden[q][tid] = (uint32_t)top[q].den; s_lidx[q][tid] = top[q].idx; }
+  __syncwarp();
+  const uint32_t nw = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
+                                 ntop, k, lane, s_wl[wid]);
+  if (lane == 0) s_wn[wid] = nw;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t wn = lane < SIM_THREADS / 32 ? s_wn[lane] : 0u;
+    const uint32_t n = warp_merge([&](uint32_t q) { return s_wl[lane][q]; }, wn, k, lane, s_sel);
+    if (lane == 0 && n < k) latch(c.sc, IL_ERR_ARG);     // fewer than k candidates
+    if (lane == 0) s_win = n;
   }
-  if (tid == 0) {
-    // emit ascending by similarity, ties by index ascending
-    Cand e[MAXK];
-    for (uint32_t r = 0; r < k; ++r) e[r] = s_sel[r];
-    for (uint32_t a = 1; a < k; ++a)
-      for (uint32_t b = a; b > 0; --b) {
-        const uint64_t l = e[b].num * e[b - 1].den, rr = e[b - 1].num * e[b].den;
-        const bool lt = l < rr || (l == rr && e[b].idx < e[b - 1].idx);
-        if (lt) { Cand t = e[b]; e[b] = e[b - 1]; e[b - 1] = t; }
-      }
-    for (uint32_t r = 0; r < k; ++r) topk[(size_t)i * k + r] = e[r].idx;
+  __syncthreads();
+  if (s_win < k) return;
+  if (tid < k) {
+    // emit ascending by similarity, ties by index ascending: position = rank
+    const Cand me = s_sel[tid];
+    uint32_t pos = 0;
+    for (uint32_t r = 0; r < k; ++r) {
+      const Cand o = s_sel[r];
+      const uint64_t l = o.num * me.den, rr = me.num * o.den;
+      pos += (l < rr || (l == rr && o.idx < me.idx)) ? 1u : 0u;
+    }
+    topk[(size_t)i * k + pos] = me.idx;
   }
 }
 
