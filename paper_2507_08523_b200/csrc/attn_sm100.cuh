@@ -75,11 +75,15 @@ constexpr int THREADS = 384;
 #define IL_SETMAXNREG 1
 #endif
 #ifndef IL_REG_PROD
-#define IL_REG_PROD 72
+#define IL_REG_PROD 56
 #endif
 #ifndef IL_REG_SM
-#define IL_REG_SM 216
+#define IL_REG_SM 224
 #endif
+// setmaxnreg.inc only completes when the CTA's pool (168 x 384 registers at launch) holds the
+// requested registers: 4 warps x IL_REG_PROD + 8 x IL_REG_SM must not exceed 12 x 168, or the
+// softmax warps wait forever
+static_assert(4 * IL_REG_PROD + 8 * IL_REG_SM <= 12 * 168, "setmaxnreg split exceeds the register pool");
 // producers / MMA issuer need few registers; the softmax warps hold a 128-column row
 #if IL_SETMAXNREG
 #define IL_REGS_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IL_REG_PROD))
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
                  const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                  float scale_log2, uint32_t g, uint32_t TQ, uint32_t phase, const __grid_constant__ CUtensorMap tm_q,
+                 const __grid_constant__ CUtensorMap tm_o,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -538,6 +543,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int rown = (int)(Tn.r0 + Tn.mt * TQ), hqn = (int)((wn % Hkv) * g);
           tma_prefetch_3d(&tm_q, 0, hqn, rown);
           tma_prefetch_3d(&tm_q, 64, hqn, rown);
+          if (phase == 1) {                             // the next item's phase-2 partial (O / l rows)
+            tma_prefetch_3d(&tm_o, 0, hqn, rown);
+            tma_prefetch_3d(&tm_o, 64, hqn, rown);
+          }
         }
         ++ix;
         w = wn;
@@ -659,18 +668,28 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_addr = (32 * q4) << 16;
     const uint32_t s_tmem = tmem + lane_addr + 128 * xo, o_tmem = tmem + lane_addr + 256 + 128 * xo;
     uint32_t it = 0, cnt = 0;
-    for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-      const Tile T = decode_tile(c, cu_q, prefix_len, 2 * (w / Hkv) + xo, TQ, phase, NC);
-      if (!T.valid) continue;                          // (uniform over the warpgroup)
+    const uint32_t t = r / g, hh = r % g;
+    // items are decoded one ahead (the decode's dependent loads stay off the item boundary)
+    auto seek = [&](uint32_t& w, Tile& T) {
+      for (; w < n_items; w += gridDim.x) {
+        T = decode_tile(c, cu_q, prefix_len, 2 * (w / Hkv) + xo, TQ, phase, NC);
+        if (T.valid) break;                            // (uniform over the warpgroup)
+      }
+    };
+    uint32_t w = blockIdx.x;
+    Tile T;
+    seek(w, T);
+    while (w < n_items) {
       const uint32_t kh = w % Hkv;
-      const uint32_t t = r / g, hh = r % g;
-      const bool valid = T.valid && (r < g * TQ) && (t < T.ntok);
-      const uint32_t pos_q = T.valid ? T.P + T.mt * TQ + min(t, T.ntok - 1) : 0;
+      const bool valid = (r < g * TQ) && (t < T.ntok);
+      const uint32_t pos_q = T.P + T.mt * TQ + min(t, T.ntok - 1);
       const size_t orow = (size_t)(T.r0 + T.mt * TQ + t) * Hq + kh * g + hh;
       float m_used = -INFINITY, l = 0.f;
       if (phase == 1) {
         // continue phase 2's partial (m + log2 l, O / l) of these rows: state (m + log2 l, 1, O / l).
         // Warp-uniform (tcgen05.st is .aligned); padding rows store zeros.
+        if (r == 0 && xo == 0) IL_TRACE(12, it & 4095);
+        // (the rows were prefetched into L2 by the Q producer one item ahead)
         if (valid) { m_used = c.attn_ml[orow]; l = 1.f; }
         const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
         uint4 raw[16];
@@ -692,6 +711,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_st32(o_tmem + 32 * q, ov);
         }
         tmem_wait_st();
+        if (r == 0 && xo == 0) IL_TRACE(14, it & 4095);
       }
       for (uint32_t n = 0; n < T.n_kv; ++n) {        // this tile's KV tiles in load order
         mbar_wait(bar(S_FULL + xo), cnt & 1);
@@ -788,6 +808,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive(bar(P_FULL + xo));
         ++cnt;
       }
+      uint32_t wn = w + gridDim.x;                     // decode the next item while the last PV runs
+      Tile Tn;
+      seek(wn, Tn);
       // epilogue: O / l -> bf16 row of `out`, natural-log LSE (or the phase-2 partial)
       mbar_wait(bar(O_FULL + xo), it & 1);
       tc_fence_after();
@@ -820,6 +843,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (r == 0 && xo == 0) IL_TRACE(15, it & 4095);  // epilogue done
       mbar_arrive(bar(O_FREE + xo));
       ++it;
+      w = wn;
+      T = Tn;
     }
   }
   tc_fence_before();
@@ -909,16 +934,16 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   const uint32_t Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads, g = Hq / Hkv, TQ = BM / g;
   auto enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return IL_ERR_CUDA; }
-  CUtensorMap tq, tk, tv;
-  {
+  CUtensorMap tq, to, tk, tv;
+  for (int which = 0; which < 2; ++which) {            // Q, and `out` (same geometry: L2 prefetch only)
     cuuint64_t dims[3] = {D, Hq, c->cfg.max_suffix_tokens};
     cuuint64_t strides[2] = {D * 2, (cuuint64_t)Hq * D * 2};
     cuuint32_t box[3] = {64, g, TQ};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)q, dims, strides, box, es,
+    CUresult r = enc(which ? &to : &tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, which ? (void*)out : (void*)q, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { set_error("tensor map (q) encode failed"); return IL_ERR_CUDA; }
+    if (r != CUDA_SUCCESS) { set_error("tensor map (q / out) encode failed"); return IL_ERR_CUDA; }
   }
   for (int which = 0; which < 2; ++which) {
     cuuint64_t dims[2] = {D, (cuuint64_t)c->cfg.kv_pages * Hkv * BS};
@@ -943,7 +968,7 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
     if (phase == 1 && !cascade) break;
     k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out,
-                                                          lse, scale * 1.4426950408889634f, g, TQ, phase, tq, tk, tv);
+                                                          lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");
   }
   c->launches += cascade ? (B > 1 ? 5 : 4) : 3;
