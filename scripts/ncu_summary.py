@@ -1,6 +1,6 @@
 """Summarise an `ncu --set full` report into a small JSON (committed under profiles/).
 
-    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep k_attn_sm100 profiles/attn_ncu_summary.json
+    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_summary.json profiles/attn_ncu_summary.json
 """
 import csv
 import io
@@ -27,17 +27,14 @@ SCALE = {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e
          "cycle/nsecond": 1e9, "cycle/usecond": 1e6}
 
 
-def main(rep, kernel, out):
+def summarise(rep):
+    """Every captured launch: name + the METRICS above (one dict per launch, capture order)."""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
-    res = {"source": f"{rep} (ncu --set full, kernel {kernel})", "launches": 0}
+    out = []
     for row in rows[2:]:
-        name = row[hdr.index("Kernel Name")]
-        if kernel not in name:
-            continue
-        res["launches"] += 1
-        res["kernel"] = name.split("(")[0]
+        res = {"kernel": row[hdr.index("Kernel Name")].split("(")[0]}
         for m, key in METRICS.items():
             cols = [j for j, h in enumerate(hdr) if h == m or h.endswith("." + m)]
             if not cols:
@@ -47,13 +44,31 @@ def main(rep, kernel, out):
                 v = float(row[i].replace(",", ""))
             except ValueError:
                 continue
-            v *= SCALE.get(units[i], 1.0)
-            res[key] = v
-        break
-    if "dram_read" in res and "dram_write" in res:
-        res["dram_bytes_per_launch"] = res["dram_read"] + res["dram_write"]
-    json.dump(res, open(out, "w"), indent=1)
-    print(json.dumps(res, indent=1))
+            res[key] = v * SCALE.get(units[i], 1.0)
+        if "dram_read" in res and "dram_write" in res:
+            res["dram_bytes"] = res["dram_read"] + res["dram_write"]
+        out.append(res)
+    return out
+
+
+def main(rep, out_all, out_attn):
+    """out_all: every launch of the capture; out_attn: the attention call (K/V append + both
+    k_attn_sm100 launches of one step) summed -- the traffic bench.py reports per call."""
+    launches = summarise(rep)
+    json.dump({"source": f"{rep} (ncu --set full --clock-control none, one steady-state step)",
+               "launches": launches}, open(out_all, "w"), indent=1)
+    parts = [x for x in launches if "k_attn_sm100" in x["kernel"] or "k_kv_append" in x["kernel"]]
+    attn = {"source": f"{rep} (ncu --set full; k_kv_append + k_attn_sm100 phase 2 + phase 1 of one step)",
+            "kernels": [x["kernel"] for x in parts],
+            "duration": sum(x.get("duration", 0.0) for x in parts),
+            "dram_read": sum(x.get("dram_read", 0.0) for x in parts),
+            "dram_write": sum(x.get("dram_write", 0.0) for x in parts)}
+    attn["dram_bytes_per_launch"] = attn["dram_read"] + attn["dram_write"]
+    attn["per_kernel"] = parts
+    json.dump(attn, open(out_attn, "w"), indent=1)
+    for x in launches:
+        print(f"{x['kernel'][:40]:40s} {x.get('duration', 0) * 1e6:9.1f} us  dram {x.get('dram_bytes', 0) / 1e6:9.1f} MB"
+              f"  issue {x.get('issue_active_pct', 0):5.1f}%  tensor {x.get('tensor_pipe_active_pct', 0):5.1f}%")
 
 
 if __name__ == "__main__":
