@@ -138,7 +138,8 @@ il_status il_pool_load(il_ctx* ctx, uint32_t n_demos,
  *                      target verbatim, rule 2 keeps DS_current, rule 3 modifies + reorders
  *   info[i]            see il_refine_info
  *   prompt_tok[i][..]  instruction ++ render(d_1..d_k) ++ query, render(m) = log ++ [TPL] ++
- *                      template ++ [SEP] (Z9); row stride = cfg.max_prompt_tokens
+ *                      template ++ [SEP] (Z9); row stride = cfg.max_prompt_tokens; the buffer
+ *                      must be 16-byte aligned (IL_ERR_ARG otherwise)
  *   prompt_len[i]
  * q_src[i] is the query's dataset row (only read with IL_F_EXCLUDE_SELF; may be NULL). */
 il_status il_refine_batch(il_ctx* ctx, uint32_t B,

@@ -15,7 +15,7 @@ namespace il {
 //   jaccard: |A n B| / |A u B|
 // Selection is by (score desc, index asc); the k winners are emitted (score asc, index asc).
 // ---------------------------------------------------------------------------------------
-constexpr int SIM_THREADS = 256;
+constexpr int SIM_THREADS = 128;               // 4 warps = 4 queries per CTA
 constexpr int QHASH = 512;
 
 struct Cand {
@@ -57,24 +57,28 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
                                                           const uint32_t* __restrict__ q_tok,
                                                           const uint32_t* __restrict__ q_src,
                                                           uint32_t* __restrict__ topk) {
-  __shared__ uint32_t s_key[QHASH], s_cnt[QHASH];
+  // one WARP per query (8 per CTA), no block-wide barriers: the query multiset goes into the
+  // warp's own shared-memory hash table, lanes score a strided subset of the pool
+  constexpr uint32_t NW = SIM_THREADS / 32;
+  __shared__ uint32_t s_key_all[NW][QHASH], s_cnt_all[NW][QHASH];
   __shared__ uint64_t s_lnum[MAXK][SIM_THREADS];
   __shared__ uint32_t s_lden[MAXK][SIM_THREADS], s_lidx[MAXK][SIM_THREADS];
-  __shared__ Cand s_wl[SIM_THREADS / 32][MAXK];
-  __shared__ uint32_t s_wn[SIM_THREADS / 32];
-  __shared__ uint32_t s_nq, s_nuq, s_win;
-  __shared__ Cand s_sel[MAXK];
-  const uint32_t i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ Cand s_sel_all[NW][MAXK];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t i = blockIdx.x * NW + wid;
+  if (i >= B) return;                                   // (warp-uniform)
+  uint32_t* s_key = s_key_all[wid];
+  uint32_t* s_cnt = s_cnt_all[wid];
+  Cand* s_sel = s_sel_all[wid];
   const uint32_t k = c.cfg.k;
-  for (uint32_t x = tid; x < QHASH; x += SIM_THREADS) { s_key[x] = NONE32; s_cnt[x] = 0; }
-  if (tid == 0) { s_nq = 0; s_nuq = 0; }
-  __syncthreads();
+  for (uint32_t x = lane; x < QHASH; x += 32) { s_key[x] = NONE32; s_cnt[x] = 0; }
+  __syncwarp();
   const uint32_t qa = q_off[i], qL = q_off[i + 1] - qa;
   if (qL > c.cfg.max_log_tokens) {
-    if (tid == 0) latch(c.sc, IL_ERR_ARG);
+    if (lane == 0) latch(c.sc, IL_ERR_ARG);
     return;
   }
-  for (uint32_t x = tid; x < qL; x += SIM_THREADS) {
+  for (uint32_t x = lane; x < qL; x += 32) {
     const uint32_t t = q_tok[qa + x];
     uint32_t s = qslot(t);
     while (true) {
@@ -84,16 +88,11 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
     }
     atomicAdd(&s_cnt[s], 1u);
   }
-  __syncthreads();
-  {
-    uint32_t nq = 0, nuq = 0;
-    for (uint32_t x = tid; x < QHASH; x += SIM_THREADS)
-      if (s_key[x] != NONE32) { nq += s_cnt[x] * s_cnt[x]; nuq += 1; }
-    for (int o = 16; o; o >>= 1) { nq += __shfl_xor_sync(~0u, nq, o); nuq += __shfl_xor_sync(~0u, nuq, o); }
-    if (lane == 0) { atomicAdd(&s_nq, nq); atomicAdd(&s_nuq, nuq); }
-  }
-  __syncthreads();
-  const uint32_t nq = s_nq, nuq = s_nuq;
+  __syncwarp();
+  uint32_t nq = 0, nuq = 0;
+  for (uint32_t x = lane; x < QHASH; x += 32)
+    if (s_key[x] != NONE32) { nq += s_cnt[x] * s_cnt[x]; nuq += 1; }
+  for (int o = 16; o; o >>= 1) { nq += __shfl_xor_sync(~0u, nq, o); nuq += __shfl_xor_sync(~0u, nuq, o); }
   const bool jac = c.cfg.metric == IL_SIM_JACCARD;
   const bool excl = (c.cfg.flags & IL_F_EXCLUDE_SELF) != 0;
   const uint32_t my_src = (excl && q_src) ? q_src[i] : NONE32;
@@ -103,21 +102,32 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
 #pragma unroll
   for (int q = 0; q < MAXK; ++q) { top[q].num = 0; top[q].den = 1; top[q].idx = NONE32; }
   uint32_t ntop = 0;
-  for (uint32_t m = tid; m < c.n_demos; m += SIM_THREADS) {
+  for (uint32_t m = lane; m < c.n_demos; m += 32) {
     if (excl && c.src[m] == my_src) continue;
     const uint32_t a = c.log_off[m], nu = c.uniq_n[m];
     uint32_t dot = 0, inter = 0;
-    for (uint32_t u = 0; u < nu; ++u) {
-      const uint32_t t = c.uniq_tok[a + u];
-      uint32_t s = qslot(t), cq = 0;
-      while (true) {
-        const uint32_t key = s_key[s];
-        if (key == t) { cq = s_cnt[s]; break; }
-        if (key == NONE32) break;
-        s = (s + 1) & (QHASH - 1);
+    // 8 tokens (+ counts) are loaded before any is probed: the loop is L2-latency bound
+    for (uint32_t u0 = 0; u0 < nu; u0 += 8) {
+      uint32_t tk[8], ct[8];
+#pragma unroll
+      for (uint32_t e = 0; e < 8; ++e) {
+        const bool in = u0 + e < nu;
+        tk[e] = in ? c.uniq_tok[a + u0 + e] : NONE32;
+        ct[e] = in ? c.uniq_cnt[a + u0 + e] : 0u;
       }
-      dot += cq * c.uniq_cnt[a + u];
-      inter += cq != 0;
+#pragma unroll
+      for (uint32_t e = 0; e < 8; ++e) {
+        const uint32_t t = tk[e];
+        uint32_t s = qslot(t), cq = 0;
+        while (t != NONE32) {
+          const uint32_t key = s_key[s];
+          if (key == t) { cq = s_cnt[s]; break; }
+          if (key == NONE32) break;
+          s = (s + 1) & (QHASH - 1);
+        }
+        dot += cq * ct[e];
+        inter += cq != 0;
+      }
     }
     Cand x;
     x.idx = m;
@@ -145,28 +155,22 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
     ntop = min(ntop + 1, (uint32_t)MAXK);
   }
   ntop = min(ntop, k);
-  // merge: every thread's sorted list goes to shared memory (static register indices), each
-  // warp merges its lanes' lists (k rounds of warp argmax; the winning lane pops its head), then
-  // warp 0 merges the 8 warp lists the same way (no block-wide rounds)
+  // merge: the lanes' sorted lists go to shared memory (static register indices), then k
+  // rounds of warp argmax (the winning lane pops its head)
 #pragma unroll
   for (int q = 0; q < MAXK; ++q)
     if ((uint32_t)q < ntop) { s_lnum[q][tid] = top[q].num; s_lden[q][tid] = (uint32_t)top[q].den; s_lidx[q][tid] = top[q].idx; }
   __syncwarp();
-  const uint32_t nw = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
-                                 ntop, k, lane, s_wl[wid]);
-  if (lane == 0) s_wn[wid] = nw;
-  __syncthreads();
-  if (wid == 0) {
-    const uint32_t wn = lane < SIM_THREADS / 32 ? s_wn[lane] : 0u;
-    const uint32_t n = warp_merge([&](uint32_t q) { return s_wl[lane][q]; }, wn, k, lane, s_sel);
-    if (lane == 0 && n < k) latch(c.sc, IL_ERR_ARG);     // fewer than k candidates
-    if (lane == 0) s_win = n;
+  const uint32_t nsel = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
+                                   ntop, k, lane, s_sel);
+  __syncwarp();
+  if (nsel < k) {
+    if (lane == 0) latch(c.sc, IL_ERR_ARG);             // fewer than k candidates
+    return;
   }
-  __syncthreads();
-  if (s_win < k) return;
-  if (tid < k) {
+  if (lane < k) {
     // emit ascending by similarity, ties by index ascending: position = rank
-    const Cand me = s_sel[tid];
+    const Cand me = s_sel[lane];
     uint32_t pos = 0;
     for (uint32_t r = 0; r < k; ++r) {
       const Cand o = s_sel[r];
@@ -226,21 +230,38 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
   uint32_t bp = 0, bs = NONE32;
   uint64_t bst = 0;
   if (c.cfg.flags & IL_F_PAIR) {
-    for (uint32_t s = tid; s < T; s += REF_THREADS) {
-      const uint64_t st = c.tab_stamp[s];
-      if (st == 0) continue;
-      uint32_t used = 0, p = 0;
-      for (uint32_t j = 0; j < k; ++j) {
-        const uint32_t t = c.tab_tpl[(size_t)j * T + s];
-        bool found = false;
+    // SCAN slots per thread per round, every stamp and template id loaded before any is used
+    // (the scan is L2-latency bound: keep the loads in flight together)
+    constexpr uint32_t SCAN = 4;
+    for (uint32_t s0 = tid; s0 < T; s0 += SCAN * REF_THREADS) {
+      uint64_t st[SCAN];
+      uint32_t tt[SCAN][MAXK];
 #pragma unroll
-        for (int q = 0; q < MAXK; ++q) {
-          if (!found && !((used >> q) & 1u) && tc[q] == t) { used |= 1u << q; found = true; }
-        }
-        if (!found) break;
-        ++p;
+      for (uint32_t u = 0; u < SCAN; ++u) {
+        const uint32_t s = s0 + u * REF_THREADS;
+        st[u] = s < T ? c.tab_stamp[s] : 0ull;
+#pragma unroll
+        for (uint32_t j = 0; j < MAXK; ++j) tt[u][j] = (s < T && j < k) ? c.tab_tpl[(size_t)j * T + s] : NONE32;
       }
-      if (p > bp || (p == bp && p > 0 && st > bst)) { bp = p; bst = st; bs = s; }
+#pragma unroll
+      for (uint32_t u = 0; u < SCAN; ++u) {
+        if (st[u] == 0) continue;
+        uint32_t used = 0, p = 0;
+        bool run = true;
+#pragma unroll
+        for (uint32_t j = 0; j < MAXK; ++j) {
+          if (run && j < k) {                          // (predicated: the loop stays unrolled)
+            bool found = false;
+#pragma unroll
+            for (int q = 0; q < MAXK; ++q) {
+              if (!found && !((used >> q) & 1u) && tc[q] == tt[u][j]) { used |= 1u << q; found = true; }
+            }
+            if (!found) run = false; else ++p;
+          }
+        }
+        const uint32_t s = s0 + u * REF_THREADS;
+        if (p > bp || (p == bp && p > 0 && st[u] > bst)) { bp = p; bst = st[u]; bs = s; }
+      }
     }
     for (int o = 16; o; o >>= 1) {
       const uint32_t op = __shfl_xor_sync(~0u, bp, o), os = __shfl_xor_sync(~0u, bs, o);
@@ -303,7 +324,13 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
   uint32_t* row = prompt_tok + (size_t)i * stride;
   auto render = [&](const uint32_t* ds, uint32_t* out) {        // all threads of the CTA
     uint32_t o = c.n_instr;
-    for (uint32_t x = tid; x < c.n_instr; x += REF_THREADS) out[x] = c.instr[x];
+    {                                                  // instruction: 16-byte vectors (row stride and
+      const uint32_t nv = c.n_instr / 4;               // buffers are 16-byte aligned), then the tail
+      const uint4* src = reinterpret_cast<const uint4*>(c.instr);
+      uint4* dst = reinterpret_cast<uint4*>(out);
+      for (uint32_t x = tid; x < nv; x += REF_THREADS) dst[x] = src[x];
+      for (uint32_t x = 4 * nv + tid; x < c.n_instr; x += REF_THREADS) out[x] = c.instr[x];
+    }
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t d = ds[j], a = c.rend_off[d], n = c.rend_len[d];
       for (uint32_t x = tid; x < n; x += REF_THREADS) out[o + x] = c.rend_tok[a + x];
@@ -364,8 +391,9 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   if (!c->pool_loaded) { set_error("il_refine_batch before il_pool_load"); return IL_ERR_STATE; }
   if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
   if (B == 0) return IL_OK;
+  if (((uintptr_t)prompt_tok & 15) != 0) { set_error("prompt_tok must be 16-byte aligned"); return IL_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)s;
-  k_sim_topk<<<B, SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+  k_sim_topk<<<cdiv(B, SIM_THREADS / 32), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
   if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
   k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
