@@ -41,19 +41,12 @@ __global__ void __launch_bounds__(256) k_kv_append(Ctx c, uint32_t B, const int3
 __global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q,
                                                     const int32_t* __restrict__ prefix_len, uint32_t tq,
                                                     uint32_t cascade) {
-  __shared__ uint32_t s[1024];
+  __shared__ uint32_t s_w[32];
   const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
   uint32_t n = 0;
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) n += cdiv((uint32_t)(cu_q[i + 1] - cu_q[i]), tq);
-  s[tid] = n;
-  __syncthreads();
-  for (uint32_t o = 1; o < 1024; o <<= 1) {
-    const uint32_t a = tid >= o ? s[tid - o] : 0;
-    __syncthreads();
-    s[tid] += a;
-    __syncthreads();
-  }
-  uint32_t acc = tid ? s[tid - 1] : 0;
+  uint32_t total;
+  uint32_t acc = block_scan(n, s_w, &total);
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     c.tile_off[i] = acc;
     const uint32_t nt = cdiv((uint32_t)(cu_q[i + 1] - cu_q[i]), tq);
@@ -61,7 +54,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int
     acc += nt;
   }
   if (tid == 1023) {
-    c.tile_off[B] = s[1023]; c.sc->n_tiles = s[1023];
+    c.tile_off[B] = total; c.sc->n_tiles = total;
     const uint32_t tot = (uint32_t)cu_q[B];
     c.sc->q_total = tot;
     c.sc->n_dense = cdiv(tot, tq);

@@ -185,30 +185,6 @@ __global__ void __launch_bounds__(256) k_tab_find(Ctx c, uint32_t B) {
   if (lane == 0) { c.tab_find[i] = found; c.tab_last[i] = rep == i; }
 }
 
-// block-wide exclusive scan of one value per thread (1024 threads)
-__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32_t* total) {
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(~0u, x, o);
-    if (lane >= (uint32_t)o) x += y;
-  }
-  if (lane == 31) s_w[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    uint32_t t = s_w[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(~0u, t, o);
-      if (lane >= (uint32_t)o) t += y;
-    }
-    s_w[lane] = t;
-  }
-  __syncthreads();
-  const uint32_t before = (w ? s_w[w - 1] : 0) + x - v;
-  *total = s_w[31];
-  __syncthreads();
-  return before;
-}
 
 // k_tab_commit (one CTA of 1024 threads, T <= 8192 slots, B <= 8192 requests).
 // The recency order after the batch is: untouched old entries (stamps of earlier batches),

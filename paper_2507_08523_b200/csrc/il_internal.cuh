@@ -178,6 +178,56 @@ __device__ __forceinline__ uint32_t index_find(const uint64_t* __restrict__ slot
 
 __host__ __device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 
+
+// block-wide exclusive scan of one value per thread (1024 threads)
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32_t* total) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(~0u, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = s_w[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(~0u, t, o);
+      if (lane >= (uint32_t)o) t += y;
+    }
+    s_w[lane] = t;
+  }
+  __syncthreads();
+  const uint32_t before = (w ? s_w[w - 1] : 0) + x - v;
+  *total = s_w[31];
+  __syncthreads();
+  return before;
+}
+
+// block-wide inclusive prefix max of one int32 per thread (1024 threads)
+__device__ __forceinline__ int32_t block_scan_max(int32_t v, int32_t* s_w) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(~0u, x, o);
+    if (lane >= (uint32_t)o) x = max(x, y);
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int32_t t = s_w[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(~0u, t, o);
+      if (lane >= (uint32_t)o) t = max(t, y);
+    }
+    s_w[lane] = t;
+  }
+  __syncthreads();
+  const int32_t r = w ? max(x, s_w[w - 1]) : x;
+  __syncthreads();
+  return r;
+}
+
 }  // namespace il
 
 struct il_ctx : public il::Ctx {};

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
                                                      int32_t* __restrict__ prefix_len, int32_t* __restrict__ cu_q,
                                                      uint64_t) {
   const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
-  __shared__ uint32_t s_need[1024], s_suf[1024];
+  __shared__ uint32_t s_w[32];
   __shared__ int32_t s_top[1025];
   const uint32_t tid = threadIdx.x, per = cdiv(B, 1024);
   // Touch + pin the instruction's hit blocks once: block j gets stamp (b, max{i : h_i > j}).
@@ -56,7 +56,12 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
   __syncthreads();
   for (uint32_t i = tid; i < B; i += 1024) atomicMax(&s_top[min(hit[i], nI)], (int32_t)i);
   __syncthreads();
-  if (tid == 0) {                                       // suffix max: s_top[c] = max over c' >= c
+  // suffix max: s_top[c] = max over c' >= c (a block max-scan over the reversed entries)
+  if (nI < 1024) {
+    const int32_t v = tid <= nI ? s_top[nI - tid] : -1;
+    const int32_t r = block_scan_max(v, reinterpret_cast<int32_t*>(s_w));
+    if (tid <= nI) s_top[nI - tid] = r;
+  } else if (tid == 0) {
     for (int x = (int)nI - 1; x >= 0; --x) s_top[x] = max(s_top[x], s_top[x + 1]);
   }
   __syncthreads();
@@ -78,15 +83,9 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
     n += cdiv(L, BS) - h;
     sfx += L - BS * h;
   }
-  s_need[tid] = n; s_suf[tid] = sfx;
-  __syncthreads();
-  for (uint32_t o = 1; o < 1024; o <<= 1) {          // Hillis-Steele inclusive scan
-    uint32_t a = tid >= o ? s_need[tid - o] : 0, b = tid >= o ? s_suf[tid - o] : 0;
-    __syncthreads();
-    s_need[tid] += a; s_suf[tid] += b;
-    __syncthreads();
-  }
-  uint32_t an = tid ? s_need[tid - 1] : 0, as = tid ? s_suf[tid - 1] : 0;
+  uint32_t need, suf;
+  uint32_t an = block_scan(n, s_w, &need);
+  uint32_t as = block_scan(sfx, s_w, &suf);
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     const uint32_t L = prompt_len[i], h = hit[i];
     c.need_off[i] = an; cu_q[i] = (int32_t)as; prefix_len[i] = (int32_t)(BS * h);
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
     as += L - BS * h;
   }
   if (tid == 1023) {
-    const uint32_t need = s_need[1023], suf = s_suf[1023];
     c.need_off[B] = need; cu_q[B] = (int32_t)suf;
     DevScalars* sc = c.sc;
     sc->need_total = need;
