@@ -53,32 +53,43 @@ __device__ __forceinline__ uint32_t warp_merge(Get get, uint32_t n, uint32_t k, 
 }
 __device__ __forceinline__ uint32_t qslot(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 9); }
 
+// QW warps per query (the CTA's 4 warps serve 4 / QW queries): QW = 1 for pools up to
+// SIM_BIG_POOL demos (no block-wide rounds, most queries per SM), QW = 4 above (4x the lanes per
+// query when the scoring loop dominates).
+constexpr uint32_t SIM_BIG_POOL = 1024;
+template <int QW>
 __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
                                                           const uint32_t* __restrict__ q_tok,
                                                           const uint32_t* __restrict__ q_src,
                                                           uint32_t* __restrict__ topk) {
-  // one WARP per query (8 per CTA), no block-wide barriers: the query multiset goes into the
-  // warp's own shared-memory hash table, lanes score a strided subset of the pool
-  constexpr uint32_t NW = SIM_THREADS / 32;
-  __shared__ uint32_t s_key_all[NW][QHASH], s_cnt_all[NW][QHASH];
+  // the query multiset goes into the query's shared-memory hash table, the query's lanes score
+  // a strided subset of the pool
+  constexpr uint32_t NW = SIM_THREADS / 32, NQ = NW / QW, GT = QW * 32;
+  __shared__ uint32_t s_key_all[NQ][QHASH], s_cnt_all[NQ][QHASH];
   __shared__ uint64_t s_lnum[MAXK][SIM_THREADS];
   __shared__ uint32_t s_lden[MAXK][SIM_THREADS], s_lidx[MAXK][SIM_THREADS];
-  __shared__ Cand s_sel_all[NW][MAXK];
+  __shared__ Cand s_wl[NW][MAXK];
+  __shared__ uint32_t s_wn[NW], s_red[NW][2];
+  __shared__ Cand s_sel_all[NQ][MAXK];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t i = blockIdx.x * NW + wid;
-  if (i >= B) return;                                   // (warp-uniform)
-  uint32_t* s_key = s_key_all[wid];
-  uint32_t* s_cnt = s_cnt_all[wid];
-  Cand* s_sel = s_sel_all[wid];
+  const uint32_t grp = wid / QW, sub = wid % QW, gt = sub * 32 + lane;
+  const uint32_t i = blockIdx.x * NQ + grp;
+  bool live = i < B;                                    // (every warp still takes the barriers)
+  uint32_t* s_key = s_key_all[grp];
+  uint32_t* s_cnt = s_cnt_all[grp];
+  Cand* s_sel = s_sel_all[grp];
   const uint32_t k = c.cfg.k;
-  for (uint32_t x = lane; x < QHASH; x += 32) { s_key[x] = NONE32; s_cnt[x] = 0; }
-  __syncwarp();
-  const uint32_t qa = q_off[i], qL = q_off[i + 1] - qa;
-  if (qL > c.cfg.max_log_tokens) {
-    if (lane == 0) latch(c.sc, IL_ERR_ARG);
-    return;
+  for (uint32_t x = gt; x < QHASH; x += GT) { s_key[x] = NONE32; s_cnt[x] = 0; }
+  __syncthreads();
+  uint32_t qa = 0, qL = 0;
+  if (live) {
+    qa = q_off[i]; qL = q_off[i + 1] - qa;
+    if (qL > c.cfg.max_log_tokens) {
+      if (gt == 0) latch(c.sc, IL_ERR_ARG);
+      live = false; qL = 0;
+    }
   }
-  for (uint32_t x = lane; x < qL; x += 32) {
+  for (uint32_t x = gt; x < qL; x += GT) {
     const uint32_t t = q_tok[qa + x];
     uint32_t s = qslot(t);
     while (true) {
@@ -88,21 +99,27 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
     }
     atomicAdd(&s_cnt[s], 1u);
   }
-  __syncwarp();
+  __syncthreads();
   uint32_t nq = 0, nuq = 0;
-  for (uint32_t x = lane; x < QHASH; x += 32)
+  for (uint32_t x = gt; x < QHASH; x += GT)
     if (s_key[x] != NONE32) { nq += s_cnt[x] * s_cnt[x]; nuq += 1; }
   for (int o = 16; o; o >>= 1) { nq += __shfl_xor_sync(~0u, nq, o); nuq += __shfl_xor_sync(~0u, nuq, o); }
+  if (QW > 1) {
+    if (lane == 0) { s_red[wid][0] = nq; s_red[wid][1] = nuq; }
+    __syncthreads();
+    nq = nuq = 0;
+    for (uint32_t q = 0; q < QW; ++q) { nq += s_red[grp * QW + q][0]; nuq += s_red[grp * QW + q][1]; }
+  }
   const bool jac = c.cfg.metric == IL_SIM_JACCARD;
   const bool excl = (c.cfg.flags & IL_F_EXCLUDE_SELF) != 0;
-  const uint32_t my_src = (excl && q_src) ? q_src[i] : NONE32;
+  const uint32_t my_src = (live && excl && q_src) ? q_src[i] : NONE32;
 
   // private sorted list, always MAXK long: padded with a sentinel every real candidate beats
   Cand top[MAXK];
 #pragma unroll
   for (int q = 0; q < MAXK; ++q) { top[q].num = 0; top[q].den = 1; top[q].idx = NONE32; }
   uint32_t ntop = 0;
-  for (uint32_t m = lane; m < c.n_demos; m += 32) {
+  for (uint32_t m = gt; m < (live ? c.n_demos : 0u); m += GT) {
     if (excl && c.src[m] == my_src) continue;
     const uint32_t a = c.log_off[m], nu = c.uniq_n[m];
     uint32_t dot = 0, inter = 0;
@@ -155,15 +172,24 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, con
     ntop = min(ntop + 1, (uint32_t)MAXK);
   }
   ntop = min(ntop, k);
-  // merge: the lanes' sorted lists go to shared memory (static register indices), then k
-  // rounds of warp argmax (the winning lane pops its head)
+  // merge: the lanes' sorted lists go to shared memory (static register indices), k rounds of
+  // warp argmax per warp (the winning lane pops its head), then (QW > 1) the query's first warp
+  // merges its QW warp lists the same way
 #pragma unroll
   for (int q = 0; q < MAXK; ++q)
     if ((uint32_t)q < ntop) { s_lnum[q][tid] = top[q].num; s_lden[q][tid] = (uint32_t)top[q].den; s_lidx[q][tid] = top[q].idx; }
   __syncwarp();
-  const uint32_t nsel = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
-                                   ntop, k, lane, s_sel);
+  uint32_t nsel = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
+                             ntop, k, lane, QW == 1 ? s_sel : s_wl[wid]);
+  if (QW > 1) {
+    if (lane == 0) s_wn[wid] = nsel;
+    __syncthreads();
+    if (sub != 0) return;
+    const uint32_t wn = lane < QW ? s_wn[grp * QW + lane] : 0u;
+    nsel = warp_merge([&](uint32_t q) { return s_wl[grp * QW + lane][q]; }, wn, k, lane, s_sel);
+  }
   __syncwarp();
+  if (!live) return;
   if (nsel < k) {
     if (lane == 0) latch(c.sc, IL_ERR_ARG);             // fewer than k candidates
     return;
@@ -393,7 +419,10 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   if (B == 0) return IL_OK;
   if (((uintptr_t)prompt_tok & 15) != 0) { set_error("prompt_tok must be 16-byte aligned"); return IL_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)s;
-  k_sim_topk<<<cdiv(B, SIM_THREADS / 32), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+  if (c->n_demos > SIM_BIG_POOL)
+    k_sim_topk<4><<<cdiv(B, SIM_THREADS / 128), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+  else
+    k_sim_topk<1><<<cdiv(B, SIM_THREADS / 32), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
   if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
   k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
