@@ -41,13 +41,10 @@ __device__ unsigned int g_trace_item[1024][4];
 #define IL_TRACE(slot, idx) do { } while (0)
 #endif
 
-constexpr uint32_t D = 128;              // head dim handled by this kernel
 constexpr uint32_t BM = 128;             // rows per M-tile
 constexpr uint32_t BN = 128;             // keys per KV tile (= 8 pages) = one softmax step
 constexpr uint32_t CB = 16384;           // one 64-column block of a 128-row bf16 tile
-constexpr uint32_t QTILE = 2 * CB;       // 128 x 128 bf16 = 32 KB
 constexpr uint32_t KCB = CB;             // one 64-column block of a 128-key K/V tile
-constexpr uint32_t KVTILE = 2 * KCB;     // 128 x 128 bf16 = 32 KB
 #ifndef IL_NSTK
 #define IL_NSTK 3
 #endif
@@ -55,12 +52,10 @@ constexpr uint32_t KVTILE = 2 * KCB;     // 128 x 128 bf16 = 32 KB
 #define IL_NSTV 2
 #endif
 constexpr uint32_t NSTK = IL_NSTK, NSTV = IL_NSTV;   // K and V ring depths
-constexpr uint32_t OFF_QA = 0, OFF_QB = QTILE;
-constexpr uint32_t OFF_K = 2 * QTILE;                // K[s] = OFF_K + s * KVTILE
-constexpr uint32_t OFF_V = OFF_K + NSTK * KVTILE;    // V[s] = OFF_V + s * KVTILE
-constexpr uint32_t OFF_BAR = OFF_V + NSTV * KVTILE;
+// smem (per head dim DH, NCB = DH / 64 column blocks): Q pair [0, 2 QTILE), K ring at OFF_K
+// (K[s] = OFF_K + s KVTILE), V ring at OFF_V, barriers at OFF_BAR; QTILE = KVTILE = NCB x 16 KB
+__host__ __device__ constexpr uint32_t smem_bytes(uint32_t DH) { return (2 + NSTK + NSTV) * (DH / 64) * CB + 256; }
 constexpr uint32_t NBAR = 16 + 2 * NSTK + 2 * NSTV;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
 constexpr int THREADS = 384;
 // Softmax warpgroup x owns Q tile x (thread = one full 128-key row, no max exchange); the two
 // tiles' softmaxes run concurrently, so one's row max / bookkeeping overlaps the other's
@@ -297,8 +292,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 // instruction descriptor kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // A major [15] (0 = K), B major [16] (1 = MN), N >> 3 [17,23), M >> 4 [24,29)
+template <uint32_t DH>   // P V: A = P (K-major), B = V (MN-major), N = head dim
+constexpr uint32_t IDESC_PV_T = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((DH >> 3) << 17) | ((BM >> 4) << 24);
 constexpr uint32_t IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
-constexpr uint32_t IDESC_PV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((D >> 3) << 17) | ((BM >> 4) << 24);
 
 // ------------------------------------------------------------------ work decomposition
 // M-tile t = (request i, tile mt of TQ tokens).  A work item is a PAIR of consecutive M-tiles
@@ -465,12 +461,18 @@ struct LoadSeq {
 #define IL_STREAMS 0
 #endif
 
+template <uint32_t DH>
 __global__ void __launch_bounds__(THREADS, 1)
     k_attn_sm100(Ctx c, uint32_t B, const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
                  const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                  float scale_log2, uint32_t g, uint32_t TQ, uint32_t phase, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_o,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+  // head dim DH = 128 or 64: one 64-column (128-byte swizzle atom) block of Q / K / V per 64 dims
+  constexpr uint32_t D = DH, NCB = DH / 64;
+  constexpr uint32_t QTILE = NCB * CB, KVTILE = NCB * KCB;
+  constexpr uint32_t OFF_QA = 0, OFF_K = 2 * QTILE, OFF_V = OFF_K + NSTK * KVTILE, OFF_BAR = OFF_V + NSTV * KVTILE;
+    static_assert(DH == 64 || DH == 128, "head dim");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023) != 0) __trap();          // swizzle atoms need 1024-byte alignment
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane < 2) {
       // Q rows live in HBM (the whole batch's Q exceeds L2): the stream's NEXT Q tile is
       // prefetched into L2 when the current one is loaded, so the load at the item boundary hits L2
-      const uint32_t x = lane, qbytes = 2 * 128 * g * TQ;
+      const uint32_t x = lane, qbytes = 2 * D * g * TQ;
       auto seek = [&](uint32_t& w, Tile& T) {
         for (; w < n_items; w += gridDim.x) {
           T = decode_tile(c, cu_q, prefix_len, 2 * (w / Hkv) + x, TQ, phase, NC);
@@ -537,15 +539,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (ix >= 1) mbar_wait(bar(Q_FREE + x), (ix - 1) & 1);
         mbar_expect_tx(bar(Q_FULL + x), qbytes);
         const int row = (int)(T.r0 + T.mt * TQ), hq = (int)((w % Hkv) * g);
-        tma_load_3d(sbase + OFF_QA + x * QTILE, &tm_q, 0, hq, row, bar(Q_FULL + x));
-        tma_load_3d(sbase + OFF_QA + x * QTILE + CB, &tm_q, 64, hq, row, bar(Q_FULL + x));
+#pragma unroll
+        for (uint32_t h = 0; h < NCB; ++h)
+          tma_load_3d(sbase + OFF_QA + x * QTILE + h * CB, &tm_q, (int)(64 * h), hq, row, bar(Q_FULL + x));
         if (IL_Q_PREFETCH && wn < n_items) {
           const int rown = (int)(Tn.r0 + Tn.mt * TQ), hqn = (int)((wn % Hkv) * g);
-          tma_prefetch_3d(&tm_q, 0, hqn, rown);
-          tma_prefetch_3d(&tm_q, 64, hqn, rown);
-          if (phase == 1) {                             // the next item's phase-2 partial (O / l rows)
-            tma_prefetch_3d(&tm_o, 0, hqn, rown);
-            tma_prefetch_3d(&tm_o, 64, hqn, rown);
+#pragma unroll
+          for (uint32_t h = 0; h < NCB; ++h) {
+            tma_prefetch_3d(&tm_q, (int)(64 * h), hqn, rown);
+            if (phase == 1) tma_prefetch_3d(&tm_o, (int)(64 * h), hqn, rown);   // the next item's partial
           }
         }
         ++ix;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_expect_tx(bar(full0 + s), KVTILE);
       }
       __syncwarp();
-      if (lane < 16) {                                 // lane = (page, column half)
+      if (lane < 8 * NCB) {                            // lane = (page, 64-column block)
         const uint32_t p = lane & 7, h = lane >> 3;
         const int row = (int)(((uint32_t)page * Hkv + L.kh) * BS);
         tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
@@ -611,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // IL_P_SPLIT: keys 0-63 of P are released first; their MMAs run while the softmax
         // computes keys 64-127
         if (IL_P_SPLIT && k == 4) { mbar_wait(bar(P_FULL + x), pc[x] & 1); tc_fence_after(); }
-        mma_ts_w<IDESC_PV>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst[x] && k == 0) ? 0u : 1u);
+        mma_ts_w<IDESC_PV_T<DH>>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (fst[x] && k == 0) ? 0u : 1u);
       }
       fst[x] = false;
       commit_w(bar(PV_DONE + x));
@@ -649,7 +651,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const uint64_t dq = dq0 + (uint64_t)((x * QTILE) >> 4);
 #pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
+        for (uint32_t k = 0; k < D / 16; ++k)
           mma_ss_w<IDESC_QK>(tmem + 128 * x, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
                              dk + (uint64_t)(((k >> 2) * KCB + (k & 3) * 32) >> 4), k ? 1u : 0u);
         commit_w(bar(S_FULL + x));
@@ -692,11 +694,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         // (the rows were prefetched into L2 by the Q producer one item ahead)
         if (valid) { m_used = c.attn_ml[orow]; l = 1.f; }
         const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
-        uint4 raw[16];
+        uint4 raw[D / 8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) raw[j] = valid ? src[j] : make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < (int)(D / 8); ++j) raw[j] = valid ? src[j] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < (int)(D / 32); ++q) {
           float ov[32];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -760,7 +762,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(bar(PV_DONE + xo), (cnt - 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < (int)(D / 32); ++q) {
             float ov[32];
             tmem_ld32(o_tmem + 32 * q, ov);
             tmem_wait_ld();
@@ -817,7 +819,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       {
         const float inv = 1.f / l;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < (int)(D / 32); ++q) {
           float ov[32];
           tmem_ld32(o_tmem + 32 * q, ov);
           tmem_wait_ld();
@@ -902,7 +904,11 @@ __global__ void __launch_bounds__(256) k_shared_scan(Ctx c, uint32_t B, const in
       const uint32_t bad = __ballot_sync(~0u, ne);
       if (bad) { n += __ffs(bad) - 1; break; }
     }
-    if (lane == 0 && n < lim) atomicMin(&c.sc->shared_blk, n);
+    // n = blocks shared with request 0 (<= lim).  Also when every block up to lim matched, a
+    // request whose hits end before the current bound lowers it to its own hit count: otherwise
+    // its M-tiles would start inside the shared range (zero phase-2 KV tiles: a hang)
+    n = min(n, lim);
+    if (lane == 0 && n < *(volatile uint32_t*)&c.sc->shared_blk) atomicMin(&c.sc->shared_blk, n);
   }
 }
 
@@ -924,20 +930,20 @@ static inline bool attn_sm100_supported(const Ctx* c) {
   const char* e = getenv("IL_ATTN");
   if (e && e[0] == 's') return false;                 // IL_ATTN=simple: bring-up kernel (cross-checks)
   const uint32_t g = c->cfg.n_q_heads / c->cfg.n_kv_heads;
-  return c->cfg.head_dim == sm100::D && g >= 1 && g <= 8;
+  return (c->cfg.head_dim == 128 || c->cfg.head_dim == 64) && g >= 1 && g <= 8;
 }
 
 static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
                                           const int32_t* block_table, const il_bf16* q, il_bf16* k_pages,
                                           il_bf16* v_pages, il_bf16* out, float* lse, float scale, cudaStream_t st) {
   using namespace sm100;
-  const uint32_t Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads, g = Hq / Hkv, TQ = BM / g;
+  const uint32_t Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads, g = Hq / Hkv, TQ = BM / g, D = c->cfg.head_dim;
   auto enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return IL_ERR_CUDA; }
   CUtensorMap tq, to, tk, tv;
   for (int which = 0; which < 2; ++which) {            // Q, and `out` (same geometry: L2 prefetch only)
     cuuint64_t dims[3] = {D, Hq, c->cfg.max_suffix_tokens};
-    cuuint64_t strides[2] = {D * 2, (cuuint64_t)Hq * D * 2};
+    cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)Hq * D * 2};
     cuuint32_t box[3] = {64, g, TQ};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(which ? &to : &tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, which ? (void*)out : (void*)q, dims, strides, box, es,
@@ -947,7 +953,7 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   }
   for (int which = 0; which < 2; ++which) {
     cuuint64_t dims[2] = {D, (cuuint64_t)c->cfg.kv_pages * Hkv * BS};
-    cuuint64_t strides[1] = {D * 2};
+    cuuint64_t strides[1] = {(cuuint64_t)D * 2};
     cuuint32_t box[2] = {64, BS};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(which ? &tv : &tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, which ? (void*)v_pages : (void*)k_pages,
@@ -962,13 +968,18 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
   static bool attr = false;
   if (!attr) {
-    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(128)));
+    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(64)));
     attr = true;
   }
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
     if (phase == 1 && !cascade) break;
-    k_attn_sm100<<<c->num_sms, THREADS, SMEM_BYTES, st>>>(*c, B, cu_q, prefix_len, block_table, (__nv_bfloat16*)out,
-                                                          lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
+    if (D == 128)
+      k_attn_sm100<128><<<c->num_sms, THREADS, smem_bytes(128), st>>>(*c, B, cu_q, prefix_len, block_table,
+          (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
+    else
+      k_attn_sm100<64><<<c->num_sms, THREADS, smem_bytes(64), st>>>(*c, B, cu_q, prefix_len, block_table,
+          (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");
   }
   c->launches += cascade ? (B > 1 ? 5 : 4) : 3;

@@ -105,3 +105,12 @@ def test_attention_long_prompts_no_cascade(monkeypatch):
     # IL_CASCADE=0: one phase over each request's whole prefix (the NC = 0 path)
     monkeypatch.setenv("IL_CASCADE", "0")
     run(_long(16), n_batches=2, sample=6, max_rows=48)
+
+
+def test_attention_eviction_pressure_uneven_hits():
+    # requests of one batch with fewer cached blocks than the batch-wide shared prefix bound (LRU
+    # pressure, cold ramp): the cascade's shared range must shrink to the smallest hit count
+    # (a request whose M-tiles started inside it would have no phase-2 KV tile)
+    sp = StreamSpec(B=64, C=700, n_logs=3000, Hq=4, Hkv=4, d=128,
+                    flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4, 16))
+    run(sp, n_batches=14, sample=8)
