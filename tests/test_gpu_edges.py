@@ -1,0 +1,67 @@
+"""Edge cases and error behaviour of the boundary on the GPU (include/il.h): empty batches,
+host-detected argument errors, and device-latched capacity / length errors."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2507_08523_b200 import _lib as L
+from tests.parity_util import StreamSpec, compare_batch, compare_state, gpu_pipeline, make_stream, oracle_for
+from workload import gen
+
+pytestmark = pytest.mark.gpu
+
+
+def test_empty_batch_is_a_noop_for_the_path():
+    sp = StreamSpec(B=24, C=2048)
+    ds, pool, instr = make_stream(sp)
+    o, pl = oracle_for(sp, pool, instr), gpu_pipeline(sp, pool, instr)
+    batch = gen.make_batch(ds, 0, sp.B)
+    r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=sp.max_prompt_tokens // 16)
+    pl.stage_batch(batch); pl.step(); pl.ctx.status_sync()
+    compare_batch(r, pl, sp.B, sp, where="before")
+    before = pl.ctx.index_dump(), pl.ctx.table_dump()
+    for call in (pl.refine, pl.match, pl.synth, pl.attn):   # B = 0: every call returns IL_OK at once
+        call(0)
+    pl.ctx.status_sync()
+    after = pl.ctx.index_dump(), pl.ctx.table_dump()
+    for a, b in zip(before[0] + before[1], after[0] + after[1]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_host_detected_argument_errors():
+    sp = StreamSpec(B=8, C=512)
+    ds, pool, instr = make_stream(sp)
+    pl = gpu_pipeline(sp, pool, instr)
+    pl.stage_batch(gen.make_batch(ds, 0, sp.B))
+    with pytest.raises(L.ILError) as e:                    # B > max_batch
+        pl.refine(sp.B + 1)
+    assert e.value.status == L.IL_ERR_ARG
+    with pytest.raises(L.ILError) as e:                    # prompt rows not 16-byte aligned
+        pl.ctx.refine_batch(sp.B, pl.q_off, pl.q_tok, pl.q_src, pl.topk, pl.final_ds, pl.info,
+                            pl.prompt_tok.view(-1)[1:], pl.prompt_len)
+    assert e.value.status == L.IL_ERR_ARG
+
+
+def test_device_latched_capacity_error():
+    # a cold batch needs more pages than the cache has: il_prefix_match latches IL_ERR_CAPACITY
+    sp = StreamSpec(B=32, C=40)
+    ds, pool, instr = make_stream(sp)
+    pl = gpu_pipeline(sp, pool, instr)
+    pl.stage_batch(gen.make_batch(ds, 0, sp.B))
+    pl.refine(); pl.match()
+    with pytest.raises(L.ILError) as e:
+        pl.ctx.status_sync()
+    assert e.value.status == L.IL_ERR_CAPACITY
+
+
+def test_device_latched_prompt_too_long():
+    # instruction + k demonstrations + query longer than max_prompt_tokens: latched IL_ERR_ARG
+    sp = StreamSpec(B=8, C=512, n_instr=300, max_prompt_tokens=320)
+    ds, pool, instr = make_stream(sp)
+    pl = gpu_pipeline(sp, pool, instr)
+    pl.stage_batch(gen.make_batch(ds, 0, sp.B))
+    pl.refine()
+    with pytest.raises(L.ILError) as e:
+        pl.ctx.status_sync()
+    assert e.value.status == L.IL_ERR_ARG
