@@ -193,13 +193,15 @@ def run_ours(args, rank, world, local_rank):
     pl.ctx.status_sync(stream)
 
     stage_names = ["refine", "match", "synth", "attn", "commit"]
-    # CUDA graphs: each stage captured once for B (one replay per stage, no per-kernel launch
-    # gaps); with N > 1 the commit (NCCL all-gather inside) stays eager
+    # CUDA graphs (N = 1): each stage captured once for B (one replay per stage, no per-kernel
+    # launch gaps).  N > 1 launches eagerly: the commit's all-gather (NCCL) stays outside any
+    # graph, and eager calls keep the library's host-side call-order checks (a replayed graph does
+    # not pass through them, so an eager il_commit_index after replayed stages would be refused)
     graphs, per_step_launches = None, None
-    if not args.no_graph:
+    if not args.no_graph and dp is None:
         l0 = pl.launches()
         with torch.cuda.stream(stream):
-            graphs = pl.capture(cfg.B, stages=stage_names if dp is None else stage_names[:-1])
+            graphs = pl.capture(cfg.B, stages=stage_names)
         per_step_launches = pl.launches() - l0
         stream.synchronize()
 
@@ -351,7 +353,7 @@ def run_ours(args, rank, world, local_rank):
                    "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
                    "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
                    "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
-                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards" + ("; ICL records all-gathered per batch, NCCL)" if world > 1 else ")"),
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards" + (f"; ICL records all-gathered per batch, {dist.get_backend()})" if world > 1 else ")"),
                    "stream": f"{ds.n} distinct logs, no query repeats within the run",
                    "int_dtype": "u32/u64 bit-exact", "attn": "bf16 in, fp32 accumulate"},
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
@@ -507,6 +509,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("IL_BENCH_ONE_DEVICE"):
+        # plumbing check on a one-GPU box only (never a reported number): every rank on cuda:0,
+        # collectives over gloo (NCCL refuses two ranks on one GPU)
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -514,7 +520,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("IL_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -7,3 +7,5 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 cat gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>&1; echo ref=$?
 tail -2 gpurun_out/bench_ref.json
+# N = 2 plumbing of bench.py on a one-GPU box (gloo, both ranks on cuda:0; not a reported number)
+IL_BENCH_ONE_DEVICE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/dp2.json 2> gpurun_out/dp2.err; echo dp2=$?
