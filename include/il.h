@@ -170,7 +170,11 @@ il_status il_prefix_match(il_ctx* ctx, uint32_t B,
  *   q, out        [max_suffix_tokens][Hq][d]  bf16;  lse [..][Hq] f32 natural log, or NULL
  *   k_new, v_new  [max_suffix_tokens][Hkv][d] bf16
  *   k_pages, v_pages  [C][Hkv][16][d] bf16, caller-owned, persistent across batches
- * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27). */
+ * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27).
+ * Runs on the tcgen05/TMA kernel for head_dim 64 or 128 and Hq/Hkv in 1..8 (else the CUDA-core
+ * kernel).  Requires a preceding il_prefix_match of the same batch (IL_ERR_STATE otherwise);
+ * out and the workspace hold the cascade's partial between its two launches, so out must not be
+ * read before the call's work completes on stream s. */
 il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
                           const int32_t* block_table,
                           const il_bf16* q, const il_bf16* k_new, const il_bf16* v_new,
