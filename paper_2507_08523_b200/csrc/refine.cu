@@ -258,34 +258,40 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
   if (c.cfg.flags & IL_F_PAIR) {
     // SCAN slots per thread per round, every stamp and template id loaded before any is used
     // (the scan is L2-latency bound: keep the loads in flight together)
-    constexpr uint32_t SCAN = 4;
+    // PMC >= 1 needs the entry's first template in the request's multiset: each round loads
+    // SCAN slots' stamps and first templates together (the scan is L2-latency bound), and only
+    // entries passing that test load the rest of their templates
+    constexpr uint32_t SCAN = 8;
     for (uint32_t s0 = tid; s0 < T; s0 += SCAN * REF_THREADS) {
       uint64_t st[SCAN];
-      uint32_t tt[SCAN][MAXK];
+      uint32_t t0[SCAN];
 #pragma unroll
       for (uint32_t u = 0; u < SCAN; ++u) {
         const uint32_t s = s0 + u * REF_THREADS;
         st[u] = s < T ? c.tab_stamp[s] : 0ull;
-#pragma unroll
-        for (uint32_t j = 0; j < MAXK; ++j) tt[u][j] = (s < T && j < k) ? c.tab_tpl[(size_t)j * T + s] : NONE32;
+        t0[u] = s < T ? c.tab_tpl[s] : NONE32;
       }
 #pragma unroll
       for (uint32_t u = 0; u < SCAN; ++u) {
-        if (st[u] == 0) continue;
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < MAXK; ++q) any |= tc[q] == t0[u];
+        if (st[u] == 0 || !any) continue;              // PMC = 0: never selected
+        const uint32_t s = s0 + u * REF_THREADS;
         uint32_t used = 0, p = 0;
         bool run = true;
 #pragma unroll
         for (uint32_t j = 0; j < MAXK; ++j) {
           if (run && j < k) {                          // (predicated: the loop stays unrolled)
+            const uint32_t tj = j == 0 ? t0[u] : c.tab_tpl[(size_t)j * T + s];
             bool found = false;
 #pragma unroll
             for (int q = 0; q < MAXK; ++q) {
-              if (!found && !((used >> q) & 1u) && tc[q] == tt[u][j]) { used |= 1u << q; found = true; }
+              if (!found && !((used >> q) & 1u) && tc[q] == tj) { used |= 1u << q; found = true; }
             }
             if (!found) run = false; else ++p;
           }
         }
-        const uint32_t s = s0 + u * REF_THREADS;
         if (p > bp || (p == bp && p > 0 && st[u] > bst)) { bp = p; bst = st[u]; bs = s; }
       }
     }
