@@ -57,6 +57,9 @@ __device__ __forceinline__ uint32_t qslot(uint32_t t) { return (t * 0x9E3779B1u)
 // SIM_BIG_POOL demos (no block-wide rounds, most queries per SM), QW = 4 above (4x the lanes per
 // query when the scoring loop dominates).
 constexpr uint32_t SIM_BIG_POOL = 1024;
+#ifndef IL_SIM_QW_SMALL
+#define IL_SIM_QW_SMALL 2
+#endif
 template <int QW>
 __global__ void __launch_bounds__(SIM_THREADS) k_sim_topk(Ctx c, uint32_t B, const uint32_t* __restrict__ q_off,
                                                           const uint32_t* __restrict__ q_tok,
@@ -428,7 +431,8 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   if (c->n_demos > SIM_BIG_POOL)
     k_sim_topk<4><<<cdiv(B, SIM_THREADS / 128), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
   else
-    k_sim_topk<1><<<cdiv(B, SIM_THREADS / 32), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+    k_sim_topk<IL_SIM_QW_SMALL><<<cdiv(B, SIM_THREADS / (32 * IL_SIM_QW_SMALL)), SIM_THREADS, 0, st>>>(
+        *c, B, q_off, q_tok, q_src, topk);
   if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
   k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
