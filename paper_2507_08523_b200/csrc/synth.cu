@@ -18,10 +18,15 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 // the four elements (dims 4e .. 4e+3) of one mix, as two packed bf16 pairs
 __device__ __forceinline__ void synth_quad(uint64_t row_key, uint32_t e, float mul, uint32_t& w0, uint32_t& w1) {
   const uint32_t v = fmix32(((uint32_t)row_key ^ (e * 0x9E3779B9u)) + (uint32_t)(row_key >> 32));
-  float x[4];
+  float f[4], x[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    x[j] = __fmul_rn(__fsub_rn(__uint_as_float(0x3F800000u | (((v >> (8 * j)) & 0xFFu) << 15)), 1.5f), mul);
+  for (int j = 0; j < 4; ++j) f[j] = __uint_as_float(0x3F800000u | (((v >> (8 * j)) & 0xFFu) << 15));
+  // (f - 1.5) * mul on pairs: add.rn / mul.rn f32x2 round exactly like the scalar sub / mul
+#pragma unroll
+  for (int j = 0; j < 4; j += 2)
+    asm("{ .reg .b64 a, c, m; mov.b64 a, {%2, %3}; mov.b64 c, {%4, %4}; add.rn.f32x2 a, a, c;\n\t"
+        "mov.b64 m, {%5, %5}; mul.rn.f32x2 a, a, m; mov.b64 {%0, %1}, a; }"
+        : "=f"(x[j]), "=f"(x[j + 1]) : "f"(f[j]), "f"(f[j + 1]), "f"(-1.5f), "f"(mul));
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w0) : "f"(x[1]), "f"(x[0]));   // low half = dim 4e
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w1) : "f"(x[3]), "f"(x[2]));
 }
