@@ -108,12 +108,17 @@ __global__ void __launch_bounds__(256) k_commit_own(Ctx c, uint32_t B) {
   if (lane == 0 && owned) atomicAdd(&c.sc->resident, owned);
 }
 
-// Tombstone compaction: when live + tombstones exceed 3/4 of the slots, rebuild the table
+// Tombstone compaction: when live + tombstones exceed IL_REBUILD_PCT % of the slots, rebuild the table
 // from the resident pages (one cooperative grid).
+#ifndef IL_REBUILD_PCT
+#define IL_REBUILD_PCT 50
+#endif
 __global__ void __launch_bounds__(512) k_rebuild(Ctx c) {
   cg::grid_group grid = cg::this_grid();
   DevScalars* sc = c.sc;
-  if ((uint64_t)sc->used_slots * 4 <= (uint64_t)c.n_slots * 3) return;   // uniform
+  // (live + tombstones) / slots above IL_REBUILD_PCT % (50 and 75 measure the same at c3): probes
+  // through tombstones grow long before the table fills
+  if ((uint64_t)sc->used_slots * 100 <= (uint64_t)c.n_slots * IL_REBUILD_PCT) return;   // uniform
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (uint32_t s = gtid; s < c.n_slots; s += gs) { c.slot_key[s] = KEY_EMPTY; c.slot_page[s] = NONE32; }
   grid.sync();
@@ -164,21 +169,36 @@ __global__ void __launch_bounds__(256) k_tab_find(Ctx c, uint32_t B) {
   if (i >= B) return;
   const uint32_t k = c.cfg.k;
   const uint32_t rep = c.dd_max[c.tab_slot[i]] - 1;
-  if (lane == 0 && rep != i) {
-    bool eq = true;
-    for (uint32_t q = 0; q < k; ++q) eq &= c.final_ds[(size_t)rep * k + q] == c.final_ds[(size_t)i * k + q];
-    if (!eq) latch(c.sc, IL_ERR_INTERNAL);
+  if (rep != i) {                                      // (warp-uniform) lane q compares entry q
+    const bool ne = lane < k && c.final_ds[(size_t)rep * k + lane] != c.final_ds[(size_t)i * k + lane];
+    if (__any_sync(~0u, ne) && lane == 0) latch(c.sc, IL_ERR_INTERNAL);
   }
   const il_refine_info inf = c.info[i];
   int32_t found = -1;
   if (inf.rule == 1 && !inf.reverted) {
     found = inf.target_slot;
   } else if (inf.reverted) {
-    for (uint32_t sl = lane; sl < c.cfg.table_capacity; sl += 32) {
-      if (c.tab_stamp[sl] == 0) continue;
-      bool eq = true;
-      for (uint32_t q = 0; q < k; ++q) eq &= c.tab_ds[(size_t)sl * k + q] == c.final_ds[(size_t)i * k + q];
-      if (eq) found = (int32_t)sl;
+    // scan for DS_current: 8 slots per lane per round, stamps and first demonstrations loaded
+    // together (the scan is L2-latency bound); only slots whose first demonstration matches
+    // compare the rest
+    const uint32_t T = c.cfg.table_capacity, f0 = c.final_ds[(size_t)i * k];
+    for (uint32_t s0 = lane; s0 < T; s0 += 8 * 32) {
+      uint64_t st[8];
+      uint32_t d0[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        const uint32_t sl = s0 + 32 * u;
+        st[u] = sl < T ? c.tab_stamp[sl] : 0ull;
+        d0[u] = sl < T ? c.tab_ds[(size_t)sl * k] : 0u;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        if (st[u] == 0 || d0[u] != f0) continue;
+        const uint32_t sl = s0 + 32 * u;
+        bool eq = true;
+        for (uint32_t q = 1; q < k; ++q) eq &= c.tab_ds[(size_t)sl * k + q] == c.final_ds[(size_t)i * k + q];
+        if (eq) found = (int32_t)sl;
+      }
     }
     for (int o = 16; o; o >>= 1) found = max(found, __shfl_xor_sync(~0u, found, o));
   }
