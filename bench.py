@@ -420,7 +420,9 @@ def oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn: int, n_step
 
 def cpu_baseline(args, cfg, ds, pool, instr, plan, n_warm, flags):
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; only rank 0 runs the oracle);
+    # set before the oracle library and its OpenMP runtime are first loaded
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     v, t_int, n_int, t_att, n_att = oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags,
                                                   n_attn=max(1, args.cpu_baseline_attn // args.cpu_baseline_batches),
                                                   n_steps=args.cpu_baseline_batches)
@@ -451,7 +453,9 @@ def run_reference(args, rank, world):
     plan = plan_batches(cfg, W + K, 0, 1)
     n_ramp = len(plan) - (W + K)
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; only rank 0 runs the oracle);
+    # set before the oracle library and its OpenMP runtime are first loaded
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     o = O.Oracle(cfg.k, cfg.T, cfg.C, flags=flags)
     o.pool_load(pool, instr)
     rng = np.random.default_rng(0)
