@@ -381,7 +381,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "wall_s_timed": wall,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:        # (the contract: rank 0 at N = 1 only)
         line["cpu_baseline"] = cpu_baseline(args, cfg, ds, pool, instr, plan, n_ramp + W, flags)
     print(json.dumps(line), flush=True)
 
