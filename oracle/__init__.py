@@ -65,6 +65,8 @@ def lib():
         _lib.or_table_put.argtypes = [P, u32p, C.c_uint64]
         _lib.or_refine_one.argtypes = [P, u32p, u32p, i32p, u64p]
         _lib.or_render.argtypes = [P, u32p, u32p, C.c_uint32, u32p, u32p]
+        _lib.or_mix64.restype = C.c_uint64
+        _lib.or_mix64.argtypes = [C.c_uint64]
         _lib.or_chain_hash.argtypes = [C.c_uint64, u32p, C.c_uint32, u64p]
         _lib.or_lookup.restype = C.c_uint32
         _lib.or_lookup.argtypes = [P, u32p, C.c_uint32, C.c_uint32]
@@ -227,6 +229,10 @@ def similarity(metric: int, a, b):
 def pmc(cur_tpl, entry_tpl) -> int:
     c, e = _u32(cur_tpl), _u32(entry_tpl)
     return int(lib().or_pmc(len(c), _p(c, C.c_uint32), _p(e, C.c_uint32)))
+
+
+def mix64(x: int) -> int:
+    return int(lib().or_mix64(x & 0xFFFFFFFFFFFFFFFF))
 
 
 def chain_hash(tok, seed: int = 0) -> np.ndarray:

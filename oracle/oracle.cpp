@@ -499,6 +499,8 @@ void or_render(const or_state* s, const u32* ds, const u32* q, u32 nq, u32* out,
   *len = (u32)p.size();
 }
 
+u64 or_mix64(u64 x) { return mix64(x); }
+
 void or_chain_hash(u64 seed, const u32* tok, u32 n, u64* out) {
   std::vector<u32> v(tok, tok + n);
   std::vector<u64> H = chain_hashes(seed, v);

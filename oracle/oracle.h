@@ -76,6 +76,8 @@ void or_table_put(or_state*, const uint32_t* ds, uint64_t stamp);
 /* refine one DS against the current table (no commit): returns pmc; out final_ds, info[4], *target_stamp */
 int or_refine_one(or_state*, const uint32_t* cur_ds, uint32_t* final_ds, int32_t* info, uint64_t* target_stamp);
 void or_render(const or_state*, const uint32_t* ds, const uint32_t* q, uint32_t nq, uint32_t* out, uint32_t* len);
+/* the splitmix64 finaliser the chain hash is built from (Z17); pinned to published splitmix64 outputs */
+uint64_t or_mix64(uint64_t x);
 void or_chain_hash(uint64_t hash_seed, const uint32_t* tok, uint32_t n, uint64_t* out /* [n/16] */);
 /* kv_sim-style sequential lookup / insert, B = 1 semantics */
 uint32_t or_lookup(or_state*, const uint32_t* tok, uint32_t n, uint32_t capped);

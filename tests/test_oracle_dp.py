@@ -8,7 +8,8 @@ What fixes it independently of the implementation:
   - the replicated tables stay identical on every rank;
   - a rank's index only ever holds blocks of prompts that rank processed, and a request's hits
     are a prefix of its own block chain that is resident in its rank's index;
-  - with G = 1 the procedure is the one-GPU procedure (same outputs as or_run_batch).
+  - with one request per rank per batch, each rank's index is SPEC's sequential kv_sim over
+    that rank's prompts.
 """
 import numpy as np
 import pytest
@@ -90,16 +91,21 @@ def test_dp_rank_index_holds_only_its_own_blocks_and_hits_are_resident_prefixes(
             prev_index[g] = hashes
 
 
-def test_dp_one_rank_is_the_one_gpu_procedure():
-    sp = StreamSpec(B=64, n_logs=600)
+@pytest.mark.parametrize("G", [2, 4])
+def test_dp_one_request_per_rank_is_sequential_kv_sim_per_rank(G):
+    """With one request per rank per batch (B = G) and an unbounded cache, each rank's prefix
+    index is SPEC's sequential kv_sim over the prompts that rank processed: the hit
+    of every request equals lookup (capped, Z20) then insert on a per-rank sequential oracle, and
+    the resident sets agree.  Independent of run_batch_dp's own code path (or_lookup/or_insert)."""
+    sp = StreamSpec(B=G, n_logs=600, C=1 << 20)
     ds, pool, instr = make_stream(sp)
-    a = _ranks(sp, pool, instr, 1)[0]
-    c = _ranks(sp, pool, instr, 1)[0]
-    sp.n_batches = 5
-    for start, B in batch_plan(sp, ds.n):
-        batch = gen.make_batch(ds, start, B)
-        ra = a.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=sp.max_prompt_tokens // 16)
-        rc = O.Oracle.run_batch_dp([c], batch, prompt_stride=sp.max_prompt_tokens,
-                                   max_blocks=sp.max_prompt_tokens // 16)
-        for f in ("topk", "final_ds", "info", "hit", "prompt_len", "evicted"):
-            np.testing.assert_array_equal(getattr(ra, f), getattr(rc, f))
+    ranks = _ranks(sp, pool, instr, G)
+    seq = _ranks(sp, pool, instr, G)
+    for b in range(60):
+        r = O.Oracle.run_batch_dp(ranks, gen.make_batch(ds, b * G, G), prompt_stride=sp.max_prompt_tokens,
+                                  max_blocks=sp.max_prompt_tokens // 16)
+        for g in range(G):
+            p = r.prompt(g)
+            assert seq[g].lookup(p, capped=True) == int(r.hit[g]), (b, g)
+            seq[g].insert(p)
+            assert (ranks[g].index_dump()[0] == seq[g].index_dump()[0]).all(), (b, g)

@@ -513,3 +513,118 @@ def test_batch_invariants_and_resident_set():
     for r in res:
         rev = r.info[:, 2] == 1
         assert (r.final_ds[rev] == r.topk[rev]).all()
+
+
+# ------------------------------------------------------------------ mix64 (Z17) vs published splitmix64
+def test_mix64_published_splitmix64_outputs():
+    """Z17 builds the chain hash from the splitmix64 finaliser.  splitmix64 (state += 0x9E3779B97F4A7C15,
+    output = finaliser(state)) has published reference outputs: state 0 -> 0xE220A8397B1DCDAF first,
+    and seed 1234567 -> 6457827717110365317, 3203168211198807973, 9817491932198370423,
+    4593380528125082431, 16408922859458223821 (the generator's standard test vector).  A transposed
+    shift or multiplier constant in the oracle's mix64 fails this."""
+    g, M = 0x9E3779B97F4A7C15, (1 << 64) - 1
+    assert O.mix64(g) == 0xE220A8397B1DCDAF
+    st, out = 1234567, []
+    for _ in range(5):
+        st = (st + g) & M
+        out.append(O.mix64(st))
+    assert out == [6457827717110365317, 3203168211198807973, 9817491932198370423,
+                   4593380528125082431, 16408922859458223821]
+    assert O.mix64(0) == 0                                             # the finaliser fixes 0
+
+
+# ------------------------------------------------------------------ batch procedure at B = 1 (Z1, Z21)
+def _hdfs_stream(n_logs=600, M=60, k=3, n_instr=40):
+    ds_ = gen.make_dataset("HDFS", n_logs, 14, 1.3, 1004)
+    pool = gen.sample_pool(ds_, M, 2004)
+    return ds_, pool, gen.instruction(n_instr, 0)
+
+
+def test_batch1_run_batch_equals_sequential_lookup_insert():
+    """c.4 "B = 1 == sequential SPEC refine + insert", prefix-cache half: with an
+    unbounded cache, run_batch at B = 1 gives, request by request, the hit count SPEC's sequential
+    kv_sim gives (lookup of the prompt, capped per Z20, then insert of the prompt), and both leave
+    the same set of resident blocks."""
+    ds_, pool, instr = _hdfs_stream()
+    a = O.Oracle(k=3, table_capacity=24, kv_pages=1 << 20, flags=O.F_PAIR | O.F_VERIFY)
+    seq = O.Oracle(k=3, table_capacity=24, kv_pages=1 << 20, flags=O.F_PAIR | O.F_VERIFY)
+    a.pool_load(pool, instr); seq.pool_load(pool, instr)
+    for r in range(250):
+        res = a.run_batch(gen.make_batch(ds_, r, 1))
+        p = res.prompt(0)
+        assert seq.lookup(p, capped=True) == int(res.hit[0]), r
+        seq.insert(p)
+        assert (np.sort(a.index_dump()[0]) == np.sort(seq.index_dump()[0])).all(), r
+
+
+class _Z21Model:
+    """Literal reading Z21 + Z1 + Z22 over a plain dict:
+    hash -> [stamp, depth, parent, tokens].  Stamps are (batch << 32 | admission index)."""
+
+    def __init__(self, C, root):
+        self.C, self.root, self.res, self.b = C, root, {}, 0
+
+    def hits(self, prompt, H):
+        prev, h = self.root, 0
+        for j, x in enumerate(H):
+            e = self.res.get(x)
+            if e is None or e[2] != prev or tuple(prompt[16 * j:16 * j + 16]) != e[3]:
+                break
+            h, prev = h + 1, x
+        return min(h, max(len(prompt) - 1, 0) // 16)
+
+    def batch(self, prompts, Hs):
+        self.b += 1
+        h = [self.hits(p, H) for p, H in zip(prompts, Hs)]            # snapshot (Z1)
+        pinned = {Hs[i][j] for i in range(len(prompts)) for j in range(h[i])}
+        for i in range(len(prompts)):                                   # touch in admission order
+            for j in range(h[i]):
+                self.res[Hs[i][j]][0] = (self.b << 32) | i
+        need = sum((len(p) + 15) // 16 - h[i] for i, p in enumerate(prompts))
+        free = self.C - len(self.res)
+        victims = []
+        if need > free:                                                 # LRU: (stamp, -depth, hash)
+            order = sorted((e[0], -e[1], x) for x, e in self.res.items() if x not in pinned)
+            victims = [x for _, _, x in order[:need - free]]
+            for x in victims:
+                del self.res[x]
+        for i, p in enumerate(prompts):                                 # insert, first wins (Z22)
+            for j in range(h[i], len(Hs[i])):
+                x = Hs[i][j]
+                if x in self.res:
+                    self.res[x][0] = max(self.res[x][0], (self.b << 32) | i)
+                else:
+                    par = self.root if j == 0 else Hs[i][j - 1]
+                    self.res[x] = [(self.b << 32) | i, j, par, tuple(p[16 * j:16 * j + 16])]
+        return h, victims
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_small_cache_stream_matches_literal_z21_lru(B):
+    """Z21 with a small cache (C = 48 pages, every batch evicts): the oracle's hits, exact victim
+    lists (in eviction order) and resident blocks with their stamps, depths and parents equal a
+    literal LRU model keyed by (stamp, -depth, hash)."""
+    ds_, pool, instr = _hdfs_stream(n_instr=24)
+    C = 48
+    o = O.Oracle(k=3, table_capacity=16, kv_pages=C, flags=O.F_PAIR | O.F_VERIFY)
+    o.pool_load(pool, instr)
+    probe = O.Oracle(k=1, table_capacity=4, kv_pages=4)              # ROOT = parent of a depth-0 block
+    probe.pool_load(_pool_from_token_lists([[20]]), gen.instruction(4, 0))
+    probe.insert(np.arange(16, dtype=np.uint32) + 100)
+    m = _Z21Model(C, int(probe.index_dump()[3][0]))
+    n_evicting = 0
+    for b in range(120):
+        res = o.run_batch(gen.make_batch(ds_, b * B, B))
+        prompts = [tuple(int(t) for t in res.prompt(i)) for i in range(B)]
+        Hs = [[int(x) for x in res.block_hash[i, :len(prompts[i]) // 16]] for i in range(B)]
+        h, victims = m.batch(prompts, Hs)
+        assert [int(x) for x in res.hit] == h, b
+        assert [int(x) for x in res.evicted] == victims, b
+        n_evicting += bool(victims)
+        hh, st, dp, par = o.index_dump()
+        want = sorted(m.res.items())
+        assert [int(x) for x in hh] == [x for x, _ in want], b
+        assert [int(x) for x in st] == [e[0] for _, e in want], b
+        assert [int(x) for x in dp] == [e[1] for _, e in want], b
+        assert [int(x) for x in par] == [e[2] for _, e in want], b
+    assert n_evicting >= 40
