@@ -49,6 +49,17 @@ def ncu_traffic():
     return None, None
 
 
+# Steady state: after the cold-start ramp, untimed full batches run until the KV cache is full and
+# a batch evicts (LRU, Z21), so every warm-up and timed step runs in the eviction regime.  At most
+# this many fill batches (c3 starts evicting after ~70).
+MAX_FILL = {1: 400, 2: 200, 3: 200, 4: 200, 5: 200}
+
+
+def n_queries_for(cfg, args, world: int) -> int:
+    """Stream length both arms use (the same dataset instance): ramp + fill + warm-up + timed."""
+    return (MAX_FILL[args.config] + args.warmup + 2 * args.steps + 1) * cfg.B * world + 65 * world
+
+
 def workload(cfg_n: int, rank: int, world: int, n_queries: int = 0):
     """Config dataset, grown (same generator, same seed) to at least n_queries logs so that no
     query repeats inside the run: the paper parses every log once."""
@@ -120,6 +131,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def config_dict(cfg, args, world, ds):
+    """The `config` of the JSON line; both arms print the same one."""
+    return {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
+            "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
+            "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
+            "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
+            "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards)",
+            "stream": f"{ds.n} distinct logs, no query repeats within the run",
+            "steady_state": "LRU eviction in every timed step" if not args.no_fill else "no fill",
+            "int_dtype": "u32/u64 bit-exact", "attn": "bf16 in, fp32 accumulate"}
+
+
 # ---------------------------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -129,8 +152,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg0 = gen.config(args.config)
-    cfg, ds, pool, instr = workload(args.config, rank, world,
-                                    n_queries=(args.warmup + 2 * args.steps + 1) * cfg0.B * world + 65 * world)
+    cfg, ds, pool, instr = workload(args.config, rank, world, n_queries=n_queries_for(cfg0, args, world))
     flags = IL_F_PAIR | IL_F_VERIFY | (IL_F_GUARD if not args.no_guard else 0)
     if args.naive:
         flags = IL_F_VERIFY
@@ -152,9 +174,9 @@ def run_ours(args, rank, world, local_rank):
     commit = dp.commit if dp else pl.commit
     step = dp.step if dp else pl.step
     K, W = args.steps, args.warmup
-    plan = plan_batches(cfg, W + 2 * K, rank, world)
-    n_ramp = len(plan) - (W + 2 * K)
-    batches = [gen.make_batch(ds, s, b) for s, b in plan]
+    n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
+    plan = plan_batches(cfg, n_fill_max + W + 2 * K, rank, world)
+    n_ramp = len(plan) - (n_fill_max + W + 2 * K)
 
     def to_dev(bt):
         return (torch.from_numpy(bt.q_off.view(np.int32)).to(dev), torch.from_numpy(bt.q_tok.view(np.int32)).to(dev),
@@ -163,11 +185,35 @@ def run_ours(args, rank, world, local_rank):
     def to_pinned(bt):
         return tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src)) + (bt.B,)
 
+    def set_inputs(x):
+        pl.load_inputs(*x)                             # device-to-device into the resident input buffers
+
+    # ---- cold-start ramp, then fill until a batch evicts (untimed; all ranks stop together)
+    stats_dev = torch.zeros(64, dtype=torch.uint8, device=dev)
+    j = 0
+    with torch.cuda.stream(stream):
+        for j in range(n_ramp + n_fill_max):
+            set_inputs(to_dev(gen.make_batch(ds, *plan[j])))
+            step()
+            if j < n_ramp:
+                continue
+            pl.ctx.stats_async(stats_dev, stream=stream)
+            ev_now = pl.ctx.stats_from_bytes(stats_dev.cpu().numpy())["evicted_blocks"]
+            flag = torch.tensor([1 if ev_now > 0 else 0], device=dev)
+            if world > 1:
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            if int(flag.item()):
+                break
+    n_fill = j + 1 - n_ramp if n_fill_max else 0
+    plan = plan[:n_ramp + n_fill] + plan[n_ramp + n_fill_max:]
+    stream.synchronize()
+    batches = [gen.make_batch(ds, s, b) for s, b in plan[n_ramp + n_fill:]]
+
     # Timed steps alternate: even = device-timed (inputs already resident in HBM), odd = end to
     # end (pinned host inputs copied in, refined DS / info / hits copied out inside the timed
     # region), so both see the same part of the stream.
-    warm_in = [to_dev(bt) for bt in batches[:n_ramp + W]]
-    timed = batches[n_ramp + W:]
+    warm_in = [to_dev(bt) for bt in batches[:W]]
+    timed = batches[W:]
     dev_in = [to_dev(bt) if j % 2 == 0 else None for j, bt in enumerate(timed)]
     host_in = [to_pinned(bt) if j % 2 == 1 else None for j, bt in enumerate(timed)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -180,11 +226,9 @@ def run_ours(args, rank, world, local_rank):
     rec_hit = torch.zeros(K, cfg.B, dtype=torch.int32, device=dev)
     rec_bt = torch.zeros(K, cfg.B, ccfg.max_blocks, dtype=torch.int32, device=dev)
     rec_info = torch.zeros(K, cfg.B, 16, dtype=torch.uint8, device=dev)
+    rec_stats = torch.zeros(2 * K, 64, dtype=torch.uint8, device=dev)   # il_stats after every timed step
 
-    def set_inputs(x):
-        pl.load_inputs(*x)                             # device-to-device into the resident buffers
-
-    # ---- warm-up (cold-start ramp + W full steps), not timed
+    # ---- warm-up (W full steps in the eviction regime), not timed
     with torch.cuda.stream(stream):
         for x in warm_in:
             set_inputs(x)
@@ -240,6 +284,7 @@ def run_ours(args, rank, world, local_rank):
                     e[i].record(stream)
                     run_stage(n)
                 e[5].record(stream)
+                pl.ctx.stats_async(rec_stats[j], stream=stream)
                 evs.append(e)
                 B = dev_in[j][3]
                 rec_len[j // 2, :B].copy_(pl.prompt_len[:B]); rec_hit[j // 2, :B].copy_(pl.hit[:B])
@@ -258,6 +303,7 @@ def run_ours(args, rank, world, local_rank):
                 out_hit[:B].copy_(pl.hit[:B], non_blocking=True)
                 out_info[:B].copy_(pl.info[:B], non_blocking=True)
                 e1.record(stream)
+                pl.ctx.stats_async(rec_stats[j], stream=stream)
                 e2e_evs.append((e0, e1))
                 h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
                 d2h = 4 * B * cfg.k + 4 * B + 16 * B
@@ -273,9 +319,11 @@ def run_ours(args, rank, world, local_rank):
                   file=sys.stderr)
             prev = e.time_range.end
     clk = clocks.stop()
-    launches = pl.launches() - launches0
+    launches = pl.launches() - launches0 - 2 * K      # minus the per-step k_stats (accounting, not the path)
     if graphs is not None:                             # replays do not pass through the host counter
         launches += per_step_launches * 2 * K
+    st_steps = [pl.ctx.stats_from_bytes(r) for r in rec_stats.cpu().numpy()]
+    evicted = [s_["evicted_blocks"] for s_ in st_steps]
     pl.ctx.status_sync(stream)
     if world > 1:
         dist.barrier()
@@ -349,13 +397,14 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": B_all / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
-                   "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
-                   "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
-                   "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
-                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards" + (f"; ICL records all-gathered per batch, {dist.get_backend()})" if world > 1 else ")"),
-                   "stream": f"{ds.n} distinct logs, no query repeats within the run",
-                   "int_dtype": "u32/u64 bit-exact", "attn": "bf16 in, fp32 accumulate"},
+        "config": config_dict(cfg, args, world, ds),
+        "steady_state": {"ramp_batches": n_ramp, "fill_batches": n_fill,
+                         "evicted_blocks_per_step": {"mean": float(np.mean(evicted)), "min": int(np.min(evicted)),
+                                                     "max": int(np.max(evicted))},
+                         "evicting_steps": f"{sum(1 for x in evicted if x > 0)}/{len(evicted)}",
+                         "resident_blocks": int(st_steps[-1]["resident_blocks"]),
+                         "note": "untimed full batches after the ramp until the KV cache is full and a batch "
+                                 "evicts; every timed step then runs LRU eviction (rank 0's counts)"},
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
         "prefix_hit_pct_tokens": 100.0 * hit_tok / max(all_tok, 1),
         "pair": {"rule_counts": {"1_target": int(rules[1]), "2_unchanged": int(rules[2]), "3_modified": int(rules[3])},
@@ -382,7 +431,7 @@ def run_ours(args, rank, world, local_rank):
         "wall_s_timed": wall,
     }
     if not args.no_cpu_baseline and world == 1:        # (the contract: rank 0 at N = 1 only)
-        line["cpu_baseline"] = cpu_baseline(args, cfg, ds, pool, instr, plan, n_ramp + W, flags)
+        line["cpu_baseline"] = cpu_baseline(args, cfg, ds, pool, instr, plan, n_ramp + n_fill + W, flags)
     print(json.dumps(line), flush=True)
 
 
@@ -443,31 +492,73 @@ def cpu_model():
 
 
 def run_reference(args, rank, world):
+    """The CPU oracle on the GPU arm's workload: the same dataset instance, the same global batches
+    in the same order (ramp, fill until the first evicting batch, warm-up, then the 2K batches
+    the GPU arm alternates over), the same procedure (run_batch_dp over `world` oracle ranks =
+    the GPU arm's request shards).  A timed step = the integer path of one whole global batch
+    (the one the GPU arm device-times at that step) + fp64 attention of a random sample of its
+    requests; ms_per_step is that measured time.  value = requests/s from the measured
+    per-request costs (integer path per request + attention per sampled request): "sampled"."""
     if rank != 0:
         return
     cfg0 = gen.config(args.config)
-    cfg, ds, pool, instr = workload(args.config, 0, 1, n_queries=(args.warmup + args.steps + 1) * cfg0.B + 65)
+    cfg, ds, pool, instr = workload(args.config, 0, world, n_queries=n_queries_for(cfg0, args, world))
     import oracle as O
-    flags = O.F_PAIR | O.F_VERIFY | (0 if args.no_guard else O.F_GUARD)
+    flags = O.F_VERIFY if args.naive else (O.F_PAIR | O.F_VERIFY | (0 if args.no_guard else O.F_GUARD))
     K, W = args.steps, args.warmup
-    plan = plan_batches(cfg, W + K, 0, 1)
-    n_ramp = len(plan) - (W + K)
+    n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
+    plans = [plan_batches(cfg, n_fill_max + W + 2 * K, r, world) for r in range(world)]
+    n_ramp = len(plans[0]) - (n_fill_max + W + 2 * K)
     cores = len(os.sched_getaffinity(0))
     # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; only rank 0 runs the oracle);
     # set before the oracle library and its OpenMP runtime are first loaded
     os.environ["OMP_NUM_THREADS"] = str(cores)
-    o = O.Oracle(cfg.k, cfg.T, cfg.C, flags=flags)
-    o.pool_load(pool, instr)
+    ranks = []
+    for _ in range(world):
+        o = O.Oracle(cfg.k, cfg.T, cfg.C, flags=flags)
+        o.pool_load(pool, instr)
+        ranks.append(o)
+
+    def global_batch(j):
+        parts = [gen.make_batch(ds, *plans[r][j]) for r in range(world)]
+        if world == 1:
+            return parts[0]
+        q_off = np.concatenate([[0], np.cumsum(np.concatenate([np.diff(p.q_off.astype(np.int64)) for p in parts]))])
+        return gen.Batch(q_off.astype(np.uint32), np.concatenate([p.q_tok for p in parts]),
+                         np.concatenate([p.q_src for p in parts]))
+
+    def run(j):
+        bt = global_batch(j)
+        kw = dict(prompt_stride=cfg.max_prompt_tokens, max_blocks=cfg.max_prompt_tokens // 16)
+        r = ranks[0].run_batch(bt, **kw) if world == 1 else O.Oracle.run_batch_dp(ranks, bt, **kw)
+        return bt, r
+
+    t_prep = time.perf_counter()
+    j, n_fill = 0, 0
+    while j < n_ramp + n_fill_max:                      # ramp + fill, untimed
+        _, r = run(j)
+        j += 1
+        if j > n_ramp and len(r.evicted) > 0:
+            break
+    n_fill = j - n_ramp if n_fill_max else 0
+    order = list(range(n_ramp + n_fill_max, n_ramp + n_fill_max + W + 2 * K))
+    for jj in order[:W]:
+        run(jj)
+    t_prep = time.perf_counter() - t_prep
     rng = np.random.default_rng(0)
-    per_req = []
-    for j, (s, b) in enumerate(plan):
-        t0 = time.perf_counter()
-        r = o.run_batch(gen.make_batch(ds, s, b), prompt_stride=cfg.max_prompt_tokens, max_blocks=cfg.max_prompt_tokens // 16)
-        t_int = time.perf_counter() - t0
-        if j < n_ramp + W:
+    steps_ms, per_req = [], []
+    n_att_tot = 0
+    for step in range(2 * K):
+        jj = order[W + step]
+        if step % 2 == 1:                                 # the GPU arm's e2e steps: keep the state in step
+            run(jj)
             continue
+        t0 = time.perf_counter()
+        bt, r = run(jj)
+        t_int = time.perf_counter() - t0
+        Bg = bt.B
         t_att, n_att = 0.0, 0
-        for i in rng.choice(b, size=min(args.cpu_attn_sample, b), replace=False):
+        for i in rng.choice(Bg, size=min(args.cpu_attn_sample, Bg), replace=False):
             L, P = int(r.prompt_len[i]), 16 * int(r.hit[i])
             toks, pos = r.prompt(i), np.arange(L)
             q = gen.bf16_bits_to_f64(gen.synth_bf16_bits(cfg.qkv_seed, "q", toks[P:], pos[P:], cfg.Hq, cfg.d))
@@ -477,19 +568,23 @@ def run_reference(args, rank, world):
             O.attention(q, kk, vv, P=P, scale=cfg.d ** -0.5)
             t_att += time.perf_counter() - t1
             n_att += 1
-        per_req.append(t_int / b + t_att / max(n_att, 1))
+        n_att_tot += n_att
+        steps_ms.append(1e3 * (time.perf_counter() - t0))
+        per_req.append(t_int / Bg + t_att / max(n_att, 1))
     v = 1.0 / float(np.mean(per_req))
-    ms = 1e3 * cfg.B / v
+    sample = (f"per step: integer path of the whole global batch of {cfg.B * world} requests (the batch the GPU "
+              f"arm device-times at that step) + fp64 attention of {args.cpu_attn_sample} sampled requests; "
+              f"requests/s = 1 / (integer time per request + attention time per sampled request) [sampled]; "
+              f"{n_ramp} ramp + {n_fill} fill + {W} warm-up batches replayed untimed first ({t_prep:.1f} s)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
-                   "requests_per_gpu_per_step": cfg.B},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"per step: integer path of one full batch of {cfg.B} requests + fp64 attention of "
-                                   f"{args.cpu_attn_sample} sampled requests; requests/s = 1 / mean per-request time",
+        "ms_per_step": float(np.mean(steps_ms)), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, args, world, ds),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                          "cpu": cpu_model()},
+        "sampled": {"requests_per_step_integer": cfg.B * world, "requests_per_step_attention": args.cpu_attn_sample,
+                    "attention_requests_timed": n_att_tot},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -505,7 +600,8 @@ def main():
     ap.add_argument("--naive", action="store_true", help="PAIR off (naive prefix caching)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
-    ap.add_argument("--cpu-attn-sample", type=int, default=8, help="--impl reference: fp64 attention requests per step")
+    ap.add_argument("--no-fill", action="store_true", help="time right after the ramp (cache not yet full)")
+    ap.add_argument("--cpu-attn-sample", type=int, default=32, help="--impl reference: fp64 attention requests per step")
     ap.add_argument("--cpu-baseline-attn", type=int, default=400, help="cpu_baseline: fp64 attention requests sampled")
     ap.add_argument("--cpu-baseline-batches", type=int, default=4, help="cpu_baseline: full batches of the integer path")
     args = ap.parse_args()

@@ -115,6 +115,10 @@ il_status il_create(const il_config* cfg_h, void* workspace, size_t bytes, il_st
 il_status il_destroy(il_ctx* ctx);
 il_status il_status_sync(il_ctx* ctx, il_stream s);      /* sync s, return + clear latched status */
 il_status il_stats_sync(il_ctx* ctx, il_stream s, il_stats* out_h);
+/* The same counters written to DEVICE memory by a kernel on s (no sync; capturable in a CUDA
+ * graph): per-batch accounting inside a timed loop.  out_d: one il_stats, 8-byte aligned;
+ * `launches` holds the host counter at the time of the call (at capture, for a graph). */
+il_status il_stats_async(il_ctx* ctx, il_stats* out_d, il_stream s);
 const char* il_last_error(void);                          /* thread-local */
 
 /* ---- il_pool_load: the candidate set ("samples 200 logs ... to construct the
@@ -122,7 +126,9 @@ const char* il_last_error(void);                          /* thread-local */
  * interned template ids, dataset row (for IL_F_EXCLUDE_SELF), and the common
  * instruction.  Builds the per-demo token sets (a1) and rendered demos (a5), and
  * resets the ICL Table and the prefix index (demo ids change meaning).  The input buffers
- * may be freed once the stream reaches this call. */
+ * may be freed once the stream reaches this call.  IL_ERR_ARG if n_demos is outside
+ * [k, max_pool], the pool exceeds max_pool_tokens, or n_instr exceeds max_prompt_tokens or
+ * 16,384 tokens (1,024 instruction blocks, the per-batch instruction pin covers no more). */
 il_status il_pool_load(il_ctx* ctx, uint32_t n_demos,
                        const uint32_t* log_off, const uint32_t* log_tok,
                        const uint32_t* tpl_off, const uint32_t* tpl_tok,
@@ -171,8 +177,8 @@ il_status il_prefix_match(il_ctx* ctx, uint32_t B,
  *   k_new, v_new  [max_suffix_tokens][Hkv][d] bf16
  *   k_pages, v_pages  [C][Hkv][16][d] bf16, caller-owned, persistent across batches
  * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27).
- * Runs on the tcgen05/TMA kernel for head_dim 64 or 128 and Hq/Hkv in 1..8 (else the CUDA-core
- * kernel).  Requires a preceding il_prefix_match of the same batch (IL_ERR_STATE otherwise);
+ * Runs on the tcgen05/TMA kernel (head_dim 64 or 128, Hq/Hkv in 1..8; il_create rejects any
+ * other shape with IL_ERR_ARG, there is no other attention kernel).  Requires a preceding il_prefix_match of the same batch (IL_ERR_STATE otherwise);
  * out and the workspace hold the cascade's partial between its two launches, so out must not be
  * read before the call's work completes on stream s. */
 il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,

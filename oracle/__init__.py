@@ -253,3 +253,31 @@ def attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, P: int, scale: float,
     lib().or_attention(Hq, Hkv, d, L, P, _p(q, C.c_double), _p(k, C.c_double), _p(v, C.c_double),
                        scale, _p(out, C.c_double), _p(lse, C.c_double))
     return (out, lse) if want_lse else out
+
+
+def attention_np(q: np.ndarray, k: np.ndarray, v: np.ndarray, P: int, scale: float,
+                 want_lse: bool = False):
+    """The same definition as attention() written with fp64 numpy
+    matmuls as library steps, for checking every row of large batches in seconds:
+        logits[h, s, j] = (q[s, h] . k[j, h // g]) * scale   for j <= P + s (causal), else -inf
+        out[s, h] = sum_j softmax_j(logits[h, s, :]) v[j, h // g];  lse = log sum_j exp(logits)
+    with the row max subtracted before exp.  No blocking or reordering beyond the definition;
+    pinned to the same closed forms as attention() and to it (tests/test_oracle_attention.py)."""
+    q = np.asarray(q, np.float64); k = np.asarray(k, np.float64); v = np.asarray(v, np.float64)
+    S, Hq, d = q.shape
+    L, Hkv, _ = k.shape
+    assert S == L - P
+    g = Hq // Hkv
+    qh = q.reshape(S, Hkv, g, d).transpose(1, 2, 0, 3).reshape(Hkv, g * S, d)     # rows (hh, s)
+    logits = np.matmul(qh, k.transpose(1, 2, 0)) * scale                        # [Hkv][g*S][L]
+    pos = np.tile(np.arange(S), g) + P
+    logits = np.where(np.arange(L)[None, None, :] <= pos[None, :, None], logits, -np.inf)
+    mx = logits.max(-1, keepdims=True)
+    w = np.exp(logits - mx)
+    den = w.sum(-1, keepdims=True)
+    o = np.matmul(w / den, v.transpose(1, 0, 2))                                # [Hkv][g*S][d]
+    out = o.reshape(Hkv, g, S, d).transpose(2, 0, 1, 3).reshape(S, Hq, d)
+    if not want_lse:
+        return out
+    lse = (mx + np.log(den))[..., 0].reshape(Hkv, g, S).transpose(2, 0, 1).reshape(S, Hq)
+    return out, lse

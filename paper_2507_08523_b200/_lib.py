@@ -21,7 +21,7 @@ IL_SIM_COSINE, IL_SIM_JACCARD = 0, 1
 IL_F_PAIR, IL_F_GUARD, IL_F_EXCLUDE_SELF, IL_F_VERIFY = 1, 2, 4, 8
 
 # every symbol include/il.h declares (checked by tests/test_abi.py)
-EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "il_stats_sync",
+EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "il_stats_sync", "il_stats_async",
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
            "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
            "il_table_dump", "il_evicted_dump"]
@@ -55,6 +55,7 @@ class il_stats(C.Structure):
 
 
 assert C.sizeof(il_refine_info) == 16
+assert C.sizeof(il_stats) == 48
 
 
 _lib = None
@@ -75,6 +76,7 @@ def load():
         "il_destroy": [P],
         "il_status_sync": [P, P],
         "il_stats_sync": [P, P, C.POINTER(il_stats)],
+        "il_stats_async": [P, P, P],
         "il_pool_load": [P, U32, P, P, P, P, P, P, P, U32, P],
         "il_refine_batch": [P, U32, P, P, P, P, P, P, P, P, P],
         "il_prefix_match": [P, U32, P, P, P, P, P, P, P, P],

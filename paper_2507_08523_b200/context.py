@@ -129,6 +129,15 @@ class Context:
         L.check(self.lib.il_stats_sync(self.h, _stream(stream), C.byref(st)), "il_stats_sync")
         return {f: getattr(st, f) for f, _ in L.il_stats._fields_}
 
+    def stats_async(self, out: torch.Tensor, stream=None):
+        """il_stats written by a kernel into `out` (a device tensor of >= 48 bytes; no sync)."""
+        L.check(self.lib.il_stats_async(self.h, _p(out), _stream(stream)), "il_stats_async")
+
+    @staticmethod
+    def stats_from_bytes(raw: np.ndarray) -> dict:
+        st = L.il_stats.from_buffer_copy(np.ascontiguousarray(raw, np.uint8).tobytes()[:C.sizeof(L.il_stats)])
+        return {f: getattr(st, f) for f, _ in L.il_stats._fields_}
+
     def index_dump(self, stream=None):
         n = self.cfg.kv_pages
         h = np.zeros(n, np.uint64); s = np.zeros(n, np.uint64); d = np.zeros(n, np.uint32)

@@ -926,13 +926,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static inline bool attn_sm100_supported(const Ctx* c) {
-  const char* e = getenv("IL_ATTN");
-  if (e && e[0] == 's') return false;                 // IL_ATTN=simple: bring-up kernel (cross-checks)
-  const uint32_t g = c->cfg.n_q_heads / c->cfg.n_kv_heads;
-  return (c->cfg.head_dim == 128 || c->cfg.head_dim == 64) && g >= 1 && g <= 8;
-}
-
 static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
                                           const int32_t* block_table, const il_bf16* q, il_bf16* k_pages,
                                           il_bf16* v_pages, il_bf16* out, float* lse, float scale, cudaStream_t st) {
@@ -966,12 +959,6 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
   k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
-  static bool attr = false;
-  if (!attr) {
-    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(128)));
-    IL_CUDA(cudaFuncSetAttribute(k_attn_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(64)));
-    attr = true;
-  }
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
     if (phase == 1 && !cascade) break;
     if (D == 128)

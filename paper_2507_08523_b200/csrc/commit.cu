@@ -368,15 +368,9 @@ static il_status commit_index(Ctx* c, cudaStream_t st, uint64_t b_cur) {
     k_commit_insert<<<g, 256, 0, st>>>(*c, B, b_cur);
     k_commit_own<<<g, 256, 0, st>>>(*c, B);
   }
-  static int rb_blocks = -1;
-  if (rb_blocks < 0) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0);
-    rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
-  }
   Ctx cc = *c;
   void* args[] = {&cc};
-  IL_CUDA(cudaLaunchCooperativeKernel((void*)k_rebuild, dim3(rb_blocks), dim3(512), args, 0, st));
+  IL_CUDA(cudaLaunchCooperativeKernel((void*)k_rebuild, dim3(c->rb_blocks), dim3(512), args, 0, st));
   IL_LAUNCH_CHECK("il_commit (index)");
   c->launches += (B ? 3 : 0) + 1;
   return IL_OK;
@@ -391,11 +385,6 @@ static il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, cons
   k_tab_key<<<cdiv(B, 256), 256, 0, st>>>(*c, B);
   k_tab_find<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B);
   const size_t smem = (size_t)c->cfg.table_capacity * 8;
-  static bool attr = false;
-  if (!attr) {
-    IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
-    attr = true;
-  }
   k_tab_commit<<<1, 1024, smem, st>>>(*c, B, b_cur);
   IL_LAUNCH_CHECK("il_commit (table)");
   c->launches += 3;
@@ -403,6 +392,15 @@ static il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, cons
 }
 
 __global__ void k_end_batch(Ctx c) { c.sc->batch_done += 1; }
+
+// one-time per-context setup (il_create, current device): attributes and cooperative grid size
+il_status il::commit_setup(Ctx* c) {
+  IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+  int per_sm = 0;
+  IL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0));
+  c->rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+  return IL_OK;
+}
 
 static il_status end_batch(Ctx* c, cudaStream_t st) {
   k_end_batch<<<1, 1, 0, st>>>(*c);

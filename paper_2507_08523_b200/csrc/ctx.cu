@@ -93,6 +93,7 @@ static il_status validate(const il_config* g) {
   if (g->max_log_tokens < 1 || g->max_log_tokens > 256) { set_error("max_log_tokens in 1..256"); return IL_ERR_ARG; }
   if (g->n_kv_heads < 1 || g->n_q_heads % g->n_kv_heads) { set_error("Hq % Hkv != 0"); return IL_ERR_ARG; }
   if (g->head_dim != 64 && g->head_dim != 128) { set_error("head_dim must be 64 or 128"); return IL_ERR_ARG; }
+  if (g->n_q_heads / g->n_kv_heads > 8) { set_error("Hq / Hkv must be <= 8"); return IL_ERR_ARG; }
   if (g->metric > 1) { set_error("metric"); return IL_ERR_ARG; }
   return IL_OK;
 }
@@ -273,6 +274,10 @@ il_status il_create(const il_config* cfg, void* ws, size_t bytes, il_stream s, i
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  for (il_status (*f)(Ctx*) : {match_setup, commit_setup, attn_setup}) {
+    st = f(c);
+    if (st) { delete c; return st; }
+  }
   k_reset_index<<<c->num_sms * 4, 256, 0, (cudaStream_t)s>>>(*c);
   IL_LAUNCH_CHECK("k_reset_index");
   *out = c;
@@ -296,6 +301,28 @@ il_status il_status_sync(il_ctx* c, il_stream s) {
                                     : "device: internal invariant broken");
   }
   return (il_status)st;
+}
+
+static __global__ void k_stats(Ctx c, il_stats* out, uint64_t launches) {
+  const DevScalars& h = *c.sc;
+  out->batch = h.batch_done;
+  out->resident_blocks = h.resident;
+  out->free_pages = h.n_free;
+  out->table_entries = h.table_entries;
+  out->evicted_blocks = h.evicted;
+  out->need_pages = h.need_total;
+  out->suffix_tokens = h.suffix_total;
+  out->index_rebuilds = h.rebuilds;
+  out->status = h.status;
+  out->launches = launches;
+}
+
+il_status il_stats_async(il_ctx* c, il_stats* out, il_stream s) {
+  if (!out || ((uintptr_t)out & 7)) { set_error("il_stats_async: null or misaligned output"); return IL_ERR_ARG; }
+  k_stats<<<1, 1, 0, (cudaStream_t)s>>>(*c, out, c->launches);
+  IL_LAUNCH_CHECK("k_stats");
+  c->launches += 1;
+  return IL_OK;
 }
 
 il_status il_stats_sync(il_ctx* c, il_stream s, il_stats* out) {
@@ -322,6 +349,8 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   const il_config& g = c->cfg;
   if (n < g.k || n > g.max_pool) { set_error("n_demos must be in [k, max_pool]"); return IL_ERR_ARG; }
   if (n_instr > g.max_prompt_tokens) { set_error("instruction longer than max_prompt_tokens"); return IL_ERR_ARG; }
+  // the per-batch instruction touch/pin (k_alloc_scan) covers at most 1,024 instruction blocks
+  if (n_instr / BS > 1024) { set_error("instruction longer than 16,384 tokens"); return IL_ERR_ARG; }
   // the pool token total is needed on the host to bound the copy: read it (one-off, not on the path)
   uint32_t tot[2];
   IL_CUDA(cudaMemcpyAsync(&tot[0], log_off + n, 4, cudaMemcpyDeviceToHost, (cudaStream_t)s));

@@ -103,12 +103,18 @@ struct Ctx {
   const uint32_t* hit = nullptr;
   const int32_t* block_table = nullptr;
   int num_sms = 148;
+  int ev_blocks = 0, rb_blocks = 0;   // cooperative grid sizes (k_evict, k_rebuild), set per context
   uint64_t launches = 0;     // kernels launched by this context (host counter)
 };
 
 // ---------------------------------------------------------------- error plumbing (host)
 void set_error(const std::string& msg);
 il_status cuda_check(cudaError_t e, const char* what);
+// per-context one-time setup on the current device (il_create): kernel attributes and
+// occupancy-derived grid sizes are per device, so nothing is cached process-wide
+il_status match_setup(Ctx* c);
+il_status commit_setup(Ctx* c);
+il_status attn_setup(Ctx* c);
 #define IL_CUDA(call)                                                  \
   do {                                                                 \
     cudaError_t _e = (call);                                           \
@@ -146,12 +152,15 @@ __device__ __forceinline__ uint64_t chain_step(uint64_t prev, uint64_t content) 
   h = (h == KEY_TOMB) ? (KEY_TOMB - 1ull) : h;
   return h;
 }
-// content hash of the 16 tokens at t (16-byte aligned)
+// content hash of the 16 tokens at t (16-byte aligned).  kReadOnly: the row was written by an
+// earlier kernel and stays read-only for this one, so the non-coherent path (__ldg) is allowed;
+// otherwise (a row written earlier in the SAME kernel, e.g. the guard of k_refine) ld.global.cg.
+template <bool kReadOnly = true>
 __device__ __forceinline__ uint64_t block_content(const uint32_t* __restrict__ t, uint32_t tok[16]) {
   const uint4* v = reinterpret_cast<const uint4*>(t);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint4 x = __ldg(v + q);
+    uint4 x = kReadOnly ? __ldg(v + q) : __ldcg(v + q);   // .cg: coherent at L2, never .nc
     tok[4 * q + 0] = x.x; tok[4 * q + 1] = x.y; tok[4 * q + 2] = x.z; tok[4 * q + 3] = x.w;
   }
   uint64_t s = 0;

@@ -86,13 +86,18 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
   uint32_t need, suf;
   uint32_t an = block_scan(n, s_w, &need);
   uint32_t as = block_scan(sfx, s_w, &suf);
+  // More suffix rows than the caller's Q / K_new / V_new / out buffers hold: latch the capacity
+  // error and publish an EMPTY suffix (cu_q = 0), so that k_synth, k_kv_append, k_tile_scan and
+  // the attention kernel, which all loop up to cu_q[B], touch nothing outside the caller's buffers.
+  const bool sfx_over = suf > c.cfg.max_suffix_tokens;
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     const uint32_t L = prompt_len[i], h = hit[i];
-    c.need_off[i] = an; cu_q[i] = (int32_t)as; prefix_len[i] = (int32_t)(BS * h);
+    c.need_off[i] = an; cu_q[i] = sfx_over ? 0 : (int32_t)as; prefix_len[i] = (int32_t)(BS * h);
     an += cdiv(L, BS) - h;
     as += L - BS * h;
   }
   if (tid == 1023) {
+    if (sfx_over) suf = 0;
     c.need_off[B] = need; cu_q[B] = (int32_t)suf;
     DevScalars* sc = c.sc;
     sc->need_total = need;
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
     uint32_t m = need > sc->n_free ? need - sc->n_free : 0;
     const uint32_t cand = sc->resident - sc->pinned;
     if (m > cand) { latch(sc, IL_ERR_CAPACITY); m = 0; sc->need_total = 0; }
-    if (suf > c.cfg.max_suffix_tokens) latch(sc, IL_ERR_CAPACITY);
+    if (sfx_over) latch(sc, IL_ERR_CAPACITY);
     sc->evict_m = m;
     sc->cand = cand;
     sc->stamp_min = ~0ull;
@@ -263,6 +268,14 @@ __global__ void k_alloc_commit(Ctx c) {
 
 using namespace il;
 
+// one-time per-context setup (il_create, current device): cooperative grid size of k_evict
+il_status il::match_setup(Ctx* c) {
+  int per_sm = 0;
+  IL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_evict, EV_THREADS, 0));
+  c->ev_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+  return IL_OK;
+}
+
 extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const uint32_t* prompt_len,
                                      uint64_t* block_hash, uint32_t* hit, int32_t* block_table,
                                      int32_t* prefix_len, int32_t* cu_q, il_stream s) {
@@ -275,16 +288,10 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
   k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q, b_cur);
   {
-    static int ev_blocks = -1;
-    if (ev_blocks < 0) {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_evict, EV_THREADS, 0);
-      ev_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
-    }
     Ctx cc = *c;
     uint64_t bc = b_cur;
     void* args[] = {&cc, &bc};
-    IL_CUDA(cudaLaunchCooperativeKernel((void*)k_evict, dim3(ev_blocks), dim3(EV_THREADS), args, 0, st));
+    IL_CUDA(cudaLaunchCooperativeKernel((void*)k_evict, dim3(c->ev_blocks), dim3(EV_THREADS), args, 0, st));
   }
   if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
   k_alloc_commit<<<1, 1, 0, st>>>(*c);

@@ -14,7 +14,9 @@ namespace il {
 // shortcut, the same keys against the same snapshot.
 // Returns the hit count capped at floor((L-1)/16) (Z20).  Optionally stores every block hash
 // (hash_out[j]) and the pages of the leading run (page_out[j]).  If stop_at_miss, returns as
-// soon as the run ends (the guard only needs the count).
+// soon as the run ends (the guard only needs the count).  kRowReadOnly = false when `row` was
+// written earlier in the calling kernel (the guard): its tokens are then read with ld.global.cg.
+template <bool kRowReadOnly = true>
 __device__ __forceinline__ uint32_t warp_hash_match(const Ctx& c, const uint32_t* __restrict__ row,
                                                     uint32_t L, uint64_t* hash_out, int32_t* page_out,
                                                     bool stop_at_miss) {
@@ -37,7 +39,7 @@ __device__ __forceinline__ uint32_t warp_hash_match(const Ctx& c, const uint32_t
     const bool active = j < F;
     uint32_t tok[16];
     uint64_t content = 0;
-    if (active) content = block_content(row + (size_t)BS * j, tok);
+    if (active) content = block_content<kRowReadOnly>(row + (size_t)BS * j, tok);
     const uint64_t chunk_prev = prev;
     const uint32_t nb = min(32u, F - base);
     uint64_t H = 0;

@@ -385,8 +385,8 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
       render(cur, grow);
       __syncthreads();
       if (wid == 0) {
-        const uint32_t hf = warp_hash_match(c, row, L, nullptr, nullptr, true);
-        const uint32_t hc = warp_hash_match(c, grow, Lc, nullptr, nullptr, true);
+        const uint32_t hf = warp_hash_match<false>(c, row, L, nullptr, nullptr, true);
+        const uint32_t hc = warp_hash_match<false>(c, grow, Lc, nullptr, nullptr, true);
         if (lane == 0) {
           s_rendered = 1;
           if (hf < hc) { s_inf.reverted = 1; s_L = Lc; s_rendered = 0; }

@@ -65,3 +65,27 @@ def test_device_latched_prompt_too_long():
     with pytest.raises(L.ILError) as e:
         pl.ctx.status_sync()
     assert e.value.status == L.IL_ERR_ARG
+
+
+def test_suffix_overflow_latches_and_writes_nothing_past_the_buffers():
+    """More suffix rows than max_suffix_tokens (a cold batch): il_prefix_match latches
+    IL_ERR_CAPACITY and publishes an empty suffix (cu_q = 0), so synth / K,V append / attention
+    write nothing past the caller's [max_suffix_tokens] buffers (canary rows stay intact)."""
+    sp = StreamSpec(B=24, C=2048)
+    ds, pool, instr = make_stream(sp)
+    rows = 64
+    pl = gpu_pipeline(sp, pool, instr, max_suffix_tokens=rows)
+    canary = {}
+    for name in ("q", "k_new", "v_new", "out"):
+        t = getattr(pl, name)
+        big = torch.full((rows + 256,) + tuple(t.shape[1:]), 7.0, dtype=t.dtype, device=t.device)
+        setattr(pl, name, big[:rows])
+        canary[name] = big
+    pl.stage_batch(gen.make_batch(ds, 0, sp.B))
+    pl.refine(); pl.match(); pl.synth(); pl.attn()
+    with pytest.raises(L.ILError) as e:
+        pl.ctx.status_sync()
+    assert e.value.status == L.IL_ERR_CAPACITY
+    assert int(pl.cu_q[sp.B].item()) == 0
+    for name, big in canary.items():
+        assert bool((big[rows:] == 7.0).all()), name

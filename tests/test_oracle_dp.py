@@ -40,7 +40,7 @@ def _run(sp, G, n_batches):
     return res
 
 
-SP = dict(B=96, C=1500, n_logs=2000)
+SP = dict(B=96, C=1700, n_logs=2000)
 
 
 @pytest.mark.parametrize("G", [2, 4])

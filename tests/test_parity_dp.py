@@ -74,13 +74,19 @@ def run_dp(sp: StreamSpec, G: int, n_batches: int, attention: bool = False):
 
 
 def test_dp2_no_guard():
-    run_dp(StreamSpec(B=96, C=1500, n_logs=2000), G=2, n_batches=10)
+    run_dp(StreamSpec(B=96, C=1700, n_logs=2000), G=2, n_batches=10)
 
 
 def test_dp2_guard():
-    run_dp(StreamSpec(B=96, C=1500, n_logs=2000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD), G=2, n_batches=10)
+    run_dp(StreamSpec(B=96, C=1700, n_logs=2000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD), G=2, n_batches=10)
 
 
 def test_dp4_eviction_pressure_with_attention():
     sp = StreamSpec(B=64, C=700, n_logs=3000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4, 16))
     run_dp(sp, G=4, n_batches=14, attention=True)
+
+
+def test_dp8_guard():
+    # G = 8 ranks (the box size of SURVEY §8(e)), 16 requests per rank
+    run_dp(StreamSpec(B=128, C=600, n_logs=3000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(8, 64)),
+           G=8, n_batches=10)

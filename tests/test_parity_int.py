@@ -97,3 +97,23 @@ def test_graph_replay_stream_bit_exact():
         compare_batch(r, pl, B, sp, where=f"graph batch {b}")
         compare_state(o, pl, where=f"graph batch {b}")
     assert pl.ctx.stats()["batch"] == len(plan)
+
+
+def test_c4_full_pool_10k_k8():
+    """BASELINE configs[3] selection at full size: a 10,000-demo pool, k = 8, B = 1,024, 1,000
+    templates with Zipf 1.3 (bench.workload(4)); integer path bit-exact for 5 batches."""
+    import bench
+    cfg, ds, pool, instr = bench.workload(4, 0, 1, n_queries=6 * 1024)
+    sp = StreamSpec(M=cfg.M, k=cfg.k, B=cfg.B, n_instr=cfg.n_instr, T=cfg.T, C=cfg.C,
+                    max_prompt_tokens=cfg.max_prompt_tokens, Hq=cfg.Hq, Hkv=cfg.Hkv, d=cfg.d,
+                    flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
+    o = oracle_for(sp, pool, instr)
+    pl = gpu_pipeline(sp, pool, instr)
+    for b in range(5):
+        batch = gen.make_batch(ds, b * cfg.B, cfg.B)
+        r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=sp.max_prompt_tokens // 16)
+        pl.stage_batch(batch)
+        pl.refine(); pl.match(); pl.commit()
+        pl.ctx.status_sync()
+        compare_batch(r, pl, cfg.B, sp, where=f"c4 batch {b}")
+        compare_state(o, pl, where=f"c4 batch {b}")

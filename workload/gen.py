@@ -117,28 +117,69 @@ def make_dataset(name: str, n_logs: int, n_templates: int, zipf_s: float, seed: 
             sz = int(rng.integers(value_pool_range[0], value_pool_range[1] + 1))
             w = int(rng.integers(1, max_value_len + 1))
             alpha = int(rng.integers(4, 41))
-            vlen = rng.integers(1, w + 1, size=sz)
-            vals = [(next_value + rng.integers(0, alpha, size=vlen[v])).astype(np.uint32)
-                    for v in range(sz)]
-            pools.append((int(pos), vals))
+            vlen = rng.integers(1, w + 1, size=sz).astype(np.int64)
+            vflat = (next_value + rng.integers(0, alpha, size=int(vlen.sum()))).astype(np.uint32)
+            pools.append((int(pos), vlen, vflat))         # value v = vflat[voff[v]:voff[v+1]]
             next_value += alpha
         templates.append(tpl)
         slot_pools.append(pools)
     pop = _zipf_probs(n_templates, zipf_s)
     log_tpl = rng.choice(n_templates, size=n_logs, p=pop).astype(np.uint32)
-    rows = []
-    for t in log_tpl:
-        parts, prev = [], 0
-        for pos, vals in slot_pools[t]:
-            parts.append(templates[t][prev:pos])
-            parts.append(vals[int(rng.integers(len(vals)))])
+    log_off, log_tok = _assemble_logs(rng, templates, slot_pools, log_tpl)
+    return Dataset(name, templates, log_off, log_tok, log_tpl)
+
+
+def _ragged_arange(lens: np.ndarray) -> np.ndarray:
+    """concatenate(arange(l) for l in lens), vectorised."""
+    tot = int(lens.sum())
+    starts = np.cumsum(lens) - lens
+    return np.arange(tot, dtype=np.int64) - np.repeat(starts, lens)
+
+
+def _assemble_logs(rng, templates, slot_pools, log_tpl):
+    """Every log = its template with each slot replaced by a value drawn uniformly from that
+    slot's pool.  Vectorised per (template, slot): the value draws of all logs of a template are
+    one rng call per slot, in template order, and the ragged pieces are scattered into one flat
+    token array (a 10M-log stream takes seconds, not minutes)."""
+    n = len(log_tpl)
+    lens = np.zeros(n, np.int64)
+    plan = []
+    order = np.argsort(log_tpl, kind="stable")            # logs grouped by template, row order kept
+    bounds = np.concatenate([[0], np.cumsum(np.bincount(log_tpl, minlength=len(templates)))])
+    for t, (tpl, pools) in enumerate(zip(templates, slot_pools)):
+        idx = order[bounds[t]:bounds[t + 1]]
+        if len(idx) == 0:
+            plan.append(None)
+            continue
+        choice = []
+        for pos, vlen, vflat in pools:
+            voff = np.concatenate([[0], np.cumsum(vlen)])
+            v = rng.integers(len(vlen), size=len(idx))
+            choice.append((pos, vlen, voff, vflat, v))
+        lens[idx] = (len(tpl) - len(pools)) + sum(c[1][c[4]] for c in choice)
+        plan.append((idx, choice))
+    log_off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=log_off[1:])
+    log_tok = np.empty(int(log_off[-1]), np.uint32)
+    for t, pl in enumerate(plan):
+        if pl is None:
+            continue
+        idx, choice = pl
+        tpl = templates[t]
+        cur = log_off[idx].copy()                       # write cursor of each log of template t
+        prev = 0
+        for pos, vlen, voff, vflat, v in choice + [(len(tpl), None, None, None, None)]:
+            seg = tpl[prev:pos]                         # constant piece before this slot
+            if len(seg):
+                log_tok[cur[:, None] + np.arange(len(seg))[None, :]] = seg[None, :]
+                cur += len(seg)
+            if vlen is not None:                        # the slot's value, ragged
+                L = vlen[v]
+                r = _ragged_arange(L)
+                log_tok[np.repeat(cur, L) + r] = vflat[np.repeat(voff[v], L) + r]
+                cur += L
             prev = pos + 1
-        parts.append(templates[t][prev:])
-        rows.append(np.concatenate(parts).astype(np.uint32))
-    log_off = np.zeros(n_logs + 1, dtype=np.int64)
-    np.cumsum([len(r) for r in rows], out=log_off[1:])
-    log_tok = np.concatenate(rows).astype(np.uint32)
-    return Dataset(name, templates, log_off.astype(np.uint32), log_tok, log_tpl)
+    return log_off.astype(np.uint32), log_tok
 
 
 def sample_pool(ds: Dataset, M: int, seed: int) -> Pool:
