@@ -82,8 +82,10 @@ typedef struct {
   uint32_t metric;             /* il_sim */
   uint32_t flags;              /* IL_F_* */
   uint64_t hash_seed;          /* chain-hash root (Z17) */
-  uint32_t max_global_batch;   /* records per il_commit_records (multi-GPU: world x B); 0 = max_batch */
-  uint32_t reserved0;          /* must be 0 */
+  uint32_t max_global_batch;   /* records per il_commit_records / il_commit_apply (multi-GPU:
+                                  world x B); 0 = max_batch.  > max_batch enables the multi-GPU
+                                  block records and the residency map (ranks = ceil(./max_batch) <= 32) */
+  uint32_t max_block_records;  /* multi-GPU: block records one il_commit_export carries; 0 = 16 x max_batch */
 } il_config;
 
 /* Per-request refinement outcome (SPEC S:190-193 RefinementResult). */
@@ -107,6 +109,12 @@ typedef struct {               /* counters of the last committed batch (il_stats
   uint32_t index_rebuilds;     /* tombstone compactions so far */
   uint32_t status;             /* latched il_status */
   uint64_t launches;           /* kernels this context has launched so far */
+  uint32_t hit_blocks;         /* sum of capped hits of the last il_prefix_match (this rank) */
+  uint32_t box_hit_blocks;     /* the same against the box (this rank's index or the residency map) */
+  uint32_t full_blocks;        /* sum of floor(L_i / 16) of the last il_prefix_match */
+  uint32_t record_backlog;     /* block records waiting for a later il_commit_export */
+  uint32_t map_slots_used;     /* residency-map slots holding a key (live or dead) */
+  uint32_t reserved;
 } il_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */
@@ -210,6 +218,46 @@ il_status il_commit(il_ctx* ctx, il_stream s);
 il_status il_commit_index(il_ctx* ctx, il_stream s);
 il_status il_commit_records(il_ctx* ctx, uint32_t B_global, const uint32_t* final_ds_all,
                             const il_refine_info* info_all, il_stream s);
+
+/* ---- the per-batch exchange as ONE fixed-size record buffer per rank (
+ * north star: "all-gather prefix-index updates").  A record buffer holds
+ *   header (64 B): magic 'ILRC', B of this rank, k, n block records, batch b, backlog
+ *   ICL records:   final_ds [max_batch][k] u32 (padded to 16 B), il_refine_info [max_batch]
+ *   block records: [max_block_records] u64 chain hashes: every block this rank's prefix index
+ *                  gained (il_commit_index) or lost (LRU eviction in il_prefix_match) since the
+ *                  last export, oldest first.  More than max_block_records wait in the context
+ *                  (FIFO, `record_backlog` in il_stats) for the next export; a FIFO overflow
+ *                  latches IL_ERR_CAPACITY.
+ * The caller all-gathers the n_ranks buffers rank-major (one all_gather_into_tensor) and every
+ * rank calls il_commit_apply on the result:
+ *   - the ICL records of all ranks are applied to the replicated table in global admission
+ *     order (exactly il_commit_records over their concatenation);
+ *   - the block records build the replicated RESIDENCY MAP, hash -> owner-rank bitmask
+ *     ("shared prefix index", BASELINE configs[2]).  A block record toggles its rank's bit
+ *     (an index gains and loses a hash alternately, so applying a buffer's records in any order
+ *     gives the same map: the map equals the union of the ranks' indices whenever no records
+ *     are waiting).
+ * From then on il_prefix_match also computes every request's BOX-LEVEL hit count: the leading
+ * blocks resident in this rank's index or in the map (chain hash only, not verified), capped
+ * as Z20 -- the hit rate that box-wide reuse of remote pages would give (il_stats, il_box_hit_dump).
+ *   il_record_bytes   bytes of one rank's record buffer (256-byte multiple)
+ *   il_commit_export  after il_commit_index: write this rank's records into rec (device)
+ *   il_commit_apply   recs_all = n_ranks buffers back to back, rank r's holding
+ *                     batch_per_rank_h[r] requests (host array); sum <= max_global_batch.
+ *                     Ends the batch (il_commit == index + export + apply over one rank). */
+il_status il_record_bytes(const il_config* cfg_h, size_t* bytes_h);
+il_status il_commit_export(il_ctx* ctx, void* rec, il_stream s);
+il_status il_commit_apply(il_ctx* ctx, const void* recs_all, uint32_t n_ranks,
+                          const uint32_t* batch_per_rank_h, il_stream s);
+/* box-level hit counts of the last il_prefix_match ([B] host), zeros before any il_commit_apply */
+il_status il_box_hit_dump(il_ctx* ctx, il_stream s, uint32_t* box_hit_h, uint32_t B);
+
+/* ---- a1-a2 alone (kNN selection into topk), so that a multi-GPU driver can overlap the
+ * previous batch's record all-gather with it: selection reads only the pool, never the ICL
+ * Table.  A following il_refine_batch of the same B with the same topk buffer does not repeat
+ * it. */
+il_status il_select_batch(il_ctx* ctx, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
+                          const uint32_t* q_src, uint32_t* topk, il_stream s);
 
 /* ---- bench / test helper (not part of the method): deterministic bf16 Q, K, V for the
  * suffix rows from (seed, token, absolute position, head, dim) — the counter-based

@@ -24,7 +24,8 @@ IL_F_PAIR, IL_F_GUARD, IL_F_EXCLUDE_SELF, IL_F_VERIFY = 1, 2, 4, 8
 EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "il_stats_sync", "il_stats_async",
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
            "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
-           "il_table_dump", "il_evicted_dump"]
+           "il_table_dump", "il_evicted_dump", "il_record_bytes", "il_commit_export", "il_commit_apply",
+           "il_box_hit_dump", "il_select_batch"]
 
 
 class ILError(RuntimeError):
@@ -39,7 +40,7 @@ class il_config(C.Structure):
                 ("max_pool_tokens", C.c_uint32), ("max_log_tokens", C.c_uint32),
                 ("max_suffix_tokens", C.c_uint32), ("n_q_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
                 ("head_dim", C.c_uint32), ("metric", C.c_uint32), ("flags", C.c_uint32),
-                ("hash_seed", C.c_uint64), ("max_global_batch", C.c_uint32), ("reserved0", C.c_uint32)]
+                ("hash_seed", C.c_uint64), ("max_global_batch", C.c_uint32), ("max_block_records", C.c_uint32)]
 
 
 class il_refine_info(C.Structure):
@@ -51,11 +52,13 @@ class il_stats(C.Structure):
     _fields_ = [("batch", C.c_uint64), ("resident_blocks", C.c_uint32), ("free_pages", C.c_uint32),
                 ("table_entries", C.c_uint32), ("evicted_blocks", C.c_uint32), ("need_pages", C.c_uint32),
                 ("suffix_tokens", C.c_uint32), ("index_rebuilds", C.c_uint32), ("status", C.c_uint32),
-                ("launches", C.c_uint64)]
+                ("launches", C.c_uint64), ("hit_blocks", C.c_uint32), ("box_hit_blocks", C.c_uint32),
+                ("full_blocks", C.c_uint32), ("record_backlog", C.c_uint32), ("map_slots_used", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 assert C.sizeof(il_refine_info) == 16
-assert C.sizeof(il_stats) == 48
+assert C.sizeof(il_stats) == 72
 
 
 _lib = None
@@ -88,6 +91,11 @@ def load():
         "il_index_dump": [P, P, P, P, P, P, P],
         "il_table_dump": [P, P, P, P],
         "il_evicted_dump": [P, P, P, P],
+        "il_record_bytes": [C.POINTER(il_config), C.POINTER(C.c_size_t)],
+        "il_commit_export": [P, P, P],
+        "il_commit_apply": [P, P, U32, P, P],
+        "il_box_hit_dump": [P, P, P, U32],
+        "il_select_batch": [P, U32, P, P, P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -32,6 +32,7 @@ class Config:
     flags: int = L.IL_F_PAIR | L.IL_F_VERIFY
     hash_seed: int = 0
     max_global_batch: int = 0           # multi-GPU: world * max_batch records per table commit
+    max_block_records: int = 0          # multi-GPU: block records per export (0 = 16 * max_batch)
 
     @property
     def max_blocks(self) -> int:
@@ -42,7 +43,14 @@ class Config:
         return L.il_config(self.k, self.table_capacity, self.kv_pages, self.max_batch,
                            self.max_prompt_tokens, self.max_pool, self.max_pool_tokens,
                            self.max_log_tokens, m, self.n_q_heads, self.n_kv_heads, self.head_dim,
-                           self.metric, self.flags, self.hash_seed, self.max_global_batch, 0)
+                           self.metric, self.flags, self.hash_seed, self.max_global_batch,
+                           self.max_block_records)
+
+    def record_bytes(self) -> int:
+        cc = self.c()
+        n = C.c_size_t(0)
+        L.check(L.load().il_record_bytes(C.byref(cc), C.byref(n)), "il_record_bytes")
+        return int(n.value)
 
 
 def _p(t) -> C.c_void_p:
@@ -115,6 +123,24 @@ class Context:
     def commit_records(self, B_global, final_ds_all, info_all, stream=None):
         L.check(self.lib.il_commit_records(self.h, B_global, _p(final_ds_all), _p(info_all), _stream(stream)),
                 "il_commit_records")
+
+    def commit_export(self, rec, stream=None):
+        L.check(self.lib.il_commit_export(self.h, _p(rec), _stream(stream)), "il_commit_export")
+
+    def commit_apply(self, recs_all, batch_per_rank, stream=None):
+        bpr = (C.c_uint32 * len(batch_per_rank))(*[int(x) for x in batch_per_rank])
+        L.check(self.lib.il_commit_apply(self.h, _p(recs_all), len(batch_per_rank), bpr, _stream(stream)),
+                "il_commit_apply")
+
+    def select_batch(self, B, q_off, q_tok, q_src, topk, stream=None):
+        L.check(self.lib.il_select_batch(self.h, B, _p(q_off), _p(q_tok), _p(q_src), _p(topk), _stream(stream)),
+                "il_select_batch")
+
+    def box_hit_dump(self, B, stream=None) -> np.ndarray:
+        out = np.zeros(max(B, 1), np.uint32)
+        L.check(self.lib.il_box_hit_dump(self.h, _stream(stream), out.ctypes.data_as(C.c_void_p), B),
+                "il_box_hit_dump")
+        return out[:B]
 
     def synth_qkv(self, B, prompt_tok, cu_q, prefix_len, seed, q_scale, q, k_new, v_new, stream=None):
         L.check(self.lib.il_synth_qkv(self.h, B, _p(prompt_tok), _p(cu_q), _p(prefix_len), int(seed),

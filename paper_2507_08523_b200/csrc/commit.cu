@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) k_commit_own(Ctx c, uint32_t B) {
     c.pg_state[page] = 1;
     c.claim[o] = NONE32;
     c.cstamp[o] = 0;
+    if (c.ins_list) c.ins_list[atomicAdd(&c.sc->inserted, 1u)] = bh[j];   // multi-GPU block record
     ++owned;
   }
   if (lane == 0 && (L % BS)) push_free(c, (uint32_t)bt[F]);       // partial block (Z23)
@@ -377,8 +378,8 @@ static il_status commit_index(Ctx* c, cudaStream_t st, uint64_t b_cur) {
 }
 
 // table half: B records (final DS + refine info) in admission order, stamps (b_cur, i)
-static il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, const il_refine_info* info,
-                              cudaStream_t st, uint64_t b_cur) {
+il_status il::commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, const il_refine_info* info,
+                           cudaStream_t st, uint64_t b_cur) {
   if (!B) return IL_OK;
   c->final_ds = final_ds;
   c->info = info;
@@ -402,12 +403,12 @@ il_status il::commit_setup(Ctx* c) {
   return IL_OK;
 }
 
-static il_status end_batch(Ctx* c, cudaStream_t st) {
+il_status il::end_batch(Ctx* c, cudaStream_t st) {
   k_end_batch<<<1, 1, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_commit (end of batch)");
   c->launches += 1;
   c->batch += 1;
-  c->refined = c->matched = c->index_done = false;
+  c->refined = c->matched = c->index_done = c->exported = false;
   return IL_OK;
 }
 

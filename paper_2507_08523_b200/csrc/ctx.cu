@@ -77,6 +77,28 @@ static size_t carve(Ctx* c, void* ws) {
   c->attn_ml = w.take<float>((size_t)g.max_suffix_tokens * g.n_q_heads);
   c->evicted_list = w.take<uint64_t>(C);
   c->guard_prompt = (g.flags & IL_F_GUARD) ? w.take<uint32_t>(B * g.max_prompt_tokens) : nullptr;
+  // multi-GPU exchange: block-record FIFO, residency map (2 x ranks x C slots), box hits, gathered
+  // ICL records
+  c->n_ranks_max = g.max_global_batch > B ? (uint32_t)((g.max_global_batch + B - 1) / B) : 1;
+  if (c->n_ranks_max > 1) {
+    c->rec_R = g.max_block_records ? g.max_block_records : 16 * (uint32_t)B;
+    c->ring_cap = (uint32_t)(4 * C + B * MB + c->rec_R);
+    uint32_t n = 1024;
+    while (n < 2ull * c->n_ranks_max * C) n <<= 1;
+    c->map_slots = n; c->map_smask = n - 1;
+    c->ins_list = w.take<uint64_t>(std::min<size_t>(C, B * MB));
+    c->ring = w.take<uint64_t>(c->ring_cap);
+    c->map_key = w.take<uint64_t>(n); c->map_mask = w.take<uint32_t>(n);
+    c->map_tmp_key = w.take<uint64_t>(n); c->map_tmp_mask = w.take<uint32_t>(n);
+    c->box_hit = w.take<uint32_t>(B);
+    c->icl_fds = w.take<uint32_t>(R * g.k);
+    c->icl_info = w.take<il_refine_info>(R);
+  } else {
+    c->rec_R = c->ring_cap = c->map_slots = c->map_smask = 0;
+    c->ins_list = c->ring = c->map_key = c->map_tmp_key = nullptr;
+    c->map_mask = c->map_tmp_mask = c->box_hit = c->icl_fds = nullptr;
+    c->icl_info = nullptr;
+  }
   return w.off + 256;
 }
 
@@ -87,7 +109,10 @@ static il_status validate(const il_config* g) {
   if (g->kv_pages < 1) { set_error("kv_pages >= 1"); return IL_ERR_ARG; }
   if (g->max_batch < 1 || g->max_batch > 8192) { set_error("max_batch in 1..8192"); return IL_ERR_ARG; }
   if (g->max_global_batch > 8192) { set_error("max_global_batch <= 8192"); return IL_ERR_ARG; }
-  if (g->reserved0 != 0) { set_error("il_config.reserved0 must be 0"); return IL_ERR_ARG; }
+  if (g->max_global_batch > g->max_batch && (g->max_global_batch + g->max_batch - 1) / g->max_batch > 32) {
+    set_error("at most 32 ranks (max_global_batch / max_batch)"); return IL_ERR_ARG;
+  }
+  if (g->max_block_records > (1u << 24)) { set_error("max_block_records <= 2^24"); return IL_ERR_ARG; }
   if (g->max_prompt_tokens < 16 || (g->max_prompt_tokens % 16)) { set_error("max_prompt_tokens: multiple of 16"); return IL_ERR_ARG; }
   if (g->max_pool < g->k) { set_error("max_pool < k"); return IL_ERR_ARG; }
   if (g->max_log_tokens < 1 || g->max_log_tokens > 256) { set_error("max_log_tokens in 1..256"); return IL_ERR_ARG; }
@@ -274,12 +299,14 @@ il_status il_create(const il_config* cfg, void* ws, size_t bytes, il_stream s, i
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  for (il_status (*f)(Ctx*) : {match_setup, commit_setup, attn_setup}) {
+  for (il_status (*f)(Ctx*) : {match_setup, commit_setup, attn_setup, records_setup}) {
     st = f(c);
     if (st) { delete c; return st; }
   }
   k_reset_index<<<c->num_sms * 4, 256, 0, (cudaStream_t)s>>>(*c);
   IL_LAUNCH_CHECK("k_reset_index");
+  st = records_reset(c, (cudaStream_t)s);
+  if (st) { delete c; return st; }
   *out = c;
   return IL_OK;
 }
@@ -315,6 +342,12 @@ static __global__ void k_stats(Ctx c, il_stats* out, uint64_t launches) {
   out->index_rebuilds = h.rebuilds;
   out->status = h.status;
   out->launches = launches;
+  out->hit_blocks = h.hit_sum;
+  out->box_hit_blocks = h.box_hit_sum;
+  out->full_blocks = h.full_sum;
+  out->record_backlog = (uint32_t)(h.ring_tail - h.ring_head);
+  out->map_slots_used = h.map_used;
+  out->reserved = 0;
 }
 
 il_status il_stats_async(il_ctx* c, il_stats* out, il_stream s) {
@@ -339,6 +372,12 @@ il_status il_stats_sync(il_ctx* c, il_stream s, il_stats* out) {
   out->index_rebuilds = h.rebuilds;
   out->status = h.status;
   out->launches = c->launches;
+  out->hit_blocks = h.hit_sum;
+  out->box_hit_blocks = h.box_hit_sum;
+  out->full_blocks = h.full_sum;
+  out->record_backlog = (uint32_t)(h.ring_tail - h.ring_head);
+  out->map_slots_used = h.map_used;
+  out->reserved = 0;
   return IL_OK;
 }
 
@@ -362,6 +401,8 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   }
   cudaStream_t st = (cudaStream_t)s;
   k_reset_index<<<c->num_sms * 4, 256, 0, st>>>(*c);
+  if (il_status r = records_reset(c, st)) return r;
+  c->map_active = false;
   k_pool_copy<<<c->num_sms * 2, 256, 0, st>>>(*c, n, log_off, log_tok, tpl_off, tpl_tok, template_id,
                                                 src_index, instr_tok, n_instr);
   k_pool_sets<<<cdiv(n, 8), 256, 0, st>>>(*c, n, log_off, log_tok);
@@ -373,7 +414,8 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   c->n_instr = n_instr;
   c->n_instr_blocks = n_instr / BS;
   c->pool_loaded = true;
-  c->refined = c->matched = c->index_done = false;
+  c->refined = c->matched = c->index_done = c->exported = false;
+  c->sel_topk = nullptr;
   c->batch = 0;
   return IL_OK;
 }

@@ -47,7 +47,15 @@ struct DevScalars {
   uint32_t cand;             // eviction candidates
   uint32_t q_total;          // attention: suffix rows of the batch (cu_q[B])
   uint32_t shared_blk;       // attention: blocks every request shares (same pages, all cached)
-  uint32_t pad1[15];
+  uint32_t inserted;         // blocks this batch's il_commit_index made resident (records)
+  uint32_t hit_sum;          // last prefix match: sum of capped hits, sum of full blocks,
+  uint32_t full_sum;         //   sum of box-level hits
+  uint32_t box_hit_sum;
+  uint32_t map_used;         // residency-map slots holding a key
+  uint32_t map_rebuilds;
+  uint64_t ring_head;        // block-record FIFO (monotonic counters)
+  uint64_t ring_tail;
+  uint32_t pad1[4];
 };
 
 struct Ctx {
@@ -94,6 +102,24 @@ struct Ctx {
   float *attn_ml;            // cascade: per row log2 softmax mass of the shared-prefix partial
   uint64_t *evicted_list;
   uint32_t *guard_prompt;    // guard: DS_current prompt rows
+  // multi-GPU exchange (records.cu; allocated when max_global_batch > max_batch)
+  uint32_t n_ranks_max = 1;  // ceil(max_global_batch / max_batch)
+  uint32_t rec_R = 0;        // block records per export
+  uint32_t ring_cap = 0;     // block-record FIFO capacity
+  uint32_t map_slots = 0, map_smask = 0;
+  uint64_t *ins_list;        // this batch's newly resident block hashes (il_commit_index)
+  uint64_t *ring;            // block-record FIFO
+  uint64_t *map_key;         // residency map: open addressing, key = chain hash (0 = empty)
+  uint32_t *map_mask;        //   owner-rank bitmask (0 = dead key, reclaimed by the rebuild)
+  uint64_t *map_tmp_key;     //   rebuild scratch
+  uint32_t *map_tmp_mask;
+  uint32_t *box_hit;         // per request: box-level hit count of the last prefix match
+  uint32_t *icl_fds;         // il_commit_apply: gathered ICL records, global admission order
+  il_refine_info *icl_info;
+  bool map_active = false;   // host: an il_commit_apply with n_ranks > 1 has run
+  bool exported = false;     // host: il_commit_export ran for the current batch
+  const uint32_t* sel_topk = nullptr;   // host: il_select_batch ran for (sel_B, sel_topk)
+  uint32_t sel_B = 0;
   // pointers remembered between calls (caller-owned)
   const uint32_t* final_ds = nullptr;
   const il_refine_info* info = nullptr;
@@ -103,7 +129,8 @@ struct Ctx {
   const uint32_t* hit = nullptr;
   const int32_t* block_table = nullptr;
   int num_sms = 148;
-  int ev_blocks = 0, rb_blocks = 0;   // cooperative grid sizes (k_evict, k_rebuild), set per context
+  int ev_blocks = 0, rb_blocks = 0, mb_blocks = 0;   // cooperative grid sizes (k_evict, k_rebuild,
+                                                     // k_map_rebuild), set per context
   uint64_t launches = 0;     // kernels launched by this context (host counter)
 };
 
@@ -115,6 +142,30 @@ il_status cuda_check(cudaError_t e, const char* what);
 il_status match_setup(Ctx* c);
 il_status commit_setup(Ctx* c);
 il_status attn_setup(Ctx* c);
+il_status records_setup(Ctx* c);
+il_status records_reset(Ctx* c, cudaStream_t st);
+// shared between commit.cu and records.cu
+il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, const il_refine_info* info,
+                       cudaStream_t st, uint64_t b_cur);
+il_status end_batch(Ctx* c, cudaStream_t st);
+// record-buffer layout (il.h il_record_bytes)
+struct RecHeader {
+  uint32_t magic, B, k, n_blk;
+  uint64_t batch;
+  uint32_t backlog, pad[9];
+};
+static_assert(sizeof(RecHeader) == 64, "record header");
+constexpr uint32_t REC_MAGIC = 0x43524C49u;   // 'ILRC'
+__host__ __device__ inline size_t rec_fds_off() { return 64; }
+__host__ __device__ inline size_t rec_info_off(uint32_t max_batch, uint32_t k) {
+  return 64 + (((size_t)max_batch * k * 4 + 15) & ~size_t(15));
+}
+__host__ __device__ inline size_t rec_blk_off(uint32_t max_batch, uint32_t k) {
+  return rec_info_off(max_batch, k) + (size_t)max_batch * 16;
+}
+__host__ __device__ inline size_t rec_bytes(uint32_t max_batch, uint32_t k, uint32_t R) {
+  return (rec_blk_off(max_batch, k) + (size_t)R * 8 + 255) & ~size_t(255);
+}
 #define IL_CUDA(call)                                                  \
   do {                                                                 \
     cudaError_t _e = (call);                                           \
@@ -186,6 +237,18 @@ __device__ __forceinline__ uint32_t index_find(const uint64_t* __restrict__ slot
 }
 
 __host__ __device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+// residency map lookup (multi-GPU): some rank holds the block with chain hash `key`
+__device__ __forceinline__ bool map_has(const Ctx& c, uint64_t key) {
+  uint32_t s = (uint32_t)(key ^ (key >> 32)) & c.map_smask;
+  for (uint32_t n = 0; n <= c.map_smask; ++n) {
+    const uint64_t k = c.map_key[s];
+    if (k == key) return c.map_mask[s] != 0;
+    if (k == KEY_EMPTY) return false;
+    s = (s + 1) & c.map_smask;
+  }
+  return false;
+}
 
 
 // block-wide exclusive scan of one value per thread (1024 threads)

@@ -34,9 +34,30 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
     newly += atomicExch(&c.pg_pin[p], epoch) != epoch;
   }
   for (int o = 16; o; o >>= 1) newly += __shfl_xor_sync(~0u, newly, o);
+  // multi-GPU: box-level hits = this rank's leading run, continued through blocks the residency
+  // map says some rank holds (hash only), capped as Z20 (records.cu, il.h il_commit_apply)
+  uint32_t box = h;
+  if (c.map_active) {
+    const uint32_t F = L / BS, cap = L ? (L - 1) / BS : 0;
+    const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
+    for (uint32_t base = h; base < min(F, cap); base += 32) {
+      const uint32_t j = base + lane;
+      bool ok = false;
+      if (j < F) ok = map_has(c, bh[j]);
+      const uint32_t m = __ballot_sync(~0u, ok);
+      const uint32_t lead = (m == ~0u) ? 32u : (uint32_t)(__ffs(~m) - 1);
+      box += lead;
+      if (lead < 32) break;
+    }
+    box = min(box, cap);
+    if (lane == 0) c.box_hit[i] = box;
+  }
   if (lane == 0) {
     hit[i] = h;
     if (newly) atomicAdd(&c.sc->pinned, newly);
+    atomicAdd(&c.sc->hit_sum, h);
+    atomicAdd(&c.sc->full_sum, L / BS);
+    atomicAdd(&c.sc->box_hit_sum, box);
   }
 }
 
@@ -258,7 +279,10 @@ __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uin
   for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
 }
 // (a kernel rather than a memset node: keeps the captured match graph all-kernel)
-__global__ void k_match_begin(Ctx c) { c.sc->pinned = 0; }
+__global__ void k_match_begin(Ctx c) {
+  DevScalars* sc = c.sc;
+  sc->pinned = 0; sc->hit_sum = 0; sc->full_sum = 0; sc->box_hit_sum = 0; sc->inserted = 0;
+}
 __global__ void k_alloc_commit(Ctx c) {
   DevScalars* sc = c.sc;
   if (sc->status != IL_ERR_CAPACITY) sc->n_free -= sc->need_total;

@@ -419,6 +419,31 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
 
 using namespace il;
 
+// a1 + a2: exact similarity against the whole pool, top-k in ascending order
+static il_status select_launch(Ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
+                               const uint32_t* q_src, uint32_t* topk, cudaStream_t st) {
+  if (c->n_demos > SIM_BIG_POOL)
+    k_sim_topk<4><<<cdiv(B, SIM_THREADS / 128), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
+  else
+    k_sim_topk<IL_SIM_QW_SMALL><<<cdiv(B, SIM_THREADS / (32 * IL_SIM_QW_SMALL)), SIM_THREADS, 0, st>>>(
+        *c, B, q_off, q_tok, q_src, topk);
+  IL_LAUNCH_CHECK("k_sim_topk");
+  c->launches += 1;
+  return IL_OK;
+}
+
+extern "C" il_status il_select_batch(il_ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
+                                     const uint32_t* q_src, uint32_t* topk, il_stream s) {
+  if (!c->pool_loaded) { set_error("il_select_batch before il_pool_load"); return IL_ERR_STATE; }
+  if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
+  if (B == 0) return IL_OK;
+  il_status r = select_launch(c, B, q_off, q_tok, q_src, topk, (cudaStream_t)s);
+  if (r != IL_OK) return r;
+  c->sel_topk = topk;
+  c->sel_B = B;
+  return IL_OK;
+}
+
 extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
                                      const uint32_t* q_src, uint32_t* topk, uint32_t* final_ds,
                                      il_refine_info* info, uint32_t* prompt_tok, uint32_t* prompt_len,
@@ -428,15 +453,16 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
   if (B == 0) return IL_OK;
   if (((uintptr_t)prompt_tok & 15) != 0) { set_error("prompt_tok must be 16-byte aligned"); return IL_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)s;
-  if (c->n_demos > SIM_BIG_POOL)
-    k_sim_topk<4><<<cdiv(B, SIM_THREADS / 128), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
-  else
-    k_sim_topk<IL_SIM_QW_SMALL><<<cdiv(B, SIM_THREADS / (32 * IL_SIM_QW_SMALL)), SIM_THREADS, 0, st>>>(
-        *c, B, q_off, q_tok, q_src, topk);
+  const bool selected = c->sel_topk == topk && c->sel_B == B;   // il_select_batch already ran
+  c->sel_topk = nullptr;
+  if (!selected) {
+    il_status r = select_launch(c, B, q_off, q_tok, q_src, topk, st);
+    if (r != IL_OK) return r;
+  }
   if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
   k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
-  c->launches += (c->cfg.flags & IL_F_GUARD) ? 3 : 2;
+  c->launches += (c->cfg.flags & IL_F_GUARD) ? 2 : 1;
   c->final_ds = final_ds;
   c->info = info;
   c->refined = true;

@@ -30,7 +30,7 @@ def run_case(Hq, Hkv, d, reqs, shared_blocks=0, seed=0, big_rows=True, C=2048):
     rng = np.random.default_rng(seed)
     B = len(reqs)
     maxL = max(P + S for P, S in reqs)
-    mpt = max(64, (maxL + 15) // 16 * 16)
+    mpt = max(256, (maxL + 15) // 16 * 16)        # >= the pool instruction (128 tokens)
     tot_S = sum(S for _, S in reqs)
     sp = StreamSpec(n_logs=300, M=40, B=4)
     _, pool, instr = make_stream(sp)
