@@ -164,14 +164,14 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
     # N > 1: rank r runs the r-th slice of every global batch; the pool is
-    # broadcast from rank 0 and the ICL records are all-gathered (NCCL) at every commit
+    # broadcast from rank 0; per batch one record buffer per rank (ICL records + prefix-index
+    # updates) is all-gathered (NCCL) on a side stream, overlapping the next batch's selection
     dp = None
     if world > 1:
         from paper_2507_08523_b200.distributed import DataParallel
         dp = DataParallel(pl)
     with torch.cuda.stream(stream):
         (dp or pl).load_pool(pool, instr)
-    commit = dp.commit if dp else pl.commit
     step = dp.step if dp else pl.step
     K, W = args.steps, args.warmup
     n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
@@ -236,26 +236,43 @@ def run_ours(args, rank, world, local_rank):
     stream.synchronize()
     pl.ctx.status_sync(stream)
 
-    stage_names = ["refine", "match", "synth", "attn", "commit"]
-    # CUDA graphs (N = 1): each stage captured once for B (one replay per stage, no per-kernel
-    # launch gaps).  N > 1 launches eagerly: the commit's all-gather (NCCL) stays outside any
-    # graph, and eager calls keep the library's host-side call-order checks (a replayed graph does
-    # not pass through them, so an eager il_commit_index after replayed stages would be refused)
+    # The stages of one step.  N = 1: il_refine_batch .. il_commit.  N > 1: il_select_batch (a1-a2,
+    # overlapping the previous batch's record all-gather), then il_commit_apply of the gathered
+    # records + il_refine_batch, .., il_commit_index + il_commit_export; the all-gather itself
+    # (NCCL, side stream) and the wait for it stay outside the stages.
+    if dp is None:
+        stage_fns = {"refine": pl.refine, "match": pl.match, "synth": pl.synth, "attn": pl.attn,
+                     "commit": pl.commit}
+    else:
+        stage_fns = {"select": dp.select, "refine": lambda: (dp.apply_records(), pl.refine()),
+                     "match": pl.match, "synth": pl.synth, "attn": pl.attn, "commit": dp.export}
+    stage_names = list(stage_fns)
+    # CUDA graphs: each stage captured once for B (one replay per stage, no per-kernel launch gaps;
+    # every library call of the step is inside a graph, so the host-side call-order state stays
+    # consistent).  Capture does not run the kernels: the warm-up's pending records are applied by
+    # the first replay of the "refine" stage.
     graphs, per_step_launches = None, None
-    if not args.no_graph and dp is None:
+    if not args.no_graph:
         l0 = pl.launches()
-        with torch.cuda.stream(stream):
-            graphs = pl.capture(cfg.B, stages=stage_names)
+        pl.B = cfg.B
+        graphs = {}
+        for name in stage_names:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                stage_fns[name]()
+            graphs[name] = g
         per_step_launches = pl.launches() - l0
         stream.synchronize()
 
     def run_stage(name):
-        if graphs is not None and name in graphs:
+        if dp is not None and name == "refine":
+            dp.wait_gathered()                         # (eager: an event wait, never captured)
+        if graphs is not None:
             graphs[name].replay()
-        elif name == "commit":
-            commit()
         else:
-            getattr(pl, name)()
+            stage_fns[name]()
+        if dp is not None and name == "commit":
+            dp.gather()                                # all-gather on the comm stream (eager)
 
     def run_step():
         for n in stage_names:
@@ -279,11 +296,11 @@ def run_ours(args, rank, world, local_rank):
             flush.zero_()
             if j % 2 == 0:
                 set_inputs(dev_in[j])
-                e = [ev() for _ in range(6)]
+                e = [ev() for _ in range(len(stage_names) + 1)]
                 for i, n in enumerate(stage_names):
                     e[i].record(stream)
                     run_stage(n)
-                e[5].record(stream)
+                e[-1].record(stream)
                 pl.ctx.stats_async(rec_stats[j], stream=stream)
                 evs.append(e)
                 B = dev_in[j][3]
@@ -307,6 +324,9 @@ def run_ours(args, rank, world, local_rank):
                 e2e_evs.append((e0, e1))
                 h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
                 d2h = 4 * B * cfg.k + 4 * B + 16 * B
+    if dp is not None:
+        with torch.cuda.stream(stream):
+            dp.flush()                                 # the last batch's records (after the timed region)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall
     if prof is not None:
@@ -324,10 +344,17 @@ def run_ours(args, rank, world, local_rank):
         launches += per_step_launches * 2 * K
     st_steps = [pl.ctx.stats_from_bytes(r) for r in rec_stats.cpu().numpy()]
     evicted = [s_["evicted_blocks"] for s_ in st_steps]
+    # hit accounting of every timed step (device counters), summed over ranks: rank-local hits and
+    # box-level hits (this rank's index or the residency map, §8(e))
+    hb = torch.tensor([sum(s_[f] for s_ in st_steps) for f in ("hit_blocks", "box_hit_blocks", "full_blocks")],
+                      dtype=torch.float64, device=dev)
+    backlog = max(s_["record_backlog"] for s_ in st_steps)
+    if world > 1:
+        dist.all_reduce(hb)
     pl.ctx.status_sync(stream)
     if world > 1:
         dist.barrier()
-    step_ms = [e[0].elapsed_time(e[5]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
     stage_ms = {n: [e[i].elapsed_time(e[i + 1]) for e in evs] for i, n in enumerate(stage_names)}
     e2e_ms = [a.elapsed_time(b) for a, b in e2e_evs]
     work, hits, fulls, hit_tok, all_tok, mwork, mtouch = [], 0, 0, 0, 0, [], []
@@ -406,6 +433,13 @@ def run_ours(args, rank, world, local_rank):
                          "note": "untimed full batches after the ramp until the KV cache is full and a batch "
                                  "evicts; every timed step then runs LRU eviction (rank 0's counts)"},
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
+        "box_level": None if dp is None else {
+            "hit_pct_rank_local": 100.0 * float(hb[0]) / max(float(hb[2]), 1.0),
+            "hit_pct_box": 100.0 * float(hb[1]) / max(float(hb[2]), 1.0),
+            "note": "all ranks, all timed steps: leading blocks resident in the rank's own index vs in any rank's "
+                    "(the replicated residency map built from the all-gathered block records)",
+            "record_bytes_per_rank": dp.rec_bytes, "record_backlog_max": int(backlog),
+            "collective": "one all_gather_into_tensor of the record buffers per batch, overlapping il_select_batch"},
         "prefix_hit_pct_tokens": 100.0 * hit_tok / max(all_tok, 1),
         "pair": {"rule_counts": {"1_target": int(rules[1]), "2_unchanged": int(rules[2]), "3_modified": int(rules[3])},
                  "pmc_histogram": [int(x) for x in pmcs]},

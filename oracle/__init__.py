@@ -58,6 +58,10 @@ def lib():
         _lib.or_table_size.restype = C.c_uint32
         _lib.or_table_size.argtypes = [P]
         _lib.or_table_dump.argtypes = [P, u32p, u64p]
+        _lib.or_box_hits.argtypes = [P, u32p]
+        _lib.or_box_map_size.restype = C.c_uint32
+        _lib.or_box_map_size.argtypes = [P]
+        _lib.or_box_map_dump.argtypes = [P, u64p, u32p]
         _lib.or_similarity.argtypes = [C.c_uint32, u32p, C.c_uint32, u32p, C.c_uint32, u64p, u64p, f64p]
         _lib.or_select.argtypes = [P, u32p, C.c_uint32, C.c_uint32, u32p]
         _lib.or_pmc.restype = C.c_uint32
@@ -161,6 +165,8 @@ class Oracle:
         if rc:
             raise RuntimeError(f"or_run_batch_dp rc={rc}")
         res = BatchResult(topk, fin, info, tst, plen, ptok, bh, hit, ev[:nev[0]].copy())
+        res.box_hit = np.zeros(B, np.uint32)
+        lib().or_box_hits(ranks[0].h, _p(res.box_hit, C.c_uint32))
         off = np.concatenate([[0], np.cumsum(nrank.astype(np.int64))])
         res.evicted_rank = [res.evicted[off[r]:off[r + 1]] for r in range(G)]
         return res
@@ -176,6 +182,12 @@ class Oracle:
         lib().or_index_dump(self.h, _p(h, C.c_uint64), _p(st, C.c_uint64), _p(dp, C.c_uint32),
                             _p(par, C.c_uint64))
         return h, st, dp, par
+
+    def box_map_dump(self):
+        n = lib().or_box_map_size(self.h)
+        h = np.zeros(n, np.uint64); m = np.zeros(n, np.uint32)
+        lib().or_box_map_dump(self.h, _p(h, C.c_uint64), _p(m, C.c_uint32))
+        return h, m
 
     def table_dump(self):
         n = lib().or_table_size(self.h)

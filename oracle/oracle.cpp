@@ -44,6 +44,10 @@ struct or_state {
   std::map<std::vector<u32>, u64> table;   // ICL Table: DS tuple -> stamp (P:354 OrderedDict, Z2)
   std::map<u64, Block> index;              // prefix cache: chain hash -> resident block
   u64 batch = 0;                           // b of the last committed batch
+  // data-parallel: replicated residency map, chain hash -> owner-rank bitmask, and
+  // the box-level hit counts of the last batch
+  std::map<u64, u32> box;
+  std::vector<u32> last_box;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -282,6 +286,8 @@ int or_pool_load(or_state* s, u32 n, const u32* log_off, const u32* log_tok, con
   s->instr.assign(instr, instr + n_instr);
   s->table.clear();                                  // demo ids change: reset (il.h pool_load)
   s->index.clear();
+  s->box.clear();
+  s->last_box.clear();
   s->batch = 0;
   s->loaded = true;
   return 0;
@@ -308,7 +314,7 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
   std::vector<std::vector<u32>> q(B), cur(B), prompt(B);
   std::vector<std::vector<u64>> H(B);
   std::vector<Refined> ref(B);
-  std::vector<u32> h(B);
+  std::vector<u32> h(B), boxh(B);
   std::vector<int> err(B, 0);
 
   // Steps 1-6 per request against the snapshot (Z1) of its rank.
@@ -324,7 +330,17 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     prompt[i] = render(s, ref[i].final_ds, q[i]);
     if (prompt[i].size() > prompt_stride || prompt[i].size() / BS > max_blocks) { err[i] = 1; continue; }
     H[i] = chain_hashes(s->seed, prompt[i]);
-    h[i] = cap_hits(leading_hits(s, prompt[i], H[i]), prompt[i].size());
+    const u32 hl = leading_hits(s, prompt[i], H[i]);
+    h[i] = cap_hits(hl, prompt[i].size());
+    // box-level hits: the rank's own leading run, continued through blocks the residency map
+    // (the union of every rank's index at the snapshot) holds; hash only, capped as Z20
+    u32 hb = hl;
+    while (hb < H[i].size()) {
+      auto it = s->box.find(H[i][hb]);
+      if (it == s->box.end() || it->second == 0) break;
+      hb += 1;
+    }
+    boxh[i] = cap_hits(hb, prompt[i].size());
   }
   for (u32 i = 0; i < B; ++i) if (err[i]) return err[i];
 
@@ -367,7 +383,8 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     for (u64 v : victims[r]) st[r]->index.erase(v);
 
   // Step 9: insert the new full blocks in admission order, each into its rank's index; first
-  // wins (Z22).
+  // wins (Z22).  The blocks a rank's index gains or loses are its block records (§8(e)).
+  std::vector<std::vector<u64>> gained(G);
   for (u32 i = 0; i < B; ++i) {
     or_state* s = st[owner[i]];
     const u32 il = i - lo[owner[i]];
@@ -382,9 +399,24 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
         blk.depth = j;
         blk.stamp = stamp_of(b, il);
         s->index[H[i][j]] = blk;
+        gained[owner[i]].push_back(H[i][j]);
       }
     }
   }
+  // The residency map (replicated on every rank): each rank's lost and gained blocks toggle its
+  // owner bit, so the map is the union of the ranks' indices with their owner sets.
+  for (u32 r = 0; r < G; ++r) {
+    for (u32 q = 0; q < G; ++q) {
+      auto& bx = st[q]->box;
+      for (const auto* lst : {&victims[r], &gained[r]})
+        for (u64 x : *lst) {
+          u32& m = bx[x];
+          m ^= 1u << r;
+          if (m == 0) bx.erase(x);
+        }
+    }
+  }
+  for (u32 r = 0; r < G; ++r) st[r]->last_box = boxh;
 
   // Step 10: ICL Table commit (Z2, Z3, Z14), all B records on every rank.  Rule 1
   // refreshes the target (its key IS final_ds); rules 2/3 and reverted requests upsert
@@ -454,6 +486,14 @@ void or_index_dump(const or_state* s, u64* hash, u64* stamp, u32* depth, u64* pa
   }
 }
 u32 or_table_size(const or_state* s) { return (u32)s->table.size(); }
+void or_box_hits(const or_state* s, u32* out) {
+  for (size_t i = 0; i < s->last_box.size(); ++i) out[i] = s->last_box[i];
+}
+u32 or_box_map_size(const or_state* s) { return (u32)s->box.size(); }
+void or_box_map_dump(const or_state* s, u64* hash, u32* mask) {
+  size_t n = 0;
+  for (auto& e : s->box) { hash[n] = e.first; mask[n] = e.second; ++n; }
+}
 void or_table_dump(const or_state* s, u32* ds, u64* stamp) {
   std::vector<std::pair<u64, const std::vector<u32>*>> v;
   for (auto& e : s->table) v.push_back({e.second, &e.first});

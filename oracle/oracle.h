@@ -59,6 +59,13 @@ int or_run_batch_dp(or_state** st, uint32_t G, uint32_t B, const uint32_t* q_off
                     uint32_t* hit, uint64_t* evicted, uint32_t* n_evicted, uint32_t* n_evicted_rank);
 
 uint64_t or_batch_index(const or_state*);           /* b of the last committed batch */
+/* SURVEY §8(e) residency map (replicated on every rank of a run_batch_dp): chain hash -> bitmask
+ * of the ranks whose index holds it, i.e. the union of the ranks' indices after the batch; and
+ * the box-level hit counts of the last batch ([B]): each request's own leading run continued
+ * through blocks present in the map at the snapshot (hash only), capped as Z20. */
+void or_box_hits(const or_state*, uint32_t* out);
+uint32_t or_box_map_size(const or_state*);
+void or_box_map_dump(const or_state*, uint64_t* hash, uint32_t* mask);   /* sorted by hash */
 uint32_t or_index_size(const or_state*);
 /* sorted by hash: hash, stamp, depth, parent hash */
 void or_index_dump(const or_state*, uint64_t* hash, uint64_t* stamp, uint32_t* depth, uint64_t* parent);

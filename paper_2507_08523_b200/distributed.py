@@ -4,10 +4,12 @@ The hot path shards by request: rank r takes the r-th contiguous slice of every 
 keeps its own KV pages and prefix index, and runs the whole path on its slice.  The only
 exchanges are
   (1) the demo pool, broadcast once from rank 0 (`broadcast_pool`);
-  (2) per batch, one all-gather of the per-request ICL records (final DS + il_refine_info),
-      which every rank applies in global admission order (il_commit_records), so the ICL Table
-      stays replicated and every rank refines the next batch against the same snapshot
-      (P:356-363 applied to the whole global batch; oracle: run_batch_dp).
+  (2) per batch, one all-gather of a fixed-size record buffer per rank (il_commit_export): the
+      per-request ICL records (final DS + il_refine_info), which every rank applies in global
+      admission order, so the ICL Table stays replicated and every rank refines the next batch
+      against the same snapshot (P:356-363 applied to the whole global batch), and the rank's
+      block records (prefix-index updates), which build the replicated residency map hash ->
+      owner ranks and the box-level hit counts (oracle: run_batch_dp).
 Nothing else moves: no KV pages, no requests.  This module is plumbing (slicing, collectives,
 argument marshalling); every step of the path runs in the library's kernels.
 """
@@ -64,40 +66,103 @@ def all_gather_rows(out: torch.Tensor, local: torch.Tensor, group=None) -> torch
 
 class DataParallel:
     """Wraps one rank's Pipeline.  Every rank must call every method (collectives); slices are
-    equal-sized (the global batch is world x B)."""
+    equal-sized (the global batch is world x B).
+
+    Per batch b the exchange is ONE all-gather of a fixed-size record buffer per rank
+    (il_commit_export: the rank's ICL records + the blocks its prefix index gained or lost),
+    issued on a side stream so that it overlaps batch b+1's kNN selection (il_select_batch reads
+    only the pool); il_commit_apply then applies every rank's records: the replicated ICL Table
+    (global admission order) and the replicated residency map (box-level hits).
+
+        select(b+1) | all-gather(b) on the comm stream
+        apply(b) -> refine(b+1) -> match -> synth -> attn -> commit_index -> export(b+1) -> ...
+    """
 
     def __init__(self, pl, group=None):
         self.pl, self.group = pl, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         if pl.cfg.max_global_batch < self.world * pl.cfg.max_batch:
             raise ValueError("Config.max_global_batch must be >= world * max_batch")
-        B, k, dev = pl.cfg.max_batch, pl.cfg.k, pl.device
-        self.final_ds_all = torch.zeros(self.world * B, k, dtype=torch.int32, device=dev)
-        self.info_all = torch.zeros(self.world * B, 16, dtype=torch.uint8, device=dev)
+        dev = pl.device
+        self.rec_bytes = pl.cfg.record_bytes()
+        self.rec = torch.zeros(self.rec_bytes, dtype=torch.uint8, device=dev)
+        self.rec_all = torch.zeros(self.world * self.rec_bytes, dtype=torch.uint8, device=dev)
+        self.comm = torch.cuda.Stream(dev)
+        self.gathered = None          # event: the last all-gather finished (records not yet applied)
+        self.pending_B = 0
 
     def load_pool(self, pool, instr) -> None:
         p, ins = broadcast_pool(pool if self.rank == 0 else None, instr if self.rank == 0 else None,
                                 self.pl.device, 0, self.group)
         self.pl.load_pool(p, ins)
 
-    def commit(self, B=None) -> None:
-        """il_commit_index, all-gather of the ICL records, il_commit_records (global order)."""
+    def _main(self):
+        return self.pl.stream if self.pl.stream is not None else torch.cuda.current_stream(self.pl.device)
+
+    # ------------------------------------------------------------ stages (each capturable)
+    def select(self, B=None) -> None:
         pl = self.pl
         B = pl.B if B is None else B
+        pl.ctx.select_batch(B, pl.q_off, pl.q_tok, pl.q_src, pl.topk, stream=pl.stream)
+
+    def wait_gathered(self) -> None:
+        """Make the main stream wait for the pending all-gather (an event wait)."""
+        if self.gathered is not None:
+            self._main().wait_event(self.gathered)
+            self.gathered = None
+
+    def apply_records(self) -> None:
+        """il_commit_apply of the gathered buffers (every rank's records; ends that batch).  No
+        stream wait: capturable in a CUDA graph; call wait_gathered() first."""
+        self.pl.ctx.commit_apply(self.rec_all, [self.pending_B] * self.world, stream=self.pl.stream)
+
+    def apply(self) -> None:
+        """Wait for the pending all-gather and apply every rank's records (ends that batch)."""
+        if self.gathered is None:
+            return
+        self.wait_gathered()
+        self.apply_records()
+
+    def export(self, B=None) -> None:
+        """il_commit_index + il_commit_export of this rank's batch into its record buffer."""
+        pl = self.pl
         pl.ctx.commit_index(stream=pl.stream)
-        with torch.cuda.stream(pl.stream) if pl.stream is not None else _nullctx():
-            all_gather_rows(self.final_ds_all, pl.final_ds[:B], self.group)
-            all_gather_rows(self.info_all, pl.info[:B], self.group)
-        pl.ctx.commit_records(self.world * B, self.final_ds_all, self.info_all, stream=pl.stream)
+        pl.ctx.commit_export(self.rec, stream=pl.stream)
+        self.pending_B = pl.B if B is None else B
+
+    def gather(self) -> None:
+        """All-gather the record buffers (rank-major) on the comm stream, after the export."""
+        main = self._main()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.comm.wait_event(ev)
+        with torch.cuda.stream(self.comm):
+            all_gather_rows(self.rec_all.view(self.world, -1), self.rec.view(1, -1), self.group)
+            done = torch.cuda.Event()
+            done.record(self.comm)
+        self.gathered = done
+
+    def commit(self, B=None) -> None:
+        """The whole exchange for this batch, not overlapped: export, all-gather, apply."""
+        self.export(B)
+        self.gather()
+        self.apply()
 
     def step(self, B=None, attention: bool = True) -> None:
+        """One batch, pipelined with the previous batch's exchange; call flush() after the last."""
         pl = self.pl
+        self.select(B)
+        self.apply()
         pl.refine(B)
         pl.match(B)
         if attention:
             pl.synth(B)
             pl.attn(B)
-        self.commit(B)
+        self.export(B)
+        self.gather()
+
+    def flush(self) -> None:
+        self.apply()
 
 
 class _nullctx:

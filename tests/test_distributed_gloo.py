@@ -44,6 +44,15 @@ def _worker(rank, world, port, q):
         all_gather_rows(out_i, inf)
         want_f = np.array([[1000 * i + j for j in range(3)] for i in range(B)])
         ok_rec = np.array_equal(out_f.numpy(), want_f) and np.array_equal(out_i.numpy()[:, 0], np.arange(B))
+        # the fused per-rank record buffer (il_commit_export layout: bytes): one row per rank
+        nbytes = 4096
+        buf = torch.full((1, nbytes), rank + 1, dtype=torch.uint8)
+        buf[0, :8] = torch.tensor(list(np.int64(rank * 7919).tobytes()), dtype=torch.uint8)
+        all_buf = torch.zeros(world, nbytes, dtype=torch.uint8)
+        all_gather_rows(all_buf, buf)
+        for r in range(world):
+            ok_rec &= bool((all_buf[r, 8:] == r + 1).all())
+            ok_rec &= int(np.frombuffer(all_buf[r, :8].numpy().tobytes(), np.int64)[0]) == r * 7919
         q.put((rank, ok_pool, ok_rec))
     finally:
         dist.destroy_process_group()

@@ -109,3 +109,41 @@ def test_dp_one_request_per_rank_is_sequential_kv_sim_per_rank(G):
             assert seq[g].lookup(p, capped=True) == int(r.hit[g]), (b, g)
             seq[g].insert(p)
             assert (ranks[g].index_dump()[0] == seq[g].index_dump()[0]).all(), (b, g)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_dp_residency_map_is_union_of_rank_indices_and_box_hits_are_box_prefixes(G):
+    """§8(e) residency map: after every batch, on every rank, hash -> owner mask equals the union
+    of the ranks' prefix indices (brute force from the index dumps); a request's box-level hit is
+    the longest leading run of its blocks resident on ANY rank at the snapshot (brute force from
+    the previous batch's dumps), capped as Z20; it is >= the rank-local hit and equal to it at G = 1."""
+    sp = StreamSpec(B=96, C=1800 // G, n_logs=2000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
+    ds, pool, instr = make_stream(sp)
+    ranks = _ranks(sp, pool, instr, G)
+    prev_union = {}
+    gained_on_others = 0
+    for b in range(10):
+        r = O.Oracle.run_batch_dp(ranks, gen.make_batch(ds, b * sp.B, sp.B), prompt_stride=sp.max_prompt_tokens,
+                                  max_blocks=sp.max_prompt_tokens // 16)
+        for i in range(sp.B):
+            L = int(r.prompt_len[i])
+            chain = [int(x) for x in r.block_hash[i, :L // 16]]
+            run = 0
+            while run < len(chain) and chain[run] in prev_union:
+                run += 1
+            want = min(max(run, int(r.hit[i])), max(L - 1, 0) // 16)
+            assert int(r.box_hit[i]) == want, (b, i)
+            assert r.box_hit[i] >= r.hit[i]
+            if G == 1:
+                assert r.box_hit[i] == r.hit[i]
+            gained_on_others += int(r.box_hit[i] > r.hit[i])
+        union = {}
+        for g, o in enumerate(ranks):
+            for x in o.index_dump()[0]:
+                union[int(x)] = union.get(int(x), 0) | (1 << g)
+        for o in ranks:
+            h, m = o.box_map_dump()
+            assert dict(zip((int(x) for x in h), (int(y) for y in m))) == union, b
+        prev_union = union
+    if G > 1:
+        assert gained_on_others > 0          # remote residency is visible in the box-level hits
