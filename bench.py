@@ -189,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
         pl.load_inputs(*x)                             # device-to-device into the resident input buffers
 
     # ---- cold-start ramp, then fill until a batch evicts (untimed; all ranks stop together)
-    stats_dev = torch.zeros(64, dtype=torch.uint8, device=dev)
+    stats_dev = torch.zeros(128, dtype=torch.uint8, device=dev)
     j = 0
     with torch.cuda.stream(stream):
         for j in range(n_ramp + n_fill_max):
@@ -226,7 +226,7 @@ def run_ours(args, rank, world, local_rank):
     rec_hit = torch.zeros(K, cfg.B, dtype=torch.int32, device=dev)
     rec_bt = torch.zeros(K, cfg.B, ccfg.max_blocks, dtype=torch.int32, device=dev)
     rec_info = torch.zeros(K, cfg.B, 16, dtype=torch.uint8, device=dev)
-    rec_stats = torch.zeros(2 * K, 64, dtype=torch.uint8, device=dev)   # il_stats after every timed step
+    rec_stats = torch.zeros(2 * K, 128, dtype=torch.uint8, device=dev)   # il_stats after every timed step
 
     # ---- warm-up (W full steps in the eviction regime), not timed
     with torch.cuda.stream(stream):

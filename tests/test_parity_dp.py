@@ -136,7 +136,7 @@ def test_dp8_guard():
 
 
 def test_dp4_small_record_window_backlog():
-    # 48 block records per export: cold batches queue records in the FIFO (backlog), the table,
+    # 8 block records per export: most batches queue records in the FIFO (backlog), the table,
     # index and hits stay exact, box-level hits stay >= local hits, nothing latches
     sp = StreamSpec(B=64, C=700, n_logs=3000, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4, 16))
-    run_dp(sp, G=4, n_batches=14, rec_R=48)
+    run_dp(sp, G=4, n_batches=14, rec_R=8)
