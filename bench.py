@@ -62,7 +62,8 @@ def n_queries_for(cfg, args, world: int) -> int:
 
 def workload(cfg_n: int, rank: int, world: int, n_queries: int = 0):
     """Config dataset, grown (same generator, same seed) to at least n_queries logs so that no
-    query repeats inside the run: the paper parses every log once."""
+    query repeats inside the run: the paper parses every log once.  (Config 2's 16
+    datasets run through run_c2.)"""
     cfg = gen.config(cfg_n)
     name, n, nt, s, seed = cfg.datasets[0]
     ds = gen.make_dataset(name, max(n, n_queries), nt, s, seed)
@@ -470,6 +471,91 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------------------------
+def run_c2(args, rank, world, local_rank):
+    """BASELINE configs[1]: all 16 Loghub-2k-shaped datasets, each from a FRESH pool,
+    ICL Table and prefix cache, all 2,000 logs of the dataset as 8 batches of up to 256 concurrent
+    requests (the paper's per-dataset cold run), with PAIR and again with naive prefix
+    caching (PAIR off, the paper's baseline PC).  Every batch is device-timed with CUDA
+    events on the launching stream (L2 flushed before each).  value = total requests / total time
+    of the PAIR runs; per dataset: requests/s, block- and token-weighted hits, PAIR / naive hit
+    ratio.  One GPU; ranks > 0 exit (the datasets are independent problems)."""
+    import torch
+    from paper_2507_08523_b200 import IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
+    if rank != 0:
+        return
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = gen.config(2)
+    stream = torch.cuda.Stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    per, tot_req, tot_ms = [], 0, 0.0
+    clocks = ClockSampler(local_rank)
+    launches = 0
+    for (name, n, nt, zs, seed) in cfg.datasets:
+        ds = gen.make_dataset(name, n, nt, zs, seed)
+        pool = gen.sample_pool(ds, cfg.M, cfg.pool_seed)
+        instr = gen.instruction(cfg.n_instr, cfg.instr_seed)
+        row = {"dataset": name, "templates": nt}
+        for mode, flags in (("pair", IL_F_PAIR | IL_F_VERIFY | (0 if args.no_guard else IL_F_GUARD)),
+                            ("naive", IL_F_VERIFY)):
+            ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
+                          max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
+                          max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                          max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
+                          head_dim=cfg.d, flags=flags)
+            pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
+            with torch.cuda.stream(stream):
+                pl.load_pool(pool, instr)
+            batches = [gen.make_batch(ds, s0, min(cfg.B, ds.n - s0)) for s0 in range(0, ds.n, cfg.B)]
+            ins = [(torch.from_numpy(b.q_off.view(np.int32)).to(dev), torch.from_numpy(b.q_tok.view(np.int32)).to(dev),
+                    torch.from_numpy(b.q_src.view(np.int32)).to(dev), b.B) for b in batches]
+            l0 = pl.launches()
+            evs, hits, fulls, htok, atok = [], 0, 0, 0, 0
+            stats = torch.zeros(len(ins), 128, dtype=torch.uint8, device=dev)
+            lens = []
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                for j, x in enumerate(ins):
+                    flush.zero_()
+                    pl.load_inputs(*x)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    pl.step()
+                    e1.record(stream)
+                    pl.ctx.stats_async(stats[j], stream=stream)
+                    evs.append((e0, e1))
+                    lens.append((pl.prompt_len[:x[3]].clone(), pl.hit[:x[3]].clone()))
+            torch.cuda.synchronize()
+            pl.ctx.status_sync(stream)
+            launches += pl.launches() - l0 - len(ins)
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+            for L_, H_ in lens:
+                L_ = L_.cpu().numpy().astype(np.int64); H_ = H_.cpu().numpy().astype(np.int64)
+                hits += int(H_.sum()); fulls += int((L_ // 16).sum()); htok += int(16 * H_.sum()); atok += int(L_.sum())
+            row[mode] = {"requests_per_s": ds.n / (ms * 1e-3), "ms": ms, "block_hit_pct": 100.0 * hits / max(fulls, 1),
+                         "token_hit_pct": 100.0 * htok / max(atok, 1)}
+            if mode == "pair":
+                tot_req += ds.n; tot_ms += ms
+            del pl
+        row["pair_over_naive_block_hit"] = row["pair"]["block_hit_pct"] / max(row["naive"]["block_hit_pct"], 1e-9)
+        per.append(row)
+    clk = clocks.stop()
+    hp = [r["pair"]["block_hit_pct"] for r in per]; hn = [r["naive"]["block_hit_pct"] for r in per]
+    line = {"metric": METRIC, "value": tot_req / (tot_ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": len(per),
+            "warmup": 0, "ms_per_step": tot_ms / max(sum(len(range(0, 2000, cfg.B)) for _ in per), 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg.name, "baseline_config": "configs[1]", "datasets": 16,
+                       "requests_per_dataset": 2000, "batch": cfg.B, "k": cfg.k, "pool": cfg.M,
+                       "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
+                       "protocol": "per dataset: fresh pool/table/cache, cold start, every log once (P:515); "
+                                   "a step = one batch; L2 flushed before every batch"},
+            "block_hit_pct_mean": {"pair": float(np.mean(hp)), "naive": float(np.mean(hn)),
+                                   "ratio_of_means": float(np.mean(hp) / max(np.mean(hn), 1e-9))},
+            "per_dataset": per, "gpu_launches": int(launches), "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
 def oracle_sample(cfg, ds, pool, instr, plan, n_warm, flags, n_attn: int, n_steps: int = 1):
     """The CPU oracle as it stands: replay the warm-up batches (untimed), then time the integer
     path over full batches and fp64 attention over a sample of their requests."""
@@ -658,7 +744,10 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.config == 2:
+        run_c2(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

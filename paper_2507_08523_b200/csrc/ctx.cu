@@ -77,6 +77,18 @@ static size_t carve(Ctx* c, void* ws) {
   c->attn_ml = w.take<float>((size_t)g.max_suffix_tokens * g.n_q_heads);
   c->evicted_list = w.take<uint64_t>(C);
   c->guard_prompt = (g.flags & IL_F_GUARD) ? w.take<uint32_t>(B * g.max_prompt_tokens) : nullptr;
+  // inverted index for large pools (a1-a2, select_inv.cu): slots for every (token, chunk) key
+  if (g.max_pool > SIM_BIG_POOL) {
+    uint32_t n = 1024;
+    while (n < 2 * PT) n <<= 1;
+    c->inv_slots = n; c->inv_mask = n - 1;
+    c->inv_key = w.take<uint64_t>(n);
+    c->inv_off = w.take<uint32_t>(n); c->inv_len = w.take<uint32_t>(n); c->inv_fill = w.take<uint32_t>(n);
+    c->post_demo = w.take<uint32_t>(PT); c->post_cnt = w.take<uint32_t>(PT);
+  } else {
+    c->inv_slots = c->inv_mask = 0;
+    c->inv_key = nullptr; c->inv_off = c->inv_len = c->inv_fill = c->post_demo = c->post_cnt = nullptr;
+  }
   // multi-GPU exchange: block-record FIFO, residency map (2 x ranks x C slots), box hits, gathered
   // ICL records
   c->n_ranks_max = g.max_global_batch > B ? (uint32_t)((g.max_global_batch + B - 1) / B) : 1;
@@ -299,7 +311,7 @@ il_status il_create(const il_config* cfg, void* ws, size_t bytes, il_stream s, i
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  for (il_status (*f)(Ctx*) : {match_setup, commit_setup, attn_setup, records_setup}) {
+  for (il_status (*f)(Ctx*) : {match_setup, commit_setup, attn_setup, records_setup, inv_setup}) {
     st = f(c);
     if (st) { delete c; return st; }
   }
@@ -408,6 +420,7 @@ il_status il_pool_load(il_ctx* c, uint32_t n, const uint32_t* log_off, const uin
   k_pool_sets<<<cdiv(n, 8), 256, 0, st>>>(*c, n, log_off, log_tok);
   k_pool_scan<<<1, 1024, 0, st>>>(*c, n);
   k_pool_render<<<cdiv(n * 32, 256), 256, 0, st>>>(*c, n);
+  if (il_status r = inv_build(c, n, st)) return r;
   if (n_instr / BS) k_instr_hash<<<1, 32, 0, st>>>(*c, n_instr / BS);
   IL_LAUNCH_CHECK("pool_load kernels");
   c->n_demos = n;

@@ -18,6 +18,11 @@ constexpr uint64_t KEY_EMPTY = 0ull;
 constexpr uint64_t KEY_TOMB = ~0ull;
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 constexpr int MAXK = 8;
+// a1-a2 for pools above this many demos use the inverted index (select_inv.cu) instead of the
+// per-query pool scan; the index holds the pool in chunks of SIM_CHUNK demos (one shared-memory
+// accumulator each)
+constexpr uint32_t SIM_BIG_POOL = 1024;
+constexpr uint32_t SIM_CHUNK = 16384;
 
 // Device-resident scalars (one 256 B line).
 struct DevScalars {
@@ -102,6 +107,12 @@ struct Ctx {
   float *attn_ml;            // cascade: per row log2 softmax mass of the shared-prefix partial
   uint64_t *evicted_list;
   uint32_t *guard_prompt;    // guard: DS_current prompt rows
+  // inverted index of the pool (select_inv.cu; allocated when max_pool > SIM_BIG_POOL):
+  // key (token, chunk) -> posting list of (demo, count)
+  uint32_t inv_slots = 0, inv_mask = 0;
+  uint64_t *inv_key;         // ((chunk << 32) | token) + 1; 0 = empty
+  uint32_t *inv_off, *inv_len, *inv_fill;
+  uint32_t *post_demo, *post_cnt;
   // multi-GPU exchange (records.cu; allocated when max_global_batch > max_batch)
   uint32_t n_ranks_max = 1;  // ceil(max_global_batch / max_batch)
   uint32_t rec_R = 0;        // block records per export
@@ -144,6 +155,10 @@ il_status commit_setup(Ctx* c);
 il_status attn_setup(Ctx* c);
 il_status records_setup(Ctx* c);
 il_status records_reset(Ctx* c, cudaStream_t st);
+il_status inv_build(Ctx* c, uint32_t n_demos, cudaStream_t st);       // select_inv.cu (pool_load)
+il_status inv_select(Ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
+                     const uint32_t* q_src, uint32_t* topk, cudaStream_t st);
+il_status inv_setup(Ctx* c);
 // shared between commit.cu and records.cu
 il_status commit_table(Ctx* c, uint32_t B, const uint32_t* final_ds, const il_refine_info* info,
                        cudaStream_t st, uint64_t b_cur);

@@ -2,6 +2,7 @@
 // reorder, rules, guard) + prompt render.
 #include "il_internal.cuh"
 #include "match_dev.cuh"
+#include "sim_dev.cuh"
 
 namespace il {
 
@@ -18,45 +19,11 @@ namespace il {
 constexpr int SIM_THREADS = 128;               // 4 warps = 4 queries per CTA
 constexpr int QHASH = 512;
 
-struct Cand {
-  uint64_t num, den;
-  uint32_t idx;
-};
-__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {   // a ranks before b
-  const uint64_t l = a.num * b.den, r = b.num * a.den;                   // < 2^48: exact in u64
-  return l > r || (l == r && a.idx < b.idx);
-}
-// k rounds of warp argmax over the lanes' sorted lists (get(q) = the lane's q-th best, n of
-// them); the winning lane pops its head.  `better` is a strict total order (index breaks score
-// ties), so the result does not depend on lane order.  Picks go to out[0..n) best first.
-template <class Get>
-__device__ __forceinline__ uint32_t warp_merge(Get get, uint32_t n, uint32_t k, uint32_t lane, Cand* out) {
-  uint32_t head = 0, npick = 0;
-  for (uint32_t r = 0; r < k; ++r) {
-    Cand w;
-    uint32_t wl = NONE32;
-    if (head < n) { w = get(head); wl = lane; } else { w.num = 0; w.den = 1; w.idx = NONE32; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      Cand o_;
-      o_.num = __shfl_xor_sync(~0u, w.num, o); o_.den = __shfl_xor_sync(~0u, w.den, o);
-      o_.idx = __shfl_xor_sync(~0u, w.idx, o);
-      const uint32_t ol = __shfl_xor_sync(~0u, wl, o);
-      if (ol != NONE32 && (wl == NONE32 || better(o_, w))) { w = o_; wl = ol; }
-    }
-    if (wl == NONE32) break;                             // (uniform: every lane holds the winner)
-    if (lane == 0) out[r] = w;
-    if (lane == wl) ++head;
-    ++npick;
-  }
-  return npick;
-}
 __device__ __forceinline__ uint32_t qslot(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 9); }
 
 // QW warps per query (the CTA's 4 warps serve 4 / QW queries): QW = 1 for pools up to
 // SIM_BIG_POOL demos (no block-wide rounds, most queries per SM), QW = 4 above (4x the lanes per
 // query when the scoring loop dominates).
-constexpr uint32_t SIM_BIG_POOL = 1024;
 #ifndef IL_SIM_QW_SMALL
 #define IL_SIM_QW_SMALL 2
 #endif
@@ -422,6 +389,8 @@ using namespace il;
 // a1 + a2: exact similarity against the whole pool, top-k in ascending order
 static il_status select_launch(Ctx* c, uint32_t B, const uint32_t* q_off, const uint32_t* q_tok,
                                const uint32_t* q_src, uint32_t* topk, cudaStream_t st) {
+  if (c->n_demos > SIM_BIG_POOL && c->inv_slots)
+    return inv_select(c, B, q_off, q_tok, q_src, topk, st);
   if (c->n_demos > SIM_BIG_POOL)
     k_sim_topk<4><<<cdiv(B, SIM_THREADS / 128), SIM_THREADS, 0, st>>>(*c, B, q_off, q_tok, q_src, topk);
   else

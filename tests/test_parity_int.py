@@ -117,3 +117,40 @@ def test_c4_full_pool_10k_k8():
         pl.ctx.status_sync()
         compare_batch(r, pl, cfg.B, sp, where=f"c4 batch {b}")
         compare_state(o, pl, where=f"c4 batch {b}")
+
+
+def test_large_pool_jaccard_exclude_self():
+    # inverted-index selection (pool > 1,024 demos) with Jaccard over token sets and self-exclusion
+    sp = StreamSpec(n_logs=6000, n_templates=300, zipf=1.3, M=3000, k=5, B=128, T=256, C=4096,
+                    max_prompt_tokens=1024, n_batches=4, metric=O.SIM_JACCARD,
+                    flags=O.F_PAIR | O.F_VERIFY | O.F_EXCLUDE_SELF)
+    run_stream(sp, state_every=2)
+
+
+def test_multi_chunk_pool_20k():
+    # 20,000 demos = two 16,384-demo chunks of the inverted index (accumulators per chunk, top-k
+    # carried across chunks), cosine, k = 8
+    sp = StreamSpec(n_logs=40000, n_templates=1000, zipf=1.3, M=20000, k=8, B=96, T=512, C=8192,
+                    max_prompt_tokens=1536, n_batches=3)
+    run_stream(sp, state_every=3)
+
+
+def test_c5_pool_50k_selection():
+    """BASELINE configs[4] selection: the 50,000-demo pool sampled from the full 10,485,760-log
+    stream (bench.workload(5)), k = 5, four chunks of the inverted index; two batches of 128
+    requests bit-exact (the oracle scores every demo of the pool for every query)."""
+    import bench
+    cfg, ds, pool, instr = bench.workload(5, 0, 1)
+    sp = StreamSpec(M=cfg.M, k=cfg.k, B=128, n_instr=cfg.n_instr, T=cfg.T, C=8192,
+                    max_prompt_tokens=cfg.max_prompt_tokens, Hq=cfg.Hq, Hkv=cfg.Hkv, d=cfg.d,
+                    flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD)
+    o = oracle_for(sp, pool, instr)
+    pl = gpu_pipeline(sp, pool, instr)
+    for b in range(2):
+        batch = gen.make_batch(ds, b * sp.B, sp.B)
+        r = o.run_batch(batch, prompt_stride=sp.max_prompt_tokens, max_blocks=sp.max_prompt_tokens // 16)
+        pl.stage_batch(batch)
+        pl.refine(); pl.match(); pl.commit()
+        pl.ctx.status_sync()
+        compare_batch(r, pl, sp.B, sp, where=f"c5 batch {b}")
+        compare_state(o, pl, where=f"c5 batch {b}")

@@ -250,6 +250,13 @@ def config(n: int) -> Config:
         return Config("c4-qwen14b-skewed", [("C4", 102400, 1000, 1.3, 5000)], M=10000, k=8,
                       B=1024, n_instr=128, T=2048, C=45056, Hq=40, Hkv=8, d=128,
                       pool_seed=5001, max_prompt_tokens=1536)
+    if n == 5:
+        # Loghub-2.0 scale (BASELINE configs[4]): a ~10M-log stream, 5,000 templates, a 50k-demo pool;
+        # 8 GPUs x 1,024 requests per global batch (k and the attention shape are unspecified there:
+        # the paper's default k = 5, and the Llama shape)
+        return Config("c5-loghub2-scale", [("C5", 10_485_760, 5000, 1.1, 6000)], M=50000, k=5, B=1024,
+                      n_instr=128, T=4096, C=73728, Hq=32, Hkv=8, d=128, pool_seed=6001,
+                      max_prompt_tokens=1024)
     raise ValueError(f"unknown config {n}")
 
 
