@@ -159,7 +159,7 @@ def run_ours(args, rank, world, local_rank):
         flags = IL_F_VERIFY
     ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
                   max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
-                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                   head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world)
     stream = torch.cuda.Stream(dev)
@@ -491,7 +491,9 @@ def run_c2(args, rank, world, local_rank):
     per, tot_req, tot_ms = [], 0, 0.0
     clocks = ClockSampler(local_rank)
     launches = 0
-    for (name, n, nt, zs, seed) in cfg.datasets:
+    # the first dataset once more in front, untimed: one-time costs (module load, first launches)
+    for d_ix, (name, n, nt, zs, seed) in enumerate([cfg.datasets[0]] + list(cfg.datasets)):
+        warm = d_ix == 0
         ds = gen.make_dataset(name, n, nt, zs, seed)
         pool = gen.sample_pool(ds, cfg.M, cfg.pool_seed)
         instr = gen.instruction(cfg.n_instr, cfg.instr_seed)
@@ -500,7 +502,7 @@ def run_c2(args, rank, world, local_rank):
                             ("naive", IL_F_VERIFY)):
             ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
                           max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
-                          max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                          max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                           max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                           head_dim=cfg.d, flags=flags)
             pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
@@ -534,11 +536,12 @@ def run_c2(args, rank, world, local_rank):
                 hits += int(H_.sum()); fulls += int((L_ // 16).sum()); htok += int(16 * H_.sum()); atok += int(L_.sum())
             row[mode] = {"requests_per_s": ds.n / (ms * 1e-3), "ms": ms, "block_hit_pct": 100.0 * hits / max(fulls, 1),
                          "token_hit_pct": 100.0 * htok / max(atok, 1)}
-            if mode == "pair":
+            if mode == "pair" and not warm:
                 tot_req += ds.n; tot_ms += ms
             del pl
         row["pair_over_naive_block_hit"] = row["pair"]["block_hit_pct"] / max(row["naive"]["block_hit_pct"], 1e-9)
-        per.append(row)
+        if not warm:
+            per.append(row)
     clk = clocks.stop()
     hp = [r["pair"]["block_hit_pct"] for r in per]; hn = [r["naive"]["block_hit_pct"] for r in per]
     line = {"metric": METRIC, "value": tot_req / (tot_ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": len(per),

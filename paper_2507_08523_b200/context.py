@@ -23,7 +23,7 @@ class Config:
     max_prompt_tokens: int
     max_pool: int
     max_pool_tokens: int
-    max_log_tokens: int = 256
+    max_log_tokens: int = 255
     max_suffix_tokens: int = 0          # 0 -> max_batch * max_prompt_tokens
     n_q_heads: int = 32
     n_kv_heads: int = 8

@@ -84,10 +84,10 @@ static size_t carve(Ctx* c, void* ws) {
     c->inv_slots = n; c->inv_mask = n - 1;
     c->inv_key = w.take<uint64_t>(n);
     c->inv_off = w.take<uint32_t>(n); c->inv_len = w.take<uint32_t>(n); c->inv_fill = w.take<uint32_t>(n);
-    c->post_demo = w.take<uint32_t>(PT); c->post_cnt = w.take<uint32_t>(PT);
+    c->post_demo = w.take<uint32_t>(PT);
   } else {
     c->inv_slots = c->inv_mask = 0;
-    c->inv_key = nullptr; c->inv_off = c->inv_len = c->inv_fill = c->post_demo = c->post_cnt = nullptr;
+    c->inv_key = nullptr; c->inv_off = c->inv_len = c->inv_fill = c->post_demo = nullptr;
   }
   // multi-GPU exchange: block-record FIFO, residency map (2 x ranks x C slots), box hits, gathered
   // ICL records
@@ -128,6 +128,9 @@ static il_status validate(const il_config* g) {
   if (g->max_prompt_tokens < 16 || (g->max_prompt_tokens % 16)) { set_error("max_prompt_tokens: multiple of 16"); return IL_ERR_ARG; }
   if (g->max_pool < g->k) { set_error("max_pool < k"); return IL_ERR_ARG; }
   if (g->max_log_tokens < 1 || g->max_log_tokens > 256) { set_error("max_log_tokens in 1..256"); return IL_ERR_ARG; }
+  if (g->max_pool > SIM_BIG_POOL && g->max_log_tokens > 255) {
+    set_error("pools above 1,024 demos (inverted-index selection) need max_log_tokens <= 255"); return IL_ERR_ARG;
+  }
   if (g->n_kv_heads < 1 || g->n_q_heads % g->n_kv_heads) { set_error("Hq % Hkv != 0"); return IL_ERR_ARG; }
   if (g->head_dim != 64 && g->head_dim != 128) { set_error("head_dim must be 64 or 128"); return IL_ERR_ARG; }
   if (g->n_q_heads / g->n_kv_heads > 8) { set_error("Hq / Hkv must be <= 8"); return IL_ERR_ARG; }

@@ -112,7 +112,7 @@ struct Ctx {
   uint32_t inv_slots = 0, inv_mask = 0;
   uint64_t *inv_key;         // ((chunk << 32) | token) + 1; 0 = empty
   uint32_t *inv_off, *inv_len, *inv_fill;
-  uint32_t *post_demo, *post_cnt;
+  uint32_t *post_demo;       // (demo - chunk * SIM_CHUNK) << 18 | count
   // multi-GPU exchange (records.cu; allocated when max_global_batch > max_batch)
   uint32_t n_ranks_max = 1;  // ceil(max_global_batch / max_batch)
   uint32_t rec_R = 0;        // block records per export

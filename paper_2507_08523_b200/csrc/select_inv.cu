@@ -76,14 +76,15 @@ __global__ void __launch_bounds__(256) k_inv_fill(Ctx c, uint32_t n) {
   for (uint32_t u = lane; u < nu; u += 32) {
     const uint32_t s = inv_find(c, inv_keyof(c.uniq_tok[a + u], ch));
     const uint32_t pos = c.inv_off[s] + atomicAdd(&c.inv_fill[s], 1u);
-    c.post_demo[pos] = m;
-    c.post_cnt[pos] = c.uniq_cnt[a + u];
+    c.post_demo[pos] = ((m - ch * SIM_CHUNK) << 18) | c.uniq_cnt[a + u];   // demo in chunk | count (<= 256)
   }
 }
 
 constexpr int INV_THREADS = 256;
 constexpr int INV_QHASH = 512;
-constexpr uint32_t INV_SMEM = SIM_CHUNK * 4;      // the per-chunk accumulator (dynamic smem)
+constexpr uint32_t INV_SMEM = SIM_CHUNK * 2;      // the per-chunk accumulator: 16-bit per demo, two per word
+// (dot <= 255 x 255 < 2^16 with logs of <= 255 tokens (validate), so a half never carries into
+// the other)
 
 __device__ __forceinline__ uint32_t inv_qslot(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 9); }
 
@@ -93,12 +94,10 @@ __global__ void __launch_bounds__(INV_THREADS) k_sim_inv(Ctx c, uint32_t B, cons
                                                          const uint32_t* __restrict__ q_src,
                                                          uint32_t* __restrict__ topk) {
   constexpr uint32_t NW = INV_THREADS / 32;
-  extern __shared__ uint32_t s_acc[];                 // [SIM_CHUNK]
+  extern __shared__ uint32_t s_acc[];                 // [SIM_CHUNK / 2] packed u16 accumulators
   __shared__ uint32_t s_key[INV_QHASH], s_cnt[INV_QHASH];
   __shared__ uint32_t s_ut[256], s_uc[256], s_po[256], s_pre[257];
   __shared__ uint32_t s_nu, s_red[NW][2];
-  __shared__ uint64_t s_lnum[MAXK][INV_THREADS];
-  __shared__ uint32_t s_lden[MAXK][INV_THREADS], s_lidx[MAXK][INV_THREADS];
   __shared__ Cand s_wl[NW][MAXK], s_sel[MAXK];
   __shared__ uint32_t s_wn[NW];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -142,22 +141,29 @@ __global__ void __launch_bounds__(INV_THREADS) k_sim_inv(Ctx c, uint32_t B, cons
   const bool excl = (c.cfg.flags & IL_F_EXCLUDE_SELF) != 0;
   const uint32_t my_src = (excl && q_src) ? q_src[i] : NONE32;
 
-  Cand top[MAXK];
-#pragma unroll
-  for (int q = 0; q < MAXK; ++q) { top[q].num = 0; top[q].den = 1; top[q].idx = NONE32; }
-  uint32_t ntop = 0;
+  // one sorted top-k list per WARP: lane j < k holds entry j (best first).  Lanes score 32
+  // demos at a time; a demo whose fp32 quotient is clearly below the list's k-th entry (margin
+  // 2^-20, far above the quotients' rounding error) ranks below it exactly and is dropped; the
+  // few others are inserted one at a time with the exact comparison (warp-parallel insert).
+  Cand e;
+  e.num = 0; e.den = 1; e.idx = NONE32;
+  uint32_t nw = 0;                                      // entries in the warp's list (uniform)
+  float fk = 0.f;
+  Cand last = e;                                        // the list's k-th entry, in every lane
   const uint32_t n_chunks = cdiv(n, SIM_CHUNK);
   for (uint32_t ch = 0; ch < n_chunks; ++ch) {
     const uint32_t m0 = ch * SIM_CHUNK, mc = min(SIM_CHUNK, n - m0);
-    for (uint32_t x = tid; x < mc; x += INV_THREADS) s_acc[x] = 0;
-    // postings of the query's distinct tokens in this chunk
+    for (uint32_t x = tid; x < (mc + 1) / 2; x += INV_THREADS) s_acc[x] = 0;
+    __syncthreads();
+    // the postings of the query's distinct tokens in this chunk: token lookups, then their
+    // concatenation is cut into NW equal segments (warp w walks segment w: a long posting list
+    // is shared by several warps), lanes take 4 consecutive 32-wide rows of postings at a time
     uint32_t len = 0;
     if (tid < nuq) {
-      const uint32_t s = inv_find(c, inv_keyof(s_ut[tid], ch));
-      s_po[tid] = s == NONE32 ? 0u : c.inv_off[s];
-      len = s == NONE32 ? 0u : c.inv_len[s];
+      const uint32_t sl = inv_find(c, inv_keyof(s_ut[tid], ch));
+      s_po[tid] = sl == NONE32 ? 0u : c.inv_off[sl];
+      len = sl == NONE32 ? 0u : c.inv_len[sl];
     }
-    // prefix over the (<= 256) tokens: each thread holds at most one token
     {
       uint32_t x = len;
       for (int o = 1; o < 32; o <<= 1) {
@@ -168,61 +174,91 @@ __global__ void __launch_bounds__(INV_THREADS) k_sim_inv(Ctx c, uint32_t B, cons
       __syncthreads();
       uint32_t base = 0;
       for (uint32_t w = 0; w < wid; ++w) base += s_red[w][1];
-      if (tid < 256) s_pre[tid + 1] = base + x;
+      s_pre[tid + 1] = base + x;
       if (tid == 0) s_pre[0] = 0;
     }
     __syncthreads();
-    const uint32_t tot = s_pre[nuq];
-    for (uint32_t x = tid; x < tot; x += INV_THREADS) {
-      uint32_t lo = 0, hi = nuq;                        // token u: s_pre[u] <= x < s_pre[u + 1]
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_pre[mid] <= x) lo = mid; else hi = mid;
+    {
+      const uint32_t tot = s_pre[nuq], seg = cdiv(tot, NW);
+      const uint32_t x_lo = min(tot, wid * seg), x_hi = min(tot, x_lo + seg);
+      uint32_t u = 0;                                   // token holding x_lo: s_pre[u] <= x_lo < s_pre[u + 1]
+      {
+        uint32_t lo = 0, hi = nuq;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s_pre[mid] <= x_lo) lo = mid; else hi = mid;
+        }
+        u = lo;
       }
-      const uint32_t pos = s_po[lo] + (x - s_pre[lo]);
-      const uint32_t m = c.post_demo[pos];
-      atomicAdd(&s_acc[m - m0], jac ? 1u : s_uc[lo] * c.post_cnt[pos]);
+      for (uint32_t x0 = x_lo; x0 < x_hi;) {
+        while (s_pre[u + 1] <= x0) ++u;                  // (warp-uniform)
+        const uint32_t end = min(x_hi, s_pre[u + 1]);
+        const uint32_t off = s_po[u] - s_pre[u], cq = jac ? 1u : s_uc[u];
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t x = x0 + 32 * e + lane;
+          pk[e] = x < end ? __ldg(c.post_demo + (off + x)) : NONE32;   // (u32 sum: off may wrap)
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (pk[e] != NONE32) {
+            const uint32_t d = pk[e] >> 18;
+            atomicAdd(&s_acc[d >> 1], (jac ? 1u : cq * (pk[e] & 0x3FFFFu)) << (16 * (d & 1)));
+          }
+        x0 = min(end, x0 + 128);
+      }
     }
     __syncthreads();
-    // score every demo of the chunk exactly, keep a private sorted top list
-    for (uint32_t x = tid; x < mc; x += INV_THREADS) {
-      const uint32_t m = m0 + x;
-      if (excl && c.src[m] == my_src) continue;
-      const uint32_t acc = s_acc[x];
+    // score every demo of the chunk exactly; warp-level top-k
+    for (uint32_t x0 = wid * 32; x0 < mc; x0 += INV_THREADS) {
+      const uint32_t x = x0 + lane, m = m0 + x;
       Cand y;
-      y.idx = m;
-      if (jac) {
-        const uint32_t nu = c.uniq_n[m];
-        if (nuq == 0 && nu == 0) { y.num = 1; y.den = 1; }
-        else { y.num = acc; y.den = nuq + nu - acc; }
-      } else {
-        const uint32_t nm = c.norm2[m];
-        if (nq == 0 || nm == 0) { y.num = 0; y.den = 1; }                // zero norm (Z5)
-        else { y.num = (uint64_t)acc * acc; y.den = nm; }
+      y.num = 0; y.den = 1; y.idx = m;
+      bool cand = x < mc && !(excl && c.src[m] == my_src);
+      if (cand) {
+        const uint32_t acc = (s_acc[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
+        float fy;
+        if (jac) {
+          const uint32_t nu = c.uniq_n[m];
+          if (nuq == 0 && nu == 0) { y.num = 1; y.den = 1; }
+          else { y.num = acc; y.den = nuq + nu - acc; }
+          fy = __fdividef((float)y.num, (float)y.den);
+        } else {
+          const uint32_t nm = c.norm2[m];
+          if (nq != 0 && nm != 0) { y.num = (uint64_t)acc * acc; y.den = nm; }   // else 0 (Z5)
+          const float fa = (float)acc;
+          fy = y.num ? __fdividef(fa * fa, (float)y.den) : 0.f;
+        }
+        // (fy and fk: relative error < 2^-21 each, far inside the 2^-20 margin)
+        cand = nw < k || (fy >= fk && better(y, last));   // exact test only near the threshold
       }
-      if (ntop == MAXK && !better(y, top[MAXK - 1])) continue;          // fast reject
-      Cand prev = top[0];
-      bool bprev = better(y, prev);
-      if (bprev) top[0] = y;
-#pragma unroll
-      for (int q = 1; q < MAXK; ++q) {
-        const Cand cur = top[q];
-        const bool bq = better(y, cur);
-        if (bq) top[q] = bprev ? prev : y;
-        prev = cur;
-        bprev = bq;
+      uint32_t msk = __ballot_sync(~0u, cand);
+      while (msk) {
+        const uint32_t src = __ffs(msk) - 1;
+        msk &= msk - 1;
+        Cand cy;
+        cy.num = __shfl_sync(~0u, y.num, src); cy.den = __shfl_sync(~0u, y.den, src);
+        cy.idx = __shfl_sync(~0u, y.idx, src);
+        if (nw >= k && !better(cy, last)) continue;    // (uniform: an earlier insert raised the bar)
+        const bool bt = lane < k && (lane >= nw || better(cy, e));
+        const bool bl = __shfl_up_sync(~0u, bt, 1) && lane > 0;
+        Cand el;
+        el.num = __shfl_up_sync(~0u, e.num, 1); el.den = __shfl_up_sync(~0u, e.den, 1);
+        el.idx = __shfl_up_sync(~0u, e.idx, 1);
+        if (bt) e = bl ? el : cy;
+        nw = min(nw + 1, k);
+        if (nw == k) {
+          last.num = __shfl_sync(~0u, e.num, k - 1); last.den = __shfl_sync(~0u, e.den, k - 1);
+          last.idx = __shfl_sync(~0u, e.idx, k - 1);
+          fk = ((float)last.num / (float)last.den) * (1.f - 9.5367431640625e-7f);   // IEEE quotient (rare)
+        }
       }
-      ntop = min(ntop + 1, (uint32_t)MAXK);
     }
-    __syncthreads();                                    // s_acc, s_po, s_pre reused by the next chunk
+    __syncthreads();                                    // s_acc reused by the next chunk (and the merge)
   }
-  ntop = min(ntop, k);
-#pragma unroll
-  for (int q = 0; q < MAXK; ++q)
-    if ((uint32_t)q < ntop) { s_lnum[q][tid] = top[q].num; s_lden[q][tid] = (uint32_t)top[q].den; s_lidx[q][tid] = top[q].idx; }
-  __syncwarp();
-  const uint32_t nsel_w = warp_merge([&](uint32_t q) { Cand x; x.num = s_lnum[q][tid]; x.den = s_lden[q][tid]; x.idx = s_lidx[q][tid]; return x; },
-                                     ntop, k, lane, s_wl[wid]);
+  if (lane < k) s_wl[wid][lane] = e;
+  const uint32_t nsel_w = nw;
   if (lane == 0) s_wn[wid] = nsel_w;
   __syncthreads();
   if (wid != 0) return;

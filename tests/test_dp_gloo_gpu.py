@@ -41,7 +41,7 @@ def _worker(rank, world, port, q):
         ds, pool, instr = make_stream(sp)
         cfg = Config(k=sp.k, table_capacity=sp.T, kv_pages=sp.C, max_batch=sp.B // world,
                      max_prompt_tokens=sp.max_prompt_tokens, max_pool=sp.M,
-                     max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                     max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                      n_q_heads=sp.Hq, n_kv_heads=sp.Hkv, head_dim=sp.d, flags=sp.flags, max_global_batch=sp.B,
                      max_block_records=2 * (sp.B // world) * (sp.max_prompt_tokens // 16))
         stream = torch.cuda.Stream()

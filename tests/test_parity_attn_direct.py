@@ -35,7 +35,7 @@ def run_case(Hq, Hkv, d, reqs, shared_blocks=0, seed=0, big_rows=True, C=2048):
     sp = StreamSpec(n_logs=300, M=40, B=4)
     _, pool, instr = make_stream(sp)
     cfg = Config(k=3, table_capacity=16, kv_pages=C, max_batch=max(B, 4), max_prompt_tokens=mpt, max_pool=sp.M,
-                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                  max_suffix_tokens=tot_S, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d)
     pl = Pipeline(cfg, "cuda")
     pl.load_pool(pool, instr)

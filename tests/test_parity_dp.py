@@ -22,7 +22,7 @@ def _rank_pipeline(sp, pool, instr, G, rec_R=None):
     from paper_2507_08523_b200 import Config, Pipeline
     cfg = Config(k=sp.k, table_capacity=sp.T, kv_pages=sp.C, max_batch=sp.B // G,
                  max_prompt_tokens=sp.max_prompt_tokens, max_pool=sp.M,
-                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                  n_q_heads=sp.Hq, n_kv_heads=sp.Hkv, head_dim=sp.d, metric=sp.metric, flags=sp.flags,
                  hash_seed=sp.hash_seed, max_global_batch=sp.B,
                  # room for every block record of a batch (no FIFO backlog: the map is exact)

@@ -55,7 +55,7 @@ def test_c3_fullsize_stream_graphs():
     flags = IL_F_PAIR | IL_F_VERIFY | IL_F_GUARD
     ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
                   max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
-                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=256,
+                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                   head_dim=cfg.d, flags=flags)
     pl = Pipeline(ccfg, "cuda", qkv_seed=cfg.qkv_seed)
