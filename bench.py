@@ -30,6 +30,13 @@ METRIC = "ICL requests/s (refine+cached prefill), prefix-hit %, % HBM/TC rooflin
 UNIT = "requests/s"
 
 
+# INT32 lane-op peak for the integer stages' ALU fractions (1 membership test /
+# compare = 1 lane-op): the ALU pipe retires one warp instruction per 2 clocks per SMSP
+# (B200_PROFILING.md, "fma vs alu split": rt_SMSP = 2) = 64 lanes / clk / SM, x 148 SMs x the max
+# SM clock; scripts/alu_microbench.cu measures it (profiles/r02_alu_microbench.txt)
+INT32_LANES_PER_CLK_SM = 64
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -242,8 +249,8 @@ def run_ours(args, rank, world, local_rank):
     # records + il_refine_batch, .., il_commit_index + il_commit_export; the all-gather itself
     # (NCCL, side stream) and the wait for it stay outside the stages.
     if dp is None:
-        stage_fns = {"refine": pl.refine, "match": pl.match, "synth": pl.synth, "attn": pl.attn,
-                     "commit": pl.commit}
+        stage_fns = {"select": pl.select, "refine": pl.refine, "match": pl.match, "synth": pl.synth,
+                     "attn": pl.attn, "commit": pl.commit}
     else:
         stage_fns = {"select": dp.select, "refine": lambda: (dp.apply_records(), pl.refine()),
                      "match": pl.match, "synth": pl.synth, "attn": pl.attn, "commit": dp.export}
@@ -407,6 +414,9 @@ def run_ours(args, rank, world, local_rank):
     # the integer stages with no HBM-sized work are latency bound and reported as times only
     mt = np.array(stage_ms["match"]) * 1e-3
     mw = np.array(mwork)
+    clk_hz = (clk.get("sm_max_mhz") or 1965.0) * 1e6
+    int32_peak = INT32_LANES_PER_CLK_SM * 148 * clk_hz            # lane-ops / s
+    pool_u = int(sum(len(np.unique(pool.log_tok[pool.log_off[m]:pool.log_off[m + 1]])) for m in range(pool.n)))
     stage_roof = {
         "match": {"bound": "hbm (algorithmic); latency in practice", "bytes_per_step": float(mw.mean()),
                   "achieved": float(mw.sum() / mt.sum() / 1e9), "peak": pk["hbm"], "unit": "GB/s",
@@ -416,7 +426,20 @@ def run_ours(args, rank, world, local_rank):
                   "note": "bytes = SURVEY 8(d).2 formula (every prompt token read); bytes_touched = what this "
                           "implementation moves (instruction blocks hashed and probed once per batch)"},
         "attn": {"bound": bound, "frac": achieved / peak},
-        "refine": {"bound": "latency (ALU / L2-resident pool and table)", "ms": float(np.mean(stage_ms["refine"]))},
+        **({"select": {"bound": "ALU (INT32 lane-ops)", "ms": float(np.mean(stage_ms["select"])),
+                       "membership_tests_per_step": float(cfg.B * pool_u), "int32_peak_lane_ops_per_s": int32_peak,
+                       "frac": float(cfg.B * pool_u / (np.mean(stage_ms["select"]) * 1e-3) / int32_peak),
+                       "note": "a1+a2: B x sum_m u_m membership tests (SURVEY 8(d).2) / (64 lanes/clk/SM x 148 x clock)"}}
+           if "select" in stage_ms else {}),
+        "refine": {"bound": "ALU (PMC) / HBM write (render)", "ms": float(np.mean(stage_ms["refine"])),
+                   "pmc_compares_per_step": float(cfg.B * np.mean([s_["table_entries"] for s_ in st_steps]) * cfg.k ** 2),
+                   "pmc_frac_of_int32": float(cfg.B * np.mean([s_["table_entries"] for s_ in st_steps]) * cfg.k ** 2
+                                              / (np.mean(stage_ms["refine"]) * 1e-3) / int32_peak),
+                   "render_bytes_per_step": float(np.mean([4 * L_all[j, :dev_in[2 * j][3]].astype(np.int64).sum() for j in range(K)])),
+                   "render_frac_of_hbm": float(np.mean([4 * L_all[j, :dev_in[2 * j][3]].astype(np.int64).sum() for j in range(K)])
+                                               / (np.mean(stage_ms["refine"]) * 1e-3) / (pk["hbm"] * 1e9)),
+                   "note": "a3 (PMC vs the ICL Table) + a4 (rules, guard) + a5 (render): compares / INT32 lane-op peak, "
+                           "prompt bytes written / HBM peak, both over the whole stage time"},
         "commit": {"bound": "latency", "ms": float(np.mean(stage_ms["commit"]))},
         "synth": {"bound": "ALU (stand-in generator, not the method)", "ms": float(np.mean(stage_ms["synth"]))},
     }

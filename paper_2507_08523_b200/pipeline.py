@@ -75,6 +75,11 @@ class Pipeline:
         self.B = B
 
     # -------------------------------------------------------------- the path
+    def select(self, B=None) -> None:
+        """a1-a2 alone (il_select_batch); a following refine() of the same batch skips it."""
+        B = self.B if B is None else B
+        self.ctx.select_batch(B, self.q_off, self.q_tok, self.q_src, self.topk, stream=self.stream)
+
     def refine(self, B=None) -> None:
         B = self.B if B is None else B
         self.ctx.refine_batch(B, self.q_off, self.q_tok, self.q_src, self.topk, self.final_ds, self.info,

@@ -48,6 +48,9 @@ __global__ void k_bench(unsigned long long* out, float seed) {
       if (OP == 9) u[j] = hfma2(u[j], 0x3C003C00u, 0x3C003C00u);
       if (OP == 10) u[j] = shl_add(u[j], 7u);
       if (OP == 11) { f[j] = ex2f(f[j]); w[j] = ffma2(w[j], one2, one2); }   // MUFU + FFMA2 co-issue
+      if (OP == 12) { uint32_t d; asm volatile("add.u32 %0, %1, %2;" : "=r"(d) : "r"(u[j]), "r"(u[(j + 1) & 7])); u[j] = d; }
+      if (OP == 13) { uint32_t d; asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(u[j]), "r"(u[(j + 3) & 7]), "r"(0x5A5A5A5Au)); u[j] = d; }
+      if (OP == 14) { uint32_t d; asm volatile("{ .reg .pred p1; setp.eq.u32 p1, %1, %2; selp.u32 %0, 1, %1, p1; }" : "=r"(d) : "r"(u[j]), "r"(u[(j + 1) & 7])); u[j] = d; }
     }
   }
   const unsigned long long t1 = clock64();
@@ -89,6 +92,9 @@ int main() {
   run<9>(d, "fma.rn.f16x2 (HFMA2)", 2);
   run<10>(d, "shl+add (2 int ops)", 1);
   run<11>(d, "MUFU.EX2 + FFMA2 pairs (per pair)", 1);
+  run<12>(d, "add.u32 (IADD3, INT32 lane-op)", 1);
+  run<13>(d, "lop3.b32 (LOP3, INT32 lane-op)", 1);
+  run<14>(d, "setp.eq + selp (compare, 2 ops)", 1);
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
