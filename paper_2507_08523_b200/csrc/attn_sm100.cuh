@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t bar0 = sbase + OFF_BAR;
   auto bar = [&](uint32_t idx) { return bar0 + 8 * idx; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
+
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
   const uint32_t NC = c.sc->shared_blk / 8;
@@ -575,10 +576,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) {
         if (lc >= nst) mbar_wait(bar(free0 + s), (u - 1) & 1);
         IL_TRACE(is_k ? 0 : 1, lc & 4095);
+#ifdef IL_NO_KV_TMA
+        mbar_arrive(bar(full0 + s));                   // profiling variant: no K / V loads
+#else
         mbar_expect_tx(bar(full0 + s), KVTILE);
+#endif
       }
       __syncwarp();
+#ifdef IL_NO_KV_TMA
+      if (false) {
+#else
       if (lane < 8 * NCB) {                            // lane = (page, 64-column block)
+#endif
         const uint32_t p = lane & 7, h = lane >> 3;
         const int row = (int)(((uint32_t)page * Hkv + L.kh) * BS);
         tma_load_2d(ring + s * KVTILE + h * KCB + p * 2048, tm, (int)(64 * h), row, bar(full0 + s));
@@ -719,6 +728,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(bar(S_FULL + xo), cnt & 1);
         if (r == 0) IL_TRACE(4 + 2 * xo, cnt & 4095);
         tc_fence_after();
+#ifdef IL_NO_SOFTMAX
+        {   // profiling variant: P = 0 without touching S (the MMA / TMA pipeline alone)
+          uint32_t z[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) z[j] = 0u;
+          tmem_st32u(s_tmem, z);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar(P_HALF + xo));
+          tmem_st32u(s_tmem + 32, z);
+          tmem_wait_st();
+          tc_fence_before();
+          if (r == 0) IL_TRACE(5 + 2 * xo, cnt & 4095);
+          mbar_arrive(bar(P_FULL + xo));
+          ++cnt;
+          continue;
+        }
+#endif
         const uint32_t key0 = (T.kv0 + n) * BN;
         float a[128];
 #pragma unroll
