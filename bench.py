@@ -64,7 +64,26 @@ MAX_FILL = {1: 400, 2: 200, 3: 200, 4: 200, 5: 200}
 
 def n_queries_for(cfg, args, world: int) -> int:
     """Stream length both arms use (the same dataset instance): ramp + fill + warm-up + timed."""
-    return (MAX_FILL[args.config] + args.warmup + 2 * args.steps + 1) * cfg.B * world + 65 * world
+    n = (MAX_FILL[args.config] + args.warmup + 2 * args.steps + 1) * cfg.B * world + 65 * world
+    return int(n * 1.25) if getattr(args, "dedup", False) else n      # (the dedup'd stream is shorter)
+
+
+class Stream:
+    """The query stream: dataset rows in order, or with --dedup the LILAC / LogBatcher
+    shape: only the first occurrence of each distinct log is queried."""
+
+    def __init__(self, ds, dedup: bool):
+        self.ds = ds
+        self.rows = gen.dedup_rows(ds) if dedup else None
+
+    def batch(self, start: int, B: int):
+        if self.rows is None:
+            return gen.make_batch(self.ds, start, B)
+        return gen.make_batch_rows(self.ds, self.rows[np.arange(start, start + B) % len(self.rows)])
+
+    @property
+    def n(self) -> int:
+        return self.ds.n if self.rows is None else len(self.rows)
 
 
 def workload(cfg_n: int, rank: int, world: int, n_queries: int = 0):
@@ -161,6 +180,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     cfg0 = gen.config(args.config)
     cfg, ds, pool, instr = workload(args.config, rank, world, n_queries=n_queries_for(cfg0, args, world))
+    stream_q = Stream(ds, args.dedup)
     flags = IL_F_PAIR | IL_F_VERIFY | (IL_F_GUARD if not args.no_guard else 0)
     if args.naive:
         flags = IL_F_VERIFY
@@ -168,7 +188,7 @@ def run_ours(args, rank, world, local_rank):
                   max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
                   max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
-                  head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world)
+                  head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world, max_decode_tokens=args.decode)
     stream = torch.cuda.Stream(dev)
     pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
     # N > 1: rank r runs the r-th slice of every global batch; the pool is
@@ -181,27 +201,44 @@ def run_ours(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         (dp or pl).load_pool(pool, instr)
     step = dp.step if dp else pl.step
+    if args.decode and dp is not None:
+        raise SystemExit("--decode is measured at N = 1 only")
+    if args.decode and dp is None:
+        def step():                                    # eager step with the decode tokens
+            pl.refine(); pl.match(); pl.synth(); pl.attn()
+            for t in range(args.decode):
+                pl.decode_step(t, dec_tok[t], lse=False)
+            pl.commit()
     K, W = args.steps, args.warmup
     n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
     plan = plan_batches(cfg, n_fill_max + W + 2 * K, rank, world)
     n_ramp = len(plan) - (n_fill_max + W + 2 * K)
 
+    dec_tok = torch.zeros(args.decode, cfg.B, dtype=torch.int64, device=dev) if args.decode else None
+
+    def dec_of(bt):                                    # the batch's decode tokens [D][B] (NEXT-4 stand-ins)
+        return torch.from_numpy(np.stack([gen.decode_tokens(bt.q_src, t) for t in range(max(args.decode, 1))])
+                                .astype(np.int64))
+
     def to_dev(bt):
         return (torch.from_numpy(bt.q_off.view(np.int32)).to(dev), torch.from_numpy(bt.q_tok.view(np.int32)).to(dev),
-                torch.from_numpy(bt.q_src.view(np.int32)).to(dev), bt.B)
+                torch.from_numpy(bt.q_src.view(np.int32)).to(dev), bt.B, dec_of(bt).to(dev))
 
     def to_pinned(bt):
-        return tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src)) + (bt.B,)
+        return (tuple(torch.from_numpy(a.view(np.int32)).pin_memory() for a in (bt.q_off, bt.q_tok, bt.q_src))
+                + (bt.B, dec_of(bt).pin_memory()))
 
     def set_inputs(x):
-        pl.load_inputs(*x)                             # device-to-device into the resident input buffers
+        pl.load_inputs(*x[:4])                         # device-to-device into the resident input buffers
+        if dec_tok is not None:
+            dec_tok[:, :x[3]].copy_(x[4])
 
     # ---- cold-start ramp, then fill until a batch evicts (untimed; all ranks stop together)
     stats_dev = torch.zeros(128, dtype=torch.uint8, device=dev)
     j = 0
     with torch.cuda.stream(stream):
         for j in range(n_ramp + n_fill_max):
-            set_inputs(to_dev(gen.make_batch(ds, *plan[j])))
+            set_inputs(to_dev(stream_q.batch(*plan[j])))
             step()
             if j < n_ramp:
                 continue
@@ -215,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
     n_fill = j + 1 - n_ramp if n_fill_max else 0
     plan = plan[:n_ramp + n_fill] + plan[n_ramp + n_fill_max:]
     stream.synchronize()
-    batches = [gen.make_batch(ds, s, b) for s, b in plan[n_ramp + n_fill:]]
+    batches = [stream_q.batch(s, b) for s, b in plan[n_ramp + n_fill:]]
 
     # Timed steps alternate: even = device-timed (inputs already resident in HBM), odd = end to
     # end (pinned host inputs copied in, refined DS / info / hits copied out inside the timed
@@ -248,9 +285,17 @@ def run_ours(args, rank, world, local_rank):
     # overlapping the previous batch's record all-gather), then il_commit_apply of the gathered
     # records + il_refine_batch, .., il_commit_index + il_commit_export; the all-gather itself
     # (NCCL, side stream) and the wait for it stay outside the stages.
+    if args.decode:
+        def decode_all():
+            for t in range(args.decode):
+                pl.decode_step(t, dec_tok[t], lse=False)
     if dp is None:
         stage_fns = {"select": pl.select, "refine": pl.refine, "match": pl.match, "synth": pl.synth,
                      "attn": pl.attn, "commit": pl.commit}
+        if args.decode:
+            stage_fns = {k: v for k, v in list(stage_fns.items())[:5]}
+            stage_fns["decode"] = decode_all
+            stage_fns["commit"] = pl.commit
     else:
         stage_fns = {"select": dp.select, "refine": lambda: (dp.apply_records(), pl.refine()),
                      "match": pl.match, "synth": pl.synth, "attn": pl.attn, "commit": dp.export}
@@ -316,12 +361,14 @@ def run_ours(args, rank, world, local_rank):
                 rec_bt[j // 2, :B].copy_(pl.block_table[:B])
                 rec_info[j // 2, :B].copy_(pl.info[:B])
             else:
-                qo, qt, qs, B = host_in[j]
+                qo, qt, qs, B, dt = host_in[j]
                 e0, e1 = ev(), ev()
                 e0.record(stream)
                 pl.q_off[:B + 1].copy_(qo, non_blocking=True)        # pinned host -> resident buffers
                 pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
                 pl.q_src[:B].copy_(qs, non_blocking=True)
+                if dec_tok is not None:
+                    dec_tok[:, :B].copy_(dt, non_blocking=True)
                 pl.B = B
                 run_step()
                 out_fin[:B].copy_(pl.final_ds[:B], non_blocking=True)
@@ -330,7 +377,7 @@ def run_ours(args, rank, world, local_rank):
                 e1.record(stream)
                 pl.ctx.stats_async(rec_stats[j], stream=stream)
                 e2e_evs.append((e0, e1))
-                h2d = 4 * (qo.numel() + qt.numel() + qs.numel())
+                h2d = 4 * (qo.numel() + qt.numel() + qs.numel()) + (8 * dt.numel() if dec_tok is not None else 0)
                 d2h = 4 * B * cfg.k + 4 * B + 16 * B
     if dp is not None:
         with torch.cuda.stream(stream):
@@ -444,6 +491,23 @@ def run_ours(args, rank, world, local_rank):
         "synth": {"bound": "ALU (stand-in generator, not the method)", "ms": float(np.mean(stage_ms["synth"]))},
     }
     t_star_step = float(np.maximum(t_tc, t_hbm).mean() * 1e3 + mw.mean() / (pk["hbm"] * 1e9) * 1e3)
+    def decode_roof():
+        """Decode is HBM-bound: per decode step the K / V of every request's own blocks (past the
+        batch-shared instruction blocks, read once) are read: algorithmic bytes = (shared blocks +
+        sum_i own blocks) x 16 x Hkv x d x 2 B x 2 (K and V), averaged over the D steps."""
+        nI = cfg.n_instr // 16
+        tot = 0.0
+        for j in range(K):
+            Bj = dev_in[2 * j][3]
+            Lj = L_all[j, :Bj].astype(np.int64)
+            for t in range(args.decode):
+                blocks = nI + np.maximum((Lj + t + 1 + 15) // 16 - nI, 0).sum()
+                tot += blocks * 16 * cfg.Hkv * cfg.d * 2 * 2
+        per_step = tot / (K * args.decode)
+        t_step = np.mean(stage_ms["decode"]) * 1e-3 / args.decode
+        return {"bound": "hbm", "bytes_per_decode_step": per_step, "achieved_gbs": per_step / t_step / 1e9,
+                "frac_of_hbm": per_step / t_step / (pk["hbm"] * 1e9)}
+
     line = {
         "metric": METRIC, "value": B_all / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -456,6 +520,15 @@ def run_ours(args, rank, world, local_rank):
                          "resident_blocks": int(st_steps[-1]["resident_blocks"]),
                          "note": "untimed full batches after the ramp until the KV cache is full and a batch "
                                  "evicts; every timed step then runs LRU eviction (rank 0's counts)"},
+        "decode": None if not args.decode else {
+            "tokens_per_request": args.decode, "ms_per_step": float(np.mean(stage_ms["decode"])),
+            "tokens_per_s": B_all * args.decode / (np.mean(stage_ms["decode"]) * 1e-3),
+            **decode_roof(),
+            "note": "SURVEY 8(f) NEXT-4: after the cached prefill, D decode steps per request, one row per request "
+                    "through il_prefill_attn at positions L_i + t into the pages il_prefix_match reserved (Q/K/V from "
+                    "the synthetic projection); part of ms_per_step, as the stage 'decode'"},
+        "stream_shape": "dedup (first occurrence of each distinct log; LILAC / LogBatcher, P:637-675): "
+                        f"{stream_q.n} of {ds.n} logs" if args.dedup else "every log once (S:148)",
         "prefix_hit_pct": 100.0 * hits / max(fulls, 1),
         "box_level": None if dp is None else {
             "hit_pct_rank_local": 100.0 * float(hb[0]) / max(float(hb[2]), 1.0),
@@ -747,6 +820,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
     ap.add_argument("--no-fill", action="store_true", help="time right after the ramp (cache not yet full)")
+    ap.add_argument("--decode", type=int, default=0, help="decode tokens per request after the prefill (NEXT-4)")
+    ap.add_argument("--dedup", action="store_true", help="query only the first occurrence of each distinct log")
     ap.add_argument("--cpu-attn-sample", type=int, default=32, help="--impl reference: fp64 attention requests per step")
     ap.add_argument("--cpu-baseline-attn", type=int, default=400, help="cpu_baseline: fp64 attention requests sampled")
     ap.add_argument("--cpu-baseline-batches", type=int, default=4, help="cpu_baseline: full batches of the integer path")

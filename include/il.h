@@ -86,6 +86,10 @@ typedef struct {
                                   world x B); 0 = max_batch.  > max_batch enables the multi-GPU
                                   block records and the residency map (ranks = ceil(./max_batch) <= 32) */
   uint32_t max_block_records;  /* multi-GPU: block records one il_commit_export carries; 0 = 16 x max_batch */
+  uint32_t max_decode_tokens;  /* D: KV pages reserved per request for D decode tokens after the prompt
+                                  (il_prefix_match allocates ceil((L + D) / 16) - hit pages, il_commit
+                                  frees them); prompts must fit max_prompt_tokens - D.  0 = prefill only */
+  uint32_t reserved1;          /* must be 0 */
 } il_config;
 
 /* Per-request refinement outcome (SPEC S:190-193 RefinementResult). */
@@ -177,7 +181,10 @@ il_status il_prefix_match(il_ctx* ctx, uint32_t B,
                           int32_t* block_table, int32_t* prefix_len, int32_t* cu_q, il_stream s);
 
 /* ---- il_prefill_attn: rows r in [cu_q[i], cu_q[i+1]) are the suffix tokens of request i at
- * absolute positions p = prefix_len[i] + (r - cu_q[i]).  First writes k_new/v_new rows into
+ * absolute positions p = prefix_len[i] + (r - cu_q[i]).  prefix_len is 16 x hit after
+ * il_prefix_match; any position works (paged DECODE: one row per request at
+ * position L_i + t, its K/V written into the decode pages il_prefix_match reserved, attending over
+ * the prompt and the t decode tokens before it; see max_decode_tokens).  First writes k_new/v_new rows into
  * the request's pages, then for every q-head h:
  *   out[r][h] = sum_{j <= p} softmax_j(q[r][h] . K_j * scale) V_j,  kv-head = h / (Hq/Hkv)
  * with K_j, V_j read from the pages (cached prefix and the just-written suffix alike).

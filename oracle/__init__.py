@@ -50,6 +50,7 @@ def lib():
                                        u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p])
         _lib.or_run_batch_dp.argtypes = ([C.POINTER(P), C.c_uint32, C.c_uint32, u32p, u32p, u32p, u32p, u32p, i32p,
                                           u64p, u32p, u32p, C.c_uint32, u64p, C.c_uint32, u32p, u64p, u32p, u32p])
+        _lib.or_set_decode.argtypes = [P, C.c_uint32]
         _lib.or_batch_index.restype = C.c_uint64
         _lib.or_batch_index.argtypes = [P]
         _lib.or_index_size.restype = C.c_uint32
@@ -115,6 +116,9 @@ class Oracle:
         if getattr(self, "h", None) and _lib is not None:
             _lib.or_destroy(self.h)
             self.h = None
+
+    def set_decode(self, d: int) -> None:
+        lib().or_set_decode(self.h, d)
 
     def pool_load(self, pool, instr) -> None:
         arrs = [_u32(pool.log_off), _u32(pool.log_tok), _u32(pool.tpl_off), _u32(pool.tpl_tok),

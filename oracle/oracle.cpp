@@ -37,6 +37,7 @@ struct Block {            // a resident KV block
 
 struct or_state {
   u32 k, T, C, metric, flags;
+  u32 decode = 0;                          // D: pages reserved for D decode tokens per request
   u64 seed;
   bool loaded = false;
   std::vector<Demo> pool;
@@ -328,7 +329,7 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     ref[i] = refine(s, cur[i], q[i]);
     if (ref[i].rule < 0) { err[i] = 4; continue; }
     prompt[i] = render(s, ref[i].final_ds, q[i]);
-    if (prompt[i].size() > prompt_stride || prompt[i].size() / BS > max_blocks) { err[i] = 1; continue; }
+    if (prompt[i].size() + s->decode > prompt_stride || prompt[i].size() / BS > max_blocks) { err[i] = 1; continue; }
     H[i] = chain_hashes(s->seed, prompt[i]);
     const u32 hl = leading_hits(s, prompt[i], H[i]);
     h[i] = cap_hits(hl, prompt[i].size());
@@ -353,7 +354,7 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     for (u32 i = 0; i < B; ++i) {
       if (owner[i] != r) continue;
       for (u32 j = 0; j < h[i]; ++j) pinned.insert(H[i][j]);
-      need += (prompt[i].size() + BS - 1) / BS - h[i];
+      need += (prompt[i].size() + s->decode + BS - 1) / BS - h[i];   // (+ the decode reserve)
     }
     u64 free_pages = s->C - s->index.size();
     if (need > free_pages) {
@@ -477,6 +478,7 @@ int or_run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32* q_
 }
 
 u64 or_batch_index(const or_state* s) { return s->batch; }
+void or_set_decode(or_state* s, u32 d) { s->decode = d; }
 u32 or_index_size(const or_state* s) { return (u32)s->index.size(); }
 void or_index_dump(const or_state* s, u64* hash, u64* stamp, u32* depth, u64* parent) {
   size_t n = 0;

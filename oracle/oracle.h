@@ -59,6 +59,9 @@ int or_run_batch_dp(or_state** st, uint32_t G, uint32_t B, const uint32_t* q_off
                     uint32_t* hit, uint64_t* evicted, uint32_t* n_evicted, uint32_t* n_evicted_rank);
 
 uint64_t or_batch_index(const or_state*);           /* b of the last committed batch */
+/* reserve KV pages for d decode tokens per request: step 7 allocates
+ * ceil((L + d) / 16) - h pages per request; prompts must fit prompt_stride - d.  Default 0. */
+void or_set_decode(or_state*, uint32_t d);
 /* SURVEY §8(e) residency map (replicated on every rank of a run_batch_dp): chain hash -> bitmask
  * of the ranks whose index holds it, i.e. the union of the ranks' indices after the batch; and
  * the box-level hit counts of the last batch ([B]): each request's own leading run continued

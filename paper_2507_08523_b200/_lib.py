@@ -40,7 +40,8 @@ class il_config(C.Structure):
                 ("max_pool_tokens", C.c_uint32), ("max_log_tokens", C.c_uint32),
                 ("max_suffix_tokens", C.c_uint32), ("n_q_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
                 ("head_dim", C.c_uint32), ("metric", C.c_uint32), ("flags", C.c_uint32),
-                ("hash_seed", C.c_uint64), ("max_global_batch", C.c_uint32), ("max_block_records", C.c_uint32)]
+                ("hash_seed", C.c_uint64), ("max_global_batch", C.c_uint32), ("max_block_records", C.c_uint32),
+                ("max_decode_tokens", C.c_uint32), ("reserved1", C.c_uint32)]
 
 
 class il_refine_info(C.Structure):

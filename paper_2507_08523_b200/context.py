@@ -33,6 +33,7 @@ class Config:
     hash_seed: int = 0
     max_global_batch: int = 0           # multi-GPU: world * max_batch records per table commit
     max_block_records: int = 0          # multi-GPU: block records per export (0 = 16 * max_batch)
+    max_decode_tokens: int = 0          # KV pages reserved per request for decode tokens (NEXT-4)
 
     @property
     def max_blocks(self) -> int:
@@ -44,7 +45,7 @@ class Config:
                            self.max_prompt_tokens, self.max_pool, self.max_pool_tokens,
                            self.max_log_tokens, m, self.n_q_heads, self.n_kv_heads, self.head_dim,
                            self.metric, self.flags, self.hash_seed, self.max_global_batch,
-                           self.max_block_records)
+                           self.max_block_records, self.max_decode_tokens, 0)
 
     def record_bytes(self) -> int:
         cc = self.c()

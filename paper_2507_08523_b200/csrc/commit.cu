@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(256) k_commit_own(Ctx c, uint32_t B) {
     if (c.ins_list) c.ins_list[atomicAdd(&c.sc->inserted, 1u)] = bh[j];   // multi-GPU block record
     ++owned;
   }
-  if (lane == 0 && (L % BS)) push_free(c, (uint32_t)bt[F]);       // partial block (Z23)
+  // the partial block (Z23) and the decode reserve's pages go back to the free stack
+  for (uint32_t j = F + lane; j < cdiv(L + c.cfg.max_decode_tokens, BS); j += 32) push_free(c, (uint32_t)bt[j]);
   for (int o = 16; o; o >>= 1) owned += __shfl_xor_sync(~0u, owned, o);
   if (lane == 0 && owned) atomicAdd(&c.sc->resident, owned);
 }

@@ -125,6 +125,8 @@ static il_status validate(const il_config* g) {
     set_error("at most 32 ranks (max_global_batch / max_batch)"); return IL_ERR_ARG;
   }
   if (g->max_block_records > (1u << 24)) { set_error("max_block_records <= 2^24"); return IL_ERR_ARG; }
+  if (g->reserved1 != 0) { set_error("il_config.reserved1 must be 0"); return IL_ERR_ARG; }
+  if (g->max_decode_tokens >= g->max_prompt_tokens) { set_error("max_decode_tokens >= max_prompt_tokens"); return IL_ERR_ARG; }
   if (g->max_prompt_tokens < 16 || (g->max_prompt_tokens % 16)) { set_error("max_prompt_tokens: multiple of 16"); return IL_ERR_ARG; }
   if (g->max_pool < g->k) { set_error("max_pool < k"); return IL_ERR_ARG; }
   if (g->max_log_tokens < 1 || g->max_log_tokens > 256) { set_error("max_log_tokens in 1..256"); return IL_ERR_ARG; }

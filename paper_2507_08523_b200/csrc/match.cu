@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
   uint32_t n = 0, sfx = 0;
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     const uint32_t L = prompt_len[i], h = hit[i];
-    n += cdiv(L, BS) - h;
+    n += cdiv(L + c.cfg.max_decode_tokens, BS) - h;    // prompt pages (+ the decode reserve)
     sfx += L - BS * h;
   }
   uint32_t need, suf;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     const uint32_t L = prompt_len[i], h = hit[i];
     c.need_off[i] = an; cu_q[i] = sfx_over ? 0 : (int32_t)as; prefix_len[i] = (int32_t)(BS * h);
-    an += cdiv(L, BS) - h;
+    an += cdiv(L + c.cfg.max_decode_tokens, BS) - h;
     as += L - BS * h;
   }
   if (tid == 1023) {
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uin
   DevScalars* sc = c.sc;
   if (sc->status == IL_ERR_CAPACITY) return;
   const uint32_t base = sc->n_free - sc->need_total + c.need_off[i];
-  const uint32_t h = hit[i], nb = cdiv(prompt_len[i], BS);
+  const uint32_t h = hit[i], nb = cdiv(prompt_len[i] + c.cfg.max_decode_tokens, BS);
   int32_t* bt = block_table + (size_t)i * c.max_blocks;
   for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
 }

@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(REF_THREADS) k_refine(Ctx c, uint32_t B, const
   }
   __syncthreads();
   L = s_L;
-  if (L > stride) {
+  if (L + c.cfg.max_decode_tokens > stride) {          // (the decode reserve shares the row's blocks)
     if (tid == 0) latch(c.sc, IL_ERR_ARG);
     L = 0;
   } else if (!s_rendered) {

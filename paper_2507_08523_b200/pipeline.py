@@ -135,6 +135,36 @@ class Pipeline:
         self.q_src[:B].copy_(q_src[:B], non_blocking=True)
         self.B = B
 
+    # -------------------------------------------------------------- decode
+    def decode_step(self, t: int, tokens: torch.Tensor, B=None, lse: bool = True) -> None:
+        """Decode token t of every request (after il_prefill_attn, before il_commit; needs
+        Config.max_decode_tokens > t): tokens[i] is written at position L_i + t of the prompt
+        row, its Q / K / V come from il_synth_qkv (the QKV-projection stand-in) and il_prefill_attn
+        runs ONE row per request at position L_i + t: its K / V go into the reserved decode page,
+        attention covers the prompt and the t decode tokens before it.  Output: dec_out[:B]."""
+        B = self.B if B is None else B
+        dev = self.device
+        if not hasattr(self, "dec_q"):
+            cfg, rows = self.cfg, self.cfg.max_batch + 256       # (whole 128-row Q tiles stay in bounds)
+            bf = torch.bfloat16
+            self.dec_q = torch.zeros(rows, cfg.n_q_heads, cfg.head_dim, dtype=bf, device=dev)
+            self.dec_k = torch.zeros(rows, cfg.n_kv_heads, cfg.head_dim, dtype=bf, device=dev)
+            self.dec_v = torch.zeros(rows, cfg.n_kv_heads, cfg.head_dim, dtype=bf, device=dev)
+            self.dec_out = torch.zeros(rows, cfg.n_q_heads, cfg.head_dim, dtype=bf, device=dev)
+            self.dec_lse = torch.zeros(rows, cfg.n_q_heads, dtype=torch.float32, device=dev)
+            self.dec_cu = torch.arange(cfg.max_batch + 1, dtype=torch.int32, device=dev)
+            self.dec_pos = torch.zeros(cfg.max_batch, dtype=torch.int32, device=dev)
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(s):
+            pos = self.prompt_len[:B] + t
+            self.dec_pos[:B].copy_(pos)
+            self.prompt_tok.view(-1)[torch.arange(B, device=dev) * self.prompt_tok.shape[1] + pos] = tokens[:B].to(torch.int32)
+        self.ctx.synth_qkv(B, self.prompt_tok, self.dec_cu, self.dec_pos, self.qkv_seed, self.q_scale,
+                           self.dec_q, self.dec_k, self.dec_v, stream=self.stream)
+        self.ctx.prefill_attn(B, self.dec_cu, self.dec_pos, self.block_table, self.dec_q, self.dec_k, self.dec_v,
+                              self.k_pages, self.v_pages, self.dec_out, self.dec_lse if lse else None, self.scale,
+                              stream=self.stream)
+
     def launches(self) -> int:
         """Kernels this context has launched so far (host-side counter in the library)."""
         return int(self.ctx.stats(self.stream)["launches"])

@@ -561,8 +561,8 @@ class _Z21Model:
     """Literal reading Z21 + Z1 + Z22 over a plain dict:
     hash -> [stamp, depth, parent, tokens].  Stamps are (batch << 32 | admission index)."""
 
-    def __init__(self, C, root):
-        self.C, self.root, self.res, self.b = C, root, {}, 0
+    def __init__(self, C, root, decode=0):
+        self.C, self.root, self.res, self.b, self.decode = C, root, {}, 0, decode
 
     def hits(self, prompt, H):
         prev, h = self.root, 0
@@ -580,7 +580,7 @@ class _Z21Model:
         for i in range(len(prompts)):                                   # touch in admission order
             for j in range(h[i]):
                 self.res[Hs[i][j]][0] = (self.b << 32) | i
-        need = sum((len(p) + 15) // 16 - h[i] for i, p in enumerate(prompts))
+        need = sum((len(p) + self.decode + 15) // 16 - h[i] for i, p in enumerate(prompts))   # (+ decode reserve)
         free = self.C - len(self.res)
         victims = []
         if need > free:                                                 # LRU: (stamp, -depth, hash)
@@ -599,19 +599,20 @@ class _Z21Model:
         return h, victims
 
 
-@pytest.mark.parametrize("B", [1, 3])
-def test_small_cache_stream_matches_literal_z21_lru(B):
+@pytest.mark.parametrize("B,D", [(1, 0), (3, 0), (3, 7)])
+def test_small_cache_stream_matches_literal_z21_lru(B, D):
     """Z21 with a small cache (C = 48 pages, every batch evicts): the oracle's hits, exact victim
     lists (in eviction order) and resident blocks with their stamps, depths and parents equal a
     literal LRU model keyed by (stamp, -depth, hash)."""
     ds_, pool, instr = _hdfs_stream(n_instr=24)
     C = 48
     o = O.Oracle(k=3, table_capacity=16, kv_pages=C, flags=O.F_PAIR | O.F_VERIFY)
+    o.set_decode(D)                                                     # NEXT-4 decode reserve
     o.pool_load(pool, instr)
     probe = O.Oracle(k=1, table_capacity=4, kv_pages=4)              # ROOT = parent of a depth-0 block
     probe.pool_load(_pool_from_token_lists([[20]]), gen.instruction(4, 0))
     probe.insert(np.arange(16, dtype=np.uint32) + 100)
-    m = _Z21Model(C, int(probe.index_dump()[3][0]))
+    m = _Z21Model(C, int(probe.index_dump()[3][0]), decode=D)
     n_evicting = 0
     for b in range(120):
         res = o.run_batch(gen.make_batch(ds_, b * B, B))

@@ -200,6 +200,37 @@ def instruction(n_instr: int, seed: int) -> np.ndarray:
     return (INSTR_BASE + rng.integers(0, 1 << 16, size=n_instr)).astype(np.uint32)
 
 
+DECODE_BASE = 1 << 23    # synthetic decode-token ids
+
+
+def decode_tokens(q_src: np.ndarray, t: int) -> np.ndarray:
+    """Token t decoded for each request (a deterministic stand-in for the model's output, e.g. the
+    parsed template's tokens): a function of the query row and t only."""
+    return (DECODE_BASE + (np.asarray(q_src, np.uint64) * 2654435761 + np.uint64(t) * 40503) % 65536).astype(np.uint32)
+
+
+def dedup_rows(ds: Dataset) -> np.ndarray:
+    """The LILAC / LogBatcher stream shape: a parsing cache answers repeated logs, so
+    only the first occurrence of each distinct log reaches the LLM; the rows of those first
+    occurrences in dataset order."""
+    seen, rows = set(), []
+    for r in range(ds.n):
+        key = ds.log(r).tobytes()
+        if key not in seen:
+            seen.add(key)
+            rows.append(r)
+    return np.asarray(rows, np.int64)
+
+
+def make_batch_rows(ds: Dataset, rows: np.ndarray) -> Batch:
+    """A batch of the given dataset rows (in the given order)."""
+    rows = np.asarray(rows, np.int64)
+    lens = ds.log_off[rows + 1].astype(np.int64) - ds.log_off[rows].astype(np.int64)
+    q_off = np.zeros(len(rows) + 1, dtype=np.int64); np.cumsum(lens, out=q_off[1:])
+    q_tok = np.concatenate([ds.log(int(r)) for r in rows]) if len(rows) else np.zeros(0, np.uint32)
+    return Batch(q_off.astype(np.uint32), q_tok.astype(np.uint32), rows.astype(np.uint32))
+
+
 def make_batch(ds: Dataset, start: int, B: int) -> Batch:
     """Queries start..start+B-1 in dataset order, cycled."""
     rows = (np.arange(start, start + B, dtype=np.int64) % ds.n).astype(np.uint32)
