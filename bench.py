@@ -190,7 +190,7 @@ def run_ours(args, rank, world, local_rank):
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                   head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world, max_decode_tokens=args.decode)
     stream = torch.cuda.Stream(dev)
-    pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
+    pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream, fused_kv=not args.no_fused_kv)
     # N > 1: rank r runs the r-th slice of every global batch; the pool is
     # broadcast from rank 0; per batch one record buffer per rank (ICL records + prefix-index
     # updates) is all-gathered (NCCL) on a side stream, overlapping the next batch's selection
@@ -547,7 +547,9 @@ def run_ours(args, rank, world, local_rank):
             "value": B_all / ((sum(np.mean(v) for n, v in stage_ms.items() if n != "attn")
                                + 32 * np.mean(stage_ms["attn"])) * 1e-3),
             "unit": UNIT, "note": "B / (t_integer + t_synth + 32 x t_attention): one attention layer is what runs; 32 is the Llama-3-8B depth"},
-        "roofline": {"kernel": "il_prefill_attn (K/V append + attention)", "bound": bound, "achieved": achieved,
+        "roofline": {"kernel": "il_prefill_attn (attention; the suffix K/V written into the pages by the QKV-"
+                               "projection stand-in's epilogue)" if not args.no_fused_kv else
+                               "il_prefill_attn (K/V append + attention)", "bound": bound, "achieved": achieved,
                      "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": ncu_traffic()[0],
                      "traffic_src": ncu_traffic()[1],
                      "peak_src": pk["src"] + (" burst bf16" if bound == "tensor" else ""),
@@ -821,6 +823,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
     ap.add_argument("--no-fill", action="store_true", help="time right after the ramp (cache not yet full)")
     ap.add_argument("--decode", type=int, default=0, help="decode tokens per request after the prefill (NEXT-4)")
+    ap.add_argument("--no-fused-kv", action="store_true",
+                    help="K / V to k_new / v_new and il_prefill_attn's append pass (instead of the projection "
+                         "stand-in writing the pages)")
     ap.add_argument("--dedup", action="store_true", help="query only the first occurrence of each distinct log")
     ap.add_argument("--cpu-attn-sample", type=int, default=32, help="--impl reference: fp64 attention requests per step")
     ap.add_argument("--cpu-baseline-attn", type=int, default=400, help="cpu_baseline: fp64 attention requests sampled")

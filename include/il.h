@@ -189,7 +189,8 @@ il_status il_prefix_match(il_ctx* ctx, uint32_t B,
  *   out[r][h] = sum_{j <= p} softmax_j(q[r][h] . K_j * scale) V_j,  kv-head = h / (Hq/Hkv)
  * with K_j, V_j read from the pages (cached prefix and the just-written suffix alike).
  *   q, out        [max_suffix_tokens][Hq][d]  bf16;  lse [..][Hq] f32 natural log, or NULL
- *   k_new, v_new  [max_suffix_tokens][Hkv][d] bf16
+ *   k_new, v_new  [max_suffix_tokens][Hkv][d] bf16, or both NULL when the suffix K / V are already
+ *                 in the pages (il_synth_qkv_paged: the projection epilogue wrote them)
  *   k_pages, v_pages  [C][Hkv][16][d] bf16, caller-owned, persistent across batches
  * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27).
  * Runs on the tcgen05/TMA kernel (head_dim 64 or 128, Hq/Hkv in 1..8; il_create rejects any
@@ -268,10 +269,16 @@ il_status il_select_batch(il_ctx* ctx, uint32_t B, const uint32_t* q_off, const 
 
 /* ---- bench / test helper (not part of the method): deterministic bf16 Q, K, V for the
  * suffix rows from (seed, token, absolute position, head, dim) — the counter-based
- * generator of DESIGN.md Z28, so cached pages equal recomputation.  q_scale scales Q. */
+ * generator of DESIGN.md Z28, so cached pages equal recomputation.  q_scale scales Q.
+ * il_synth_qkv_paged writes K and V straight into the request's KV pages (block_table of the
+ * preceding il_prefix_match), as a model's QKV-projection epilogue writes the paged cache; the
+ * following il_prefill_attn then gets k_new = v_new = NULL and skips its append pass. */
 il_status il_synth_qkv(il_ctx* ctx, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
                        const int32_t* prefix_len, uint64_t seed, float q_scale,
                        il_bf16* q, il_bf16* k_new, il_bf16* v_new, il_stream s);
+il_status il_synth_qkv_paged(il_ctx* ctx, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
+                             const int32_t* prefix_len, const int32_t* block_table, uint64_t seed,
+                             float q_scale, il_bf16* q, il_bf16* k_pages, il_bf16* v_pages, il_stream s);
 
 /* ---- debug / parity helpers: copy the resident index (hash, stamp, depth, parent hash;
  * unordered) and the ICL Table (ds [T][k], stamp [T]; empty slots have stamp 0) to host. */

@@ -25,7 +25,7 @@ EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "i
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
            "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
            "il_table_dump", "il_evicted_dump", "il_record_bytes", "il_commit_export", "il_commit_apply",
-           "il_box_hit_dump", "il_select_batch"]
+           "il_box_hit_dump", "il_select_batch", "il_synth_qkv_paged"]
 
 
 class ILError(RuntimeError):
@@ -89,6 +89,7 @@ def load():
         "il_commit_index": [P, P],
         "il_commit_records": [P, U32, P, P, P],
         "il_synth_qkv": [P, U32, P, P, P, U64, F32, P, P, P, P],
+        "il_synth_qkv_paged": [P, U32, P, P, P, P, U64, F32, P, P, P, P],
         "il_index_dump": [P, P, P, P, P, P, P],
         "il_table_dump": [P, P, P, P],
         "il_evicted_dump": [P, P, P, P],

@@ -148,6 +148,12 @@ class Context:
                                       float(q_scale), _p(q), _p(k_new), _p(v_new), _stream(stream)),
                 "il_synth_qkv")
 
+    def synth_qkv_paged(self, B, prompt_tok, cu_q, prefix_len, block_table, seed, q_scale, q, k_pages, v_pages,
+                        stream=None):
+        L.check(self.lib.il_synth_qkv_paged(self.h, B, _p(prompt_tok), _p(cu_q), _p(prefix_len), _p(block_table),
+                                            int(seed), float(q_scale), _p(q), _p(k_pages), _p(v_pages),
+                                            _stream(stream)), "il_synth_qkv_paged")
+
     def status_sync(self, stream=None):
         L.check(self.lib.il_status_sync(self.h, _stream(stream)), "device status")
 

@@ -84,10 +84,13 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
   if (!c->matched) { set_error("il_prefill_attn before il_prefix_match"); return IL_ERR_STATE; }
   if (B == 0) return IL_OK;
   cudaStream_t st = (cudaStream_t)s;
-  k_kv_append<<<c->num_sms * 8, 256, 0, st>>>(*c, B, cu_q, prefix_len, block_table, (const uint4*)k_new,
-                                              (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
-  IL_LAUNCH_CHECK("k_kv_append");
-  c->launches += 1;
+  if (k_new || v_new) {                                 // (both NULL: the suffix K / V are already in the pages)
+    if (!k_new || !v_new) { set_error("k_new and v_new: both or neither"); return IL_ERR_ARG; }
+    k_kv_append<<<c->num_sms * 8, 256, 0, st>>>(*c, B, cu_q, prefix_len, block_table, (const uint4*)k_new,
+                                                (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
+    IL_LAUNCH_CHECK("k_kv_append");
+    c->launches += 1;
+  }
   return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
 }
 

@@ -33,9 +33,13 @@ __device__ __forceinline__ void synth_quad(uint64_t row_key, uint32_t e, float m
 
 // One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
 // row and tensor; each element then costs one mix.  Lanes write 8 consecutive bf16 (16 B).
-template <int D>
+// PAGED: K and V go straight into the request's KV pages ([C][Hkv][16][d], page =
+// block_table[i][pos / 16], slot pos % 16) -- the projection's epilogue writing the paged cache, so
+// il_prefill_attn needs no separate append pass.
+template <int D, bool PAGED>
 __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
                                                const int32_t* __restrict__ cu_q, const int32_t* __restrict__ prefix_len,
+                                               const int32_t* __restrict__ block_table,
                                                uint64_t sq, uint64_t sk, uint64_t sv, float qmul, float kvmul,
                                                __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ kn,
                                                __nv_bfloat16* __restrict__ vn) {
@@ -52,6 +56,7 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
     const uint64_t kk = mix64(mix64(sk ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint64_t kv = mix64(mix64(sv ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint32_t nvec = (Hq + 2 * Hkv) * VPH;
+    const size_t page_row = PAGED ? (size_t)(uint32_t)block_table[(size_t)i * c.max_blocks + pos / BS] * Hkv : 0;
     for (uint32_t e = lane; e < nvec; e += 32) {
       const uint32_t h = e / VPH, x0 = (e % VPH) * 8;
       uint64_t key;
@@ -59,8 +64,13 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
       __nv_bfloat16* dst;
       uint32_t hh;
       if (h < Hq) { key = kq; mul = qmul; hh = h; dst = q + ((size_t)r * Hq + h) * D + x0; }
-      else if (h < Hq + Hkv) { key = kk; mul = kvmul; hh = h - Hq; dst = kn + ((size_t)r * Hkv + hh) * D + x0; }
-      else { key = kv; mul = kvmul; hh = h - Hq - Hkv; dst = vn + ((size_t)r * Hkv + hh) * D + x0; }
+      else if (h < Hq + Hkv) {
+        key = kk; mul = kvmul; hh = h - Hq;
+        dst = kn + (PAGED ? ((page_row + hh) * BS + pos % BS) * D : ((size_t)r * Hkv + hh) * D) + x0;
+      } else {
+        key = kv; mul = kvmul; hh = h - Hq - Hkv;
+        dst = vn + (PAGED ? ((page_row + hh) * BS + pos % BS) * D : ((size_t)r * Hkv + hh) * D) + x0;
+      }
       uint32_t w[4];
       synth_quad(key, hh * 64 + x0 / 4, mul, w[0], w[1]);
       synth_quad(key, hh * 64 + x0 / 4 + 1, mul, w[2], w[3]);
@@ -73,20 +83,36 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
 
 using namespace il;
 
-extern "C" il_status il_synth_qkv(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
-                                  const int32_t* prefix_len, uint64_t seed, float q_scale, il_bf16* q,
-                                  il_bf16* k_new, il_bf16* v_new, il_stream s) {
+template <bool PAGED>
+static il_status synth_launch(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
+                              const int32_t* prefix_len, const int32_t* block_table, uint64_t seed, float q_scale,
+                              il_bf16* q, il_bf16* kd, il_bf16* vd, il_stream s) {
   if (B == 0) return IL_OK;
   auto tseed = [&](uint64_t salt) { return mix64((seed << 8) ^ salt); };
   const float unit = 2.0f;                             // x = (f - 1.5) * 2 * scale
   const uint32_t d = c->cfg.head_dim;
   if (d == 128)
-    k_synth<128><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),
-        tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (__nv_bfloat16*)v_new);
+    k_synth<128, PAGED><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, block_table,
+        tseed(0x51), tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)kd,
+        (__nv_bfloat16*)vd);
   else
-    k_synth<64><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, tseed(0x51),
-        tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (__nv_bfloat16*)v_new);
+    k_synth<64, PAGED><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, block_table,
+        tseed(0x51), tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)kd,
+        (__nv_bfloat16*)vd);
   IL_LAUNCH_CHECK("k_synth");
   c->launches += 1;
   return IL_OK;
+}
+
+extern "C" il_status il_synth_qkv(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
+                                  const int32_t* prefix_len, uint64_t seed, float q_scale, il_bf16* q,
+                                  il_bf16* k_new, il_bf16* v_new, il_stream s) {
+  return synth_launch<false>(c, B, prompt_tok, cu_q, prefix_len, nullptr, seed, q_scale, q, k_new, v_new, s);
+}
+
+extern "C" il_status il_synth_qkv_paged(il_ctx* c, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
+                                        const int32_t* prefix_len, const int32_t* block_table, uint64_t seed,
+                                        float q_scale, il_bf16* q, il_bf16* k_pages, il_bf16* v_pages, il_stream s) {
+  if (!c->matched) { set_error("il_synth_qkv_paged before il_prefix_match"); return IL_ERR_STATE; }
+  return synth_launch<true>(c, B, prompt_tok, cu_q, prefix_len, block_table, seed, q_scale, q, k_pages, v_pages, s);
 }

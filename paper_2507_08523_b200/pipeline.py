@@ -21,12 +21,16 @@ def _dev_u32(a, device) -> torch.Tensor:
 
 class Pipeline:
     def __init__(self, cfg: Config, device="cuda", qkv_seed: int = 3000, q_scale: float = 1.0,
-                 max_query_tokens: int | None = None, stream: torch.cuda.Stream | None = None):
+                 max_query_tokens: int | None = None, stream: torch.cuda.Stream | None = None,
+                 fused_kv: bool = False):
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream
         self.ctx = Context(cfg, self.device, stream)
         self.qkv_seed, self.q_scale = qkv_seed, q_scale
+        # fused_kv: the projection stand-in writes K / V straight into the pages (il_synth_qkv_paged)
+        # and il_prefill_attn skips its append pass
+        self.fused_kv = fused_kv
         B, S, MB, k = cfg.max_batch, cfg.max_prompt_tokens, cfg.max_blocks, cfg.k
         dev, i32 = self.device, torch.int32
         self.topk = torch.zeros(B, k, dtype=i32, device=dev)
@@ -92,12 +96,17 @@ class Pipeline:
 
     def synth(self, B=None) -> None:
         B = self.B if B is None else B
+        if self.fused_kv:
+            self.ctx.synth_qkv_paged(B, self.prompt_tok, self.cu_q, self.prefix_len, self.block_table, self.qkv_seed,
+                                     self.q_scale, self.q, self.k_pages, self.v_pages, stream=self.stream)
+            return
         self.ctx.synth_qkv(B, self.prompt_tok, self.cu_q, self.prefix_len, self.qkv_seed, self.q_scale,
                            self.q, self.k_new, self.v_new, stream=self.stream)
 
     def attn(self, B=None, lse: bool = True) -> None:
         B = self.B if B is None else B
-        self.ctx.prefill_attn(B, self.cu_q, self.prefix_len, self.block_table, self.q, self.k_new, self.v_new,
+        kn, vn = (None, None) if self.fused_kv else (self.k_new, self.v_new)
+        self.ctx.prefill_attn(B, self.cu_q, self.prefix_len, self.block_table, self.q, kn, vn,
                               self.k_pages, self.v_pages, self.out, self.lse if lse else None, self.scale,
                               stream=self.stream)
 

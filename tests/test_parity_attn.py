@@ -32,8 +32,18 @@ def check_request(pl, r, i, sp, seed, q_scale, max_rows=None):
     kb = gen.synth_bf16_bits(seed, "k", toks, pos, sp.Hkv, sp.d)
     vb = gen.synth_bf16_bits(seed, "v", toks, pos, sp.Hkv, sp.d)
     np.testing.assert_array_equal(bf16_bits(pl.q[r0:r0 + S]), qb)
-    np.testing.assert_array_equal(bf16_bits(pl.k_new[r0:r0 + S]), kb[P:])
-    np.testing.assert_array_equal(bf16_bits(pl.v_new[r0:r0 + S]), vb[P:])
+    if getattr(pl, "fused_kv", False):
+        # the projection stand-in wrote K / V into the request's pages: read them back by position
+        bt = pl.block_table[i].cpu().numpy()
+        pages = torch.from_numpy(bt[pos[P:] // 16].astype(np.int64)).to(pl.k_pages.device)
+        slot = torch.from_numpy((pos[P:] % 16).astype(np.int64)).to(pl.k_pages.device)
+        kp = pl.k_pages[pages, :, slot]                   # [S][Hkv][d]
+        vp = pl.v_pages[pages, :, slot]
+        np.testing.assert_array_equal(bf16_bits(kp), kb[P:])
+        np.testing.assert_array_equal(bf16_bits(vp), vb[P:])
+    else:
+        np.testing.assert_array_equal(bf16_bits(pl.k_new[r0:r0 + S]), kb[P:])
+        np.testing.assert_array_equal(bf16_bits(pl.v_new[r0:r0 + S]), vb[P:])
     rows = np.arange(S) if max_rows is None or S <= max_rows else np.unique(
         np.concatenate([np.arange(4), np.linspace(0, S - 1, max_rows).astype(int)]))
     ref, lse = O.attention(gen.bf16_bits_to_f64(qb)[rows[-1] * 0:], gen.bf16_bits_to_f64(kb),
@@ -46,10 +56,11 @@ def check_request(pl, r, i, sp, seed, q_scale, max_rows=None):
     return float(err.max())
 
 
-def run(sp: StreamSpec, n_batches: int, seed=3000, q_scale=1.0, sample=6, max_rows=None):
+def run(sp: StreamSpec, n_batches: int, seed=3000, q_scale=1.0, sample=6, max_rows=None, fused=False):
     ds, pool, instr = make_stream(sp)
     o = oracle_for(sp, pool, instr)
     pl = gpu_pipeline(sp, pool, instr)
+    pl.fused_kv = fused
     pl.qkv_seed, pl.q_scale = seed, q_scale
     rng = np.random.default_rng(0)
     worst = 0.0
@@ -70,6 +81,13 @@ def run(sp: StreamSpec, n_batches: int, seed=3000, q_scale=1.0, sample=6, max_ro
 
 def test_attention_c1_shape():
     run(StreamSpec(B=24), n_batches=4)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_attention_fused_kv_into_pages(d):
+    # il_synth_qkv_paged writes the suffix K / V into the pages, il_prefill_attn skips its append
+    sp = StreamSpec(B=24, k=5, Hq=32 if d == 128 else 4, Hkv=8 if d == 128 else 4, d=d, max_prompt_tokens=1024)
+    run(sp, n_batches=4, fused=True, sample=10)
 
 
 def test_attention_llama_gqa_shape():
