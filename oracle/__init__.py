@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC = [os.path.join(HERE, "oracle.cpp"), os.path.join(HERE, "oracle.h")]
 
 SIM_COSINE, SIM_JACCARD = 0, 1
-F_PAIR, F_GUARD, F_EXCLUDE_SELF, F_VERIFY = 1, 2, 4, 8
+F_PAIR, F_GUARD, F_EXCLUDE_SELF, F_VERIFY, F_DEDUP = 1, 2, 4, 8, 16
 
 
 def build(force: bool = False) -> str:

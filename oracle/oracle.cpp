@@ -345,6 +345,37 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
   }
   for (u32 i = 0; i < B; ++i) if (err[i]) return err[i];
 
+  // NEXT-1 in-batch dedup (OR_F_DEDUP; Z22b): a block that an earlier request of the
+  // same rank computes in this batch (a full block at its position >= its own hit count h) is
+  // not computed again.  Owner of a hash = the lowest admission index presenting it that way (and
+  // its depth); request i's leading run continues from its hit count h_i through blocks whose
+  // owner is an earlier request at the same depth with equal block tokens, capped as Z20.  The
+  // run's pages are the owner's; only the snapshot hits [0, h_i) are touched and pinned.
+  std::vector<u32> hloc = h;
+  if (st[0]->flags & OR_F_DEDUP) {
+    for (u32 r = 0; r < G; ++r) {
+      std::map<u64, std::pair<u32, u32>> own;           // hash -> (first request, depth)
+      for (u32 i = 0; i < B; ++i) {
+        if (owner[i] != r) continue;
+        for (u32 j = hloc[i]; j < H[i].size(); ++j) own.emplace(H[i][j], std::make_pair(i, j));
+      }
+      for (u32 i = 0; i < B; ++i) {
+        if (owner[i] != r) continue;
+        const u32 cap = cap_hits((u32)H[i].size(), prompt[i].size());
+        u32 he = hloc[i];
+        while (he < cap) {
+          auto it = own.find(H[i][he]);
+          if (it == own.end() || it->second.first >= i || it->second.second != he) break;
+          const u32 o = it->second.first;
+          if (!std::equal(&prompt[o][he * BS], &prompt[o][he * BS] + BS, &prompt[i][he * BS])) break;
+          he += 1;
+        }
+        h[i] = he;
+        boxh[i] = std::max(boxh[i], he);
+      }
+    }
+  }
+
   // Step 7 per rank: touch + pin the hit blocks, then evict for the pages its slice needs (Z21).
   std::vector<std::vector<u64>> victims(G);
   for (u32 r = 0; r < G; ++r) {
@@ -353,7 +384,7 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
     u64 need = 0;
     for (u32 i = 0; i < B; ++i) {
       if (owner[i] != r) continue;
-      for (u32 j = 0; j < h[i]; ++j) pinned.insert(H[i][j]);
+      for (u32 j = 0; j < hloc[i]; ++j) pinned.insert(H[i][j]);
       need += (prompt[i].size() + s->decode + BS - 1) / BS - h[i];   // (+ the decode reserve)
     }
     u64 free_pages = s->C - s->index.size();
@@ -379,7 +410,7 @@ static int run_batch_dp(or_state** st, u32 G, u32 B, const u32* q_off, const u32
   std::vector<u32> lo(G + 1);
   for (u32 r = 0; r <= G; ++r) lo[r] = (u32)((u64)r * B / G);
   for (u32 i = 0; i < B; ++i)
-    for (u32 j = 0; j < h[i]; ++j) st[owner[i]]->index[H[i][j]].stamp = stamp_of(b, i - lo[owner[i]]);
+    for (u32 j = 0; j < hloc[i]; ++j) st[owner[i]]->index[H[i][j]].stamp = stamp_of(b, i - lo[owner[i]]);
   for (u32 r = 0; r < G; ++r)
     for (u64 v : victims[r]) st[r]->index.erase(v);
 

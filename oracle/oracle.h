@@ -22,7 +22,7 @@ extern "C" {
 #endif
 
 enum { OR_SIM_COSINE = 0, OR_SIM_JACCARD = 1 };
-enum { OR_F_PAIR = 1u << 0, OR_F_GUARD = 1u << 1, OR_F_EXCLUDE_SELF = 1u << 2, OR_F_VERIFY = 1u << 3 };
+enum { OR_F_PAIR = 1u << 0, OR_F_GUARD = 1u << 1, OR_F_EXCLUDE_SELF = 1u << 2, OR_F_VERIFY = 1u << 3, OR_F_DEDUP = 1u << 4 };
 
 typedef struct or_state or_state;
 
