@@ -65,7 +65,12 @@ enum {
   IL_F_PAIR = 1u << 0,         /* PAIR on; off = naive prefix caching (paper baseline "PC") */
   IL_F_GUARD = 1u << 1,        /* never-worse guard (Z25; not in the paper) */
   IL_F_EXCLUDE_SELF = 1u << 2, /* a query never selects its own dataset row */
-  IL_F_VERIFY = 1u << 3        /* a hit also requires equal block tokens + parent hash (Z19) */
+  IL_F_VERIFY = 1u << 3,       /* a hit also requires equal block tokens + parent hash (Z19) */
+  IL_F_DEDUP = 1u << 4         /* NEXT-1 in-batch dedup (Z22b): a full block an earlier
+                                  request of the batch computes (same depth, same prefix, equal
+                                  tokens) is not computed again; the later request's hit run
+                                  continues through it and its block table points at the
+                                  earlier request's page.  hit_blocks then counts those too. */
 };
 
 typedef struct {
@@ -113,12 +118,13 @@ typedef struct {               /* counters of the last committed batch (il_stats
   uint32_t index_rebuilds;     /* tombstone compactions so far */
   uint32_t status;             /* latched il_status */
   uint64_t launches;           /* kernels this context has launched so far */
-  uint32_t hit_blocks;         /* sum of capped hits of the last il_prefix_match (this rank) */
+  uint32_t hit_blocks;         /* sum of capped hits of the last il_prefix_match (this rank;
+                                  with IL_F_DEDUP including the in-batch shared blocks) */
   uint32_t box_hit_blocks;     /* the same against the box (this rank's index or the residency map) */
   uint32_t full_blocks;        /* sum of floor(L_i / 16) of the last il_prefix_match */
   uint32_t record_backlog;     /* block records waiting for a later il_commit_export */
   uint32_t map_slots_used;     /* residency-map slots holding a key (live or dead) */
-  uint32_t reserved;
+  uint32_t dedup_blocks;       /* IL_F_DEDUP: blocks of hit_blocks shared in-batch (not cached) */
 } il_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */

@@ -18,7 +18,7 @@ IL_OK, IL_ERR_ARG, IL_ERR_CAPACITY, IL_ERR_STATE, IL_ERR_INTERNAL, IL_ERR_CUDA =
 STATUS_NAMES = {0: "IL_OK", 1: "IL_ERR_ARG", 2: "IL_ERR_CAPACITY", 3: "IL_ERR_STATE",
                 4: "IL_ERR_INTERNAL", 5: "IL_ERR_CUDA"}
 IL_SIM_COSINE, IL_SIM_JACCARD = 0, 1
-IL_F_PAIR, IL_F_GUARD, IL_F_EXCLUDE_SELF, IL_F_VERIFY = 1, 2, 4, 8
+IL_F_PAIR, IL_F_GUARD, IL_F_EXCLUDE_SELF, IL_F_VERIFY, IL_F_DEDUP = 1, 2, 4, 8, 16
 
 # every symbol include/il.h declares (checked by tests/test_abi.py)
 EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "il_stats_sync", "il_stats_async",
@@ -55,7 +55,7 @@ class il_stats(C.Structure):
                 ("suffix_tokens", C.c_uint32), ("index_rebuilds", C.c_uint32), ("status", C.c_uint32),
                 ("launches", C.c_uint64), ("hit_blocks", C.c_uint32), ("box_hit_blocks", C.c_uint32),
                 ("full_blocks", C.c_uint32), ("record_backlog", C.c_uint32), ("map_slots_used", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("dedup_blocks", C.c_uint32)]
 
 
 assert C.sizeof(il_refine_info) == 16

@@ -76,6 +76,15 @@ static size_t carve(Ctx* c, void* ws) {
   c->pair_nsh = w.take<uint32_t>((size_t)g.max_suffix_tokens / 32 + B + 1);
   c->attn_ml = w.take<float>((size_t)g.max_suffix_tokens * g.n_q_heads);
   c->evicted_list = w.take<uint64_t>(C);
+  c->hit_local = w.take<uint32_t>(B);
+  if (g.flags & IL_F_DEDUP) {                          // every full block of the batch, half full
+    uint32_t n = 1024;
+    while (n < 2ull * B * MB) n <<= 1;
+    c->bd_mask = n - 1;
+    c->bd_key = w.take<uint64_t>(n); c->bd_owner = w.take<uint32_t>(n);
+  } else {
+    c->bd_mask = 0; c->bd_key = nullptr; c->bd_owner = nullptr;
+  }
   c->guard_prompt = (g.flags & IL_F_GUARD) ? w.take<uint32_t>(B * g.max_prompt_tokens) : nullptr;
   // inverted index for large pools (a1-a2, select_inv.cu): slots for every (token, chunk) key
   if (g.max_pool > SIM_BIG_POOL) {
@@ -125,6 +134,7 @@ static il_status validate(const il_config* g) {
     set_error("at most 32 ranks (max_global_batch / max_batch)"); return IL_ERR_ARG;
   }
   if (g->max_block_records > (1u << 24)) { set_error("max_block_records <= 2^24"); return IL_ERR_ARG; }
+  if (g->flags & ~0x1Fu) { set_error("unknown il_config.flags bits"); return IL_ERR_ARG; }
   if (g->reserved1 != 0) { set_error("il_config.reserved1 must be 0"); return IL_ERR_ARG; }
   if (g->max_decode_tokens >= g->max_prompt_tokens) { set_error("max_decode_tokens >= max_prompt_tokens"); return IL_ERR_ARG; }
   if (g->max_prompt_tokens < 16 || (g->max_prompt_tokens % 16)) { set_error("max_prompt_tokens: multiple of 16"); return IL_ERR_ARG; }
@@ -364,7 +374,7 @@ static __global__ void k_stats(Ctx c, il_stats* out, uint64_t launches) {
   out->full_blocks = h.full_sum;
   out->record_backlog = (uint32_t)(h.ring_tail - h.ring_head);
   out->map_slots_used = h.map_used;
-  out->reserved = 0;
+  out->dedup_blocks = h.dedup_sum;
 }
 
 il_status il_stats_async(il_ctx* c, il_stats* out, il_stream s) {
@@ -394,7 +404,7 @@ il_status il_stats_sync(il_ctx* c, il_stream s, il_stats* out) {
   out->full_blocks = h.full_sum;
   out->record_backlog = (uint32_t)(h.ring_tail - h.ring_head);
   out->map_slots_used = h.map_used;
-  out->reserved = 0;
+  out->dedup_blocks = h.dedup_sum;
   return IL_OK;
 }
 

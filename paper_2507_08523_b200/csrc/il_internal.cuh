@@ -60,7 +60,8 @@ struct DevScalars {
   uint32_t map_rebuilds;
   uint64_t ring_head;        // block-record FIFO (monotonic counters)
   uint64_t ring_tail;
-  uint32_t pad1[4];
+  uint32_t dedup_sum;        // last prefix match: blocks shared in-batch (IL_F_DEDUP)
+  uint32_t pad1[3];
 };
 
 struct Ctx {
@@ -125,6 +126,12 @@ struct Ctx {
   uint64_t *map_tmp_key;     //   rebuild scratch
   uint32_t *map_tmp_mask;
   uint32_t *box_hit;         // per request: box-level hit count of the last prefix match
+  // in-batch dedup (IL_F_DEDUP, match.cu): snapshot hits before dedup, and the batch's table
+  // hash -> lowest admission index presenting it as a block it computes
+  uint32_t *hit_local;
+  uint64_t *bd_key;          // 0 = empty (chain hashes are never 0, Z18)
+  uint32_t *bd_owner;
+  uint32_t bd_mask = 0;
   uint32_t *icl_fds;         // il_commit_apply: gathered ICL records, global admission order
   il_refine_info *icl_info;
   bool map_active = false;   // host: an il_commit_apply with n_ranks > 1 has run

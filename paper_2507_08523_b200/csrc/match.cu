@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
   }
   if (lane == 0) {
     hit[i] = h;
+    c.hit_local[i] = h;
     if (newly) atomicAdd(&c.sc->pinned, newly);
     atomicAdd(&c.sc->hit_sum, h);
     atomicAdd(&c.sc->full_sum, L / BS);
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(Ctx c, uint32_t B, const ui
   const uint32_t nI = min(c.n_instr_blocks, 1024u);
   for (uint32_t x = tid; x <= nI; x += 1024) s_top[x] = -1;
   __syncthreads();
-  for (uint32_t i = tid; i < B; i += 1024) atomicMax(&s_top[min(hit[i], nI)], (int32_t)i);
+  for (uint32_t i = tid; i < B; i += 1024) atomicMax(&s_top[min(c.hit_local[i], nI)], (int32_t)i);
   __syncthreads();
   // suffix max: s_top[c] = max over c' >= c (a block max-scan over the reversed entries)
   if (nI < 1024) {
@@ -278,10 +279,113 @@ __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uin
   int32_t* bt = block_table + (size_t)i * c.max_blocks;
   for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
 }
+// NEXT-1 in-batch dedup (IL_F_DEDUP; Z22b, oracle run_batch_dp).  The batch's table
+// of computed blocks: hash -> the lowest admission index presenting it at a position >= its own
+// snapshot hit count.  A later request's leading run continues from its snapshot hits through
+// blocks owned by an earlier request at the same depth with equal tokens (capped as Z20); those
+// blocks' pages are the owner's.  Only the snapshot hits were touched and pinned (k_hash_match).
+__device__ __forceinline__ uint32_t bd_slot0(const Ctx& c, uint64_t H) {
+  return (uint32_t)((H >> 17) ^ (H >> 40)) & c.bd_mask;    // (bits other than the index table's)
+}
+__device__ __forceinline__ uint32_t bd_find(const Ctx& c, uint64_t H) {
+  for (uint32_t s = bd_slot0(c, H);; s = (s + 1) & c.bd_mask) {
+    const uint64_t k = c.bd_key[s];
+    if (k == H) return c.bd_owner[s];
+    if (k == 0) return NONE32;
+  }
+}
+__global__ void __launch_bounds__(256) k_bd_clear(Ctx c) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s <= c.bd_mask; s += gridDim.x * blockDim.x) {
+    c.bd_key[s] = 0;
+    c.bd_owner[s] = NONE32;
+  }
+}
+// warp per request: every full block at j >= h_i (the blocks request i computes) -> owner min i
+__global__ void __launch_bounds__(256) k_bd_insert(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
+                                                   const uint64_t* __restrict__ block_hash,
+                                                   const uint32_t* __restrict__ hit) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t F = prompt_len[i] / BS;
+  const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
+  for (uint32_t j = hit[i] + lane; j < F; j += 32) {
+    const uint64_t H = bh[j];
+    uint32_t s = bd_slot0(c, H);
+    while (true) {
+      const uint64_t k = c.bd_key[s];
+      if (k == H) break;
+      if (k == 0) {
+        const uint64_t old = atomicCAS((unsigned long long*)&c.bd_key[s], 0ull, (unsigned long long)H);
+        if (old == 0 || old == H) break;
+      }
+      s = (s + 1) & c.bd_mask;
+    }
+    atomicMin(&c.bd_owner[s], i);
+  }
+}
+// warp per request: extend hit[i] through blocks an earlier request computes
+__global__ void __launch_bounds__(256) k_bd_resolve(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
+                                                    const uint32_t* __restrict__ prompt_len,
+                                                    const uint64_t* __restrict__ block_hash,
+                                                    uint32_t* __restrict__ hit) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  const uint32_t L = prompt_len[i], F = L / BS, cap = L ? (L - 1) / BS : 0, lim = min(F, cap);
+  const uint32_t hl = hit[i];
+  const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
+  const uint32_t* row = prompt_tok + (size_t)i * c.cfg.max_prompt_tokens;
+  uint32_t he = hl;
+  for (uint32_t base = hl; base < lim; base += 32) {
+    const uint32_t j = base + lane;
+    bool ok = false;
+    if (j < lim) {
+      const uint64_t H = bh[j];
+      const uint32_t o = bd_find(c, H);
+      if (o < i && block_hash[(size_t)o * c.max_blocks + j] == H) {
+        const uint4* a = reinterpret_cast<const uint4*>(row + (size_t)BS * j);
+        const uint4* b = reinterpret_cast<const uint4*>(prompt_tok + (size_t)o * c.cfg.max_prompt_tokens + (size_t)BS * j);
+        ok = true;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 x = a[q], y = b[q];
+          ok &= x.x == y.x && x.y == y.y && x.z == y.z && x.w == y.w;
+        }
+      }
+    }
+    const uint32_t m = __ballot_sync(~0u, ok);
+    const uint32_t lead = (m == ~0u) ? 32u : (uint32_t)(__ffs(~m) - 1);
+    he += lead;
+    if (lead < 32) break;
+  }
+  if (lane == 0 && he > hl) {
+    hit[i] = he;
+    atomicAdd(&c.sc->dedup_sum, he - hl);
+    atomicAdd(&c.sc->hit_sum, he - hl);
+    if (!c.map_active) {                              // box-level hits include the shared run (oracle)
+      atomicAdd(&c.sc->box_hit_sum, he - hl);
+    } else if (he > c.box_hit[i]) {
+      atomicAdd(&c.sc->box_hit_sum, he - c.box_hit[i]);
+      c.box_hit[i] = he;
+    }
+  }
+}
+// warp per request, after k_alloc_fill: the shared run's block-table entries = the owner's pages
+__global__ void __launch_bounds__(256) k_bd_fill(Ctx c, uint32_t B, const uint64_t* __restrict__ block_hash,
+                                                 const uint32_t* __restrict__ hit, int32_t* __restrict__ block_table) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= B) return;
+  if (c.sc->status == IL_ERR_CAPACITY) return;
+  const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
+  for (uint32_t j = c.hit_local[i] + lane; j < hit[i]; j += 32) {
+    const uint32_t o = bd_find(c, bh[j]);
+    block_table[(size_t)i * c.max_blocks + j] = block_table[(size_t)o * c.max_blocks + j];
+  }
+}
+
 // (a kernel rather than a memset node: keeps the captured match graph all-kernel)
 __global__ void k_match_begin(Ctx c) {
   DevScalars* sc = c.sc;
-  sc->pinned = 0; sc->hit_sum = 0; sc->full_sum = 0; sc->box_hit_sum = 0; sc->inserted = 0;
+  sc->pinned = 0; sc->hit_sum = 0; sc->full_sum = 0; sc->box_hit_sum = 0; sc->inserted = 0; sc->dedup_sum = 0;
 }
 __global__ void k_alloc_commit(Ctx c) {
   DevScalars* sc = c.sc;
@@ -309,9 +413,15 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)s;
   const uint64_t b_cur = c->batch + 1;
+  const bool dedup = (c->cfg.flags & IL_F_DEDUP) && B > 1;
   k_match_begin<<<1, 1, 0, st>>>(*c);
+  if (dedup) k_bd_clear<<<c->num_sms * 4, 256, 0, st>>>(*c);
   k_instr_probe<<<1, 256, 0, st>>>(*c);
   if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
+  if (dedup) {
+    k_bd_insert<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, block_hash, hit);
+    k_bd_resolve<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit);
+  }
   k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q, b_cur);
   {
     Ctx cc = *c;
@@ -320,9 +430,10 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
     IL_CUDA(cudaLaunchCooperativeKernel((void*)k_evict, dim3(c->ev_blocks), dim3(EV_THREADS), args, 0, st));
   }
   if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
+  if (dedup) k_bd_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, block_hash, hit, block_table);
   k_alloc_commit<<<1, 1, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_prefix_match");
-  c->launches += B ? 7 : 5;
+  c->launches += (B ? 7 : 5) + (dedup ? 4 : 0);
   c->prompt_tok = prompt_tok;
   c->prompt_len = prompt_len;
   c->block_hash = block_hash;
