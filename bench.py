@@ -163,7 +163,8 @@ def config_dict(cfg, args, world, ds):
     return {"workload": cfg.name, "baseline_config": f"configs[{args.config - 1}]",
             "requests_per_gpu_per_step": cfg.B, "k": cfg.k, "pool": cfg.M, "instr_tokens": cfg.n_instr,
             "table_capacity": cfg.T, "kv_pages": cfg.C, "heads_q_kv_d": [cfg.Hq, cfg.Hkv, cfg.d],
-            "layers": 1, "flags": "naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")),
+            "layers": 1, "flags": ("naive-PC" if args.naive else ("PAIR+verify" + ("" if args.no_guard else "+guard")))
+            + ("+batch-dedup" if args.batch_dedup else ""),
             "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (request shards)",
             "stream": f"{ds.n} distinct logs, no query repeats within the run",
             "steady_state": "LRU eviction in every timed step" if not args.no_fill else "no fill",
@@ -174,7 +175,7 @@ def config_dict(cfg, args, world, ds):
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2507_08523_b200 import IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
+    from paper_2507_08523_b200 import IL_F_DEDUP, IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -184,6 +185,8 @@ def run_ours(args, rank, world, local_rank):
     flags = IL_F_PAIR | IL_F_VERIFY | (IL_F_GUARD if not args.no_guard else 0)
     if args.naive:
         flags = IL_F_VERIFY
+    if args.batch_dedup:
+        flags |= IL_F_DEDUP
     ccfg = Config(k=cfg.k, table_capacity=cfg.T, kv_pages=cfg.C, max_batch=cfg.B,
                   max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
                   max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
@@ -578,7 +581,7 @@ def run_c2(args, rank, world, local_rank):
     of the PAIR runs; per dataset: requests/s, block- and token-weighted hits, PAIR / naive hit
     ratio.  One GPU; ranks > 0 exit (the datasets are independent problems)."""
     import torch
-    from paper_2507_08523_b200 import IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
+    from paper_2507_08523_b200 import IL_F_DEDUP, IL_F_GUARD, IL_F_PAIR, IL_F_VERIFY, Config, Pipeline
     if rank != 0:
         return
     torch.cuda.set_device(local_rank)
@@ -602,7 +605,7 @@ def run_c2(args, rank, world, local_rank):
                           max_prompt_tokens=cfg.max_prompt_tokens, max_pool=cfg.M,
                           max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                           max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
-                          head_dim=cfg.d, flags=flags)
+                          head_dim=cfg.d, flags=flags | (IL_F_DEDUP if args.batch_dedup else 0))
             pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream)
             with torch.cuda.stream(stream):
                 pl.load_pool(pool, instr)
@@ -634,6 +637,10 @@ def run_c2(args, rank, world, local_rank):
                 hits += int(H_.sum()); fulls += int((L_ // 16).sum()); htok += int(16 * H_.sum()); atok += int(L_.sum())
             row[mode] = {"requests_per_s": ds.n / (ms * 1e-3), "ms": ms, "block_hit_pct": 100.0 * hits / max(fulls, 1),
                          "token_hit_pct": 100.0 * htok / max(atok, 1)}
+            if args.batch_dedup:                       # hits above include the in-batch shared blocks
+                dd = sum(pl.ctx.stats_from_bytes(stats[j].cpu().numpy())["dedup_blocks"] for j in range(len(ins)))
+                row[mode]["dedup_blocks"] = int(dd)
+                row[mode]["cache_block_hit_pct"] = 100.0 * (hits - dd) / max(fulls, 1)
             if mode == "pair" and not warm:
                 tot_req += ds.n; tot_ms += ms
             del pl
@@ -726,6 +733,8 @@ def run_reference(args, rank, world):
     cfg, ds, pool, instr = workload(args.config, 0, world, n_queries=n_queries_for(cfg0, args, world))
     import oracle as O
     flags = O.F_VERIFY if args.naive else (O.F_PAIR | O.F_VERIFY | (0 if args.no_guard else O.F_GUARD))
+    if args.batch_dedup:
+        flags |= O.F_DEDUP
     K, W = args.steps, args.warmup
     n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
     plans = [plan_batches(cfg, n_fill_max + W + 2 * K, r, world) for r in range(world)]
@@ -827,6 +836,8 @@ def main():
                     help="K / V to k_new / v_new and il_prefill_attn's append pass (instead of the projection "
                          "stand-in writing the pages)")
     ap.add_argument("--dedup", action="store_true", help="query only the first occurrence of each distinct log")
+    ap.add_argument("--batch-dedup", action="store_true",
+                    help="IL_F_DEDUP (NEXT-1): a block an earlier request of the batch computes is not computed again")
     ap.add_argument("--cpu-attn-sample", type=int, default=32, help="--impl reference: fp64 attention requests per step")
     ap.add_argument("--cpu-baseline-attn", type=int, default=400, help="cpu_baseline: fp64 attention requests sampled")
     ap.add_argument("--cpu-baseline-batches", type=int, default=4, help="cpu_baseline: full batches of the integer path")

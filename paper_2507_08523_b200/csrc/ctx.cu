@@ -81,9 +81,9 @@ static size_t carve(Ctx* c, void* ws) {
     uint32_t n = 1024;
     while (n < 2ull * B * MB) n <<= 1;
     c->bd_mask = n - 1;
-    c->bd_key = w.take<uint64_t>(n); c->bd_owner = w.take<uint32_t>(n);
+    c->bd_key = w.take<uint64_t>(n); c->bd_owner = w.take<uint32_t>(n); c->bd_list = w.take<uint32_t>(B * MB);
   } else {
-    c->bd_mask = 0; c->bd_key = nullptr; c->bd_owner = nullptr;
+    c->bd_mask = 0; c->bd_key = nullptr; c->bd_owner = c->bd_list = nullptr;
   }
   c->guard_prompt = (g.flags & IL_F_GUARD) ? w.take<uint32_t>(B * g.max_prompt_tokens) : nullptr;
   // inverted index for large pools (a1-a2, select_inv.cu): slots for every (token, chunk) key
@@ -164,6 +164,8 @@ __global__ void k_reset_index(Ctx c) {
     c.tab_stamp[t] = 0;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4096; t += stride) c.hist[t] = 0;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.dd_mask; t += stride) { c.dd_key[t] = 0; c.dd_max[t] = 0; }
+  if (c.bd_key)
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.bd_mask; t += stride) { c.bd_key[t] = 0; c.bd_owner[t] = 0; }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevScalars z;
     memset(&z, 0, sizeof(z));

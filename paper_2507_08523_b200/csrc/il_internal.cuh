@@ -61,7 +61,8 @@ struct DevScalars {
   uint64_t ring_head;        // block-record FIFO (monotonic counters)
   uint64_t ring_tail;
   uint32_t dedup_sum;        // last prefix match: blocks shared in-batch (IL_F_DEDUP)
-  uint32_t pad1[3];
+  uint32_t bd_n;             // in-batch dedup table: slots taken this batch (cleared by k_alloc_commit)
+  uint32_t pad1[2];
 };
 
 struct Ctx {
@@ -130,7 +131,8 @@ struct Ctx {
   // hash -> lowest admission index presenting it as a block it computes
   uint32_t *hit_local;
   uint64_t *bd_key;          // 0 = empty (chain hashes are never 0, Z18)
-  uint32_t *bd_owner;
+  uint32_t *bd_owner;        // ~(lowest admission index); 0 = none
+  uint32_t *bd_list;         // slots taken this batch
   uint32_t bd_mask = 0;
   uint32_t *icl_fds;         // il_commit_apply: gathered ICL records, global admission order
   il_refine_info *icl_info;

@@ -9,13 +9,45 @@ namespace cg = cooperative_groups;
 
 namespace il {
 
+// NEXT-1 in-batch dedup (IL_F_DEDUP; DESIGN.md Z22b, oracle run_batch_dp).  The batch's table
+// of computed blocks: hash -> the lowest admission index presenting it at a position >= its own
+// snapshot hit count.  A later request's leading run continues from its snapshot hits through
+// blocks owned by an earlier request at the same depth with equal tokens (capped as Z20); those
+// blocks' pages are the owner's.  Only the snapshot hits were touched and pinned (k_hash_match).
+__device__ __forceinline__ uint32_t bd_slot0(const Ctx& c, uint64_t H) {
+  return (uint32_t)((H >> 17) ^ (H >> 40)) & c.bd_mask;    // (bits other than the index table's)
+}
+__device__ __forceinline__ uint32_t bd_find(const Ctx& c, uint64_t H) {
+  for (uint32_t s = bd_slot0(c, H);; s = (s + 1) & c.bd_mask) {
+    const uint64_t k = c.bd_key[s];
+    if (k == H) return ~c.bd_owner[s];
+    if (k == 0) return NONE32;
+  }
+}
+// (k_hash_match, per block j >= h_i of request i) owner <- min(owner, i); a slot taken for the
+// first time this batch goes on bd_list, which k_alloc_commit clears after the last lookup
+__device__ __forceinline__ void bd_insert(const Ctx& c, uint64_t H, uint32_t i) {
+  uint32_t s = bd_slot0(c, H);
+  while (true) {
+    const uint64_t k = c.bd_key[s];
+    if (k == H) break;
+    if (k == 0) {
+      const uint64_t old = atomicCAS((unsigned long long*)&c.bd_key[s], 0ull, (unsigned long long)H);
+      if (old == 0) { c.bd_list[atomicAdd(&c.sc->bd_n, 1u)] = s; break; }
+      if (old == H) break;
+    }
+    s = (s + 1) & c.bd_mask;
+  }
+  atomicMax(&c.bd_owner[s], ~i);
+}
+
 // K5: one warp per request.  Hashes every full block (block_hash row), finds the capped
 // leading run of resident + verified blocks in the snapshot index, writes the hit pages to
 // the block table, and touches + pins them: stamp <- max(stamp, (b, i)) (Z21).
 __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
                                                     const uint32_t* __restrict__ prompt_len,
                                                     uint64_t* __restrict__ block_hash, uint32_t* __restrict__ hit,
-                                                    int32_t* __restrict__ block_table, uint64_t) {
+                                                    int32_t* __restrict__ block_table, uint32_t dedup) {
   const uint64_t b_cur = c.sc->batch_done + 1;     // device batch counter (graph-replay safe)
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= B) return;
@@ -24,6 +56,8 @@ __global__ void __launch_bounds__(256) k_hash_match(Ctx c, uint32_t B, const uin
   int32_t* bt = block_table + (size_t)i * c.max_blocks;
   const uint32_t h = warp_hash_match(c, row, L, block_hash + (size_t)i * c.max_blocks, bt, false);
   __syncwarp();
+  if (dedup)                                        // the blocks this request computes -> dedup table
+    for (uint32_t j = h + lane; j < L / BS; j += 32) bd_insert(c, block_hash[(size_t)i * c.max_blocks + j], i);
   const uint64_t st = stamp_of(b_cur, i);
   const uint32_t epoch = (uint32_t)b_cur;
   uint32_t newly = 0;
@@ -269,7 +303,8 @@ __global__ void __launch_bounds__(EV_THREADS) k_evict(Ctx c, uint64_t) {
 
 // K6c: pop the batch's pages (free stack top) into the block table after the hit pages.
 __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
-                                                    const uint32_t* __restrict__ hit, int32_t* __restrict__ block_table) {
+                                                    const uint32_t* __restrict__ hit, const uint64_t* __restrict__ block_hash,
+                                                    int32_t* __restrict__ block_table) {
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= B) return;
   DevScalars* sc = c.sc;
@@ -278,50 +313,13 @@ __global__ void __launch_bounds__(256) k_alloc_fill(Ctx c, uint32_t B, const uin
   const uint32_t h = hit[i], nb = cdiv(prompt_len[i] + c.cfg.max_decode_tokens, BS);
   int32_t* bt = block_table + (size_t)i * c.max_blocks;
   for (uint32_t j = h + lane; j < nb; j += 32) bt[j] = (int32_t)c.free_list[base + (j - h)];
-}
-// NEXT-1 in-batch dedup (IL_F_DEDUP; DESIGN.md Z22b, oracle run_batch_dp).  The batch's table
-// of computed blocks: hash -> the lowest admission index presenting it at a position >= its own
-// snapshot hit count.  A later request's leading run continues from its snapshot hits through
-// blocks owned by an earlier request at the same depth with equal tokens (capped as Z20); those
-// blocks' pages are the owner's.  Only the snapshot hits were touched and pinned (k_hash_match).
-__device__ __forceinline__ uint32_t bd_slot0(const Ctx& c, uint64_t H) {
-  return (uint32_t)((H >> 17) ^ (H >> 40)) & c.bd_mask;    // (bits other than the index table's)
-}
-__device__ __forceinline__ uint32_t bd_find(const Ctx& c, uint64_t H) {
-  for (uint32_t s = bd_slot0(c, H);; s = (s + 1) & c.bd_mask) {
-    const uint64_t k = c.bd_key[s];
-    if (k == H) return c.bd_owner[s];
-    if (k == 0) return NONE32;
-  }
-}
-__global__ void __launch_bounds__(256) k_bd_clear(Ctx c) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s <= c.bd_mask; s += gridDim.x * blockDim.x) {
-    c.bd_key[s] = 0;
-    c.bd_owner[s] = NONE32;
-  }
-}
-// warp per request: every full block at j >= h_i (the blocks request i computes) -> owner min i
-__global__ void __launch_bounds__(256) k_bd_insert(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_len,
-                                                   const uint64_t* __restrict__ block_hash,
-                                                   const uint32_t* __restrict__ hit) {
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= B) return;
-  const uint32_t F = prompt_len[i] / BS;
-  const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
-  for (uint32_t j = hit[i] + lane; j < F; j += 32) {
-    const uint64_t H = bh[j];
-    uint32_t s = bd_slot0(c, H);
-    while (true) {
-      const uint64_t k = c.bd_key[s];
-      if (k == H) break;
-      if (k == 0) {
-        const uint64_t old = atomicCAS((unsigned long long*)&c.bd_key[s], 0ull, (unsigned long long)H);
-        if (old == 0 || old == H) break;
-      }
-      s = (s + 1) & c.bd_mask;
+  // IL_F_DEDUP: the in-batch shared run [snapshot hits, h) gets the owner's pages, popped for the
+  // owner's blocks [h_o, nb_o) from the same stack (the owner's run ends before any block it owns)
+  if (c.bd_key)
+    for (uint32_t j = c.hit_local[i] + lane; j < h; j += 32) {
+      const uint32_t o = bd_find(c, block_hash[(size_t)i * c.max_blocks + j]);
+      bt[j] = (int32_t)c.free_list[sc->n_free - sc->need_total + c.need_off[o] + (j - hit[o])];
     }
-    atomicMin(&c.bd_owner[s], i);
-  }
 }
 // warp per request: extend hit[i] through blocks an earlier request computes
 __global__ void __launch_bounds__(256) k_bd_resolve(Ctx c, uint32_t B, const uint32_t* __restrict__ prompt_tok,
@@ -369,27 +367,26 @@ __global__ void __launch_bounds__(256) k_bd_resolve(Ctx c, uint32_t B, const uin
     }
   }
 }
-// warp per request, after k_alloc_fill: the shared run's block-table entries = the owner's pages
-__global__ void __launch_bounds__(256) k_bd_fill(Ctx c, uint32_t B, const uint64_t* __restrict__ block_hash,
-                                                 const uint32_t* __restrict__ hit, int32_t* __restrict__ block_table) {
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= B) return;
-  if (c.sc->status == IL_ERR_CAPACITY) return;
-  const uint64_t* bh = block_hash + (size_t)i * c.max_blocks;
-  for (uint32_t j = c.hit_local[i] + lane; j < hit[i]; j += 32) {
-    const uint32_t o = bd_find(c, bh[j]);
-    block_table[(size_t)i * c.max_blocks + j] = block_table[(size_t)o * c.max_blocks + j];
-  }
-}
-
 // (a kernel rather than a memset node: keeps the captured match graph all-kernel)
 __global__ void k_match_begin(Ctx c) {
   DevScalars* sc = c.sc;
   sc->pinned = 0; sc->hit_sum = 0; sc->full_sum = 0; sc->box_hit_sum = 0; sc->inserted = 0; sc->dedup_sum = 0;
 }
-__global__ void k_alloc_commit(Ctx c) {
+__global__ void __launch_bounds__(1024) k_alloc_commit(Ctx c) {
   DevScalars* sc = c.sc;
-  if (sc->status != IL_ERR_CAPACITY) sc->n_free -= sc->need_total;
+  if (c.bd_key) {                                   // the dedup table's lookups are over: clear it
+    const uint32_t n = sc->bd_n;
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const uint32_t s = c.bd_list[x];
+      c.bd_key[s] = 0;
+      c.bd_owner[s] = 0;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (sc->status != IL_ERR_CAPACITY) sc->n_free -= sc->need_total;
+    sc->bd_n = 0;
+  }
 }
 
 }  // namespace il
@@ -415,13 +412,10 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   const uint64_t b_cur = c->batch + 1;
   const bool dedup = (c->cfg.flags & IL_F_DEDUP) && B > 1;
   k_match_begin<<<1, 1, 0, st>>>(*c);
-  if (dedup) k_bd_clear<<<c->num_sms * 4, 256, 0, st>>>(*c);
   k_instr_probe<<<1, 256, 0, st>>>(*c);
-  if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table, b_cur);
-  if (dedup) {
-    k_bd_insert<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, block_hash, hit);
-    k_bd_resolve<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit);
-  }
+  if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table,
+                                                           dedup ? 1u : 0u);
+  if (dedup) k_bd_resolve<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit);
   k_alloc_scan<<<1, 1024, 0, st>>>(*c, B, prompt_len, hit, prefix_len, cu_q, b_cur);
   {
     Ctx cc = *c;
@@ -429,11 +423,10 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
     void* args[] = {&cc, &bc};
     IL_CUDA(cudaLaunchCooperativeKernel((void*)k_evict, dim3(c->ev_blocks), dim3(EV_THREADS), args, 0, st));
   }
-  if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_table);
-  if (dedup) k_bd_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, block_hash, hit, block_table);
-  k_alloc_commit<<<1, 1, 0, st>>>(*c);
+  if (B) k_alloc_fill<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_len, hit, block_hash, block_table);
+  k_alloc_commit<<<1, 1024, 0, st>>>(*c);
   IL_LAUNCH_CHECK("il_prefix_match");
-  c->launches += (B ? 7 : 5) + (dedup ? 4 : 0);
+  c->launches += (B ? 7 : 5) + (dedup ? 1 : 0);
   c->prompt_tok = prompt_tok;
   c->prompt_len = prompt_len;
   c->block_hash = block_hash;
