@@ -4,7 +4,7 @@ k_commit_insert / k_commit_own, cooperative k_rebuild (tombstone compaction), th
 commit (k_tab_key / k_tab_find / k_tab_commit) -- and, with --attn, the attention call; every
 batch is checked bit-exact against the CPU oracle, so a race that changes a result fails too.
 
-    compute-sanitizer --tool {memcheck,racecheck,synccheck} python scripts/sanitize_index.py [--attn]
+    compute-sanitizer --tool {memcheck,racecheck,synccheck} python scripts/sanitize_index.py [--attn] [--dedup]
 """
 import os
 import sys
@@ -31,7 +31,8 @@ def main():
         return main_dp()
     attn = "--attn" in sys.argv
     # 160 KV pages for 8 ~15-page prompts per batch: most batches evict, tombstones force rebuilds
-    sp = StreamSpec(C=160, B=8, T=32, n_logs=1200, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD,
+    dedup = "--dedup" in sys.argv                     # IL_F_DEDUP: the in-batch table and owner pages
+    sp = StreamSpec(C=160, B=8, T=32, n_logs=1200, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD | (O.F_DEDUP if dedup else 0),
                     n_batches=int(os.environ.get("NB", "60")), ramp=(2, 4))
     ds, pool, instr = make_stream(sp)
     o = oracle_for(sp, pool, instr)
@@ -47,7 +48,8 @@ def main():
         compare_state(o, pl, where=f"batch {b}")
         ev += len(r.evicted) > 0
     st = pl.ctx.stats()
-    print(f"sanitize_index: {b + 1} batches bit-exact, {ev} evicting, {st['index_rebuilds']} index rebuilds, attention={attn}")
+    print(f"sanitize_index: {b + 1} batches bit-exact, {ev} evicting, {st['index_rebuilds']} index rebuilds, "
+          f"attention={attn}, dedup={dedup}")
 
 
 if __name__ == "__main__":
