@@ -46,9 +46,12 @@ def peaks():
     return {"hbm": 6650.0, "tc": 1590.0, "tc_sustained": 1400.0, "src": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic():
+def ncu_traffic(args=None):
     """dram read+write bytes per launch of the attention kernel from the committed ncu summary
-    (profiles/attn_ncu_summary.json, written from one `ncu --set full` capture), or None."""
+    (profiles/attn_ncu_summary.json, written from one `ncu --set full` capture of the DEFAULT
+    run: c3, PAIR, fused K/V, no decode), or None for any other workload."""
+    if args is not None and (args.config != 3 or args.naive or args.no_fused_kv or args.decode):
+        return None, "no ncu capture of this workload (profiles/attn_ncu_summary.json is the default c3 run's)"
     p = os.path.join(ROOT, "profiles", "attn_ncu_summary.json")
     if os.path.exists(p):
         d = json.load(open(p))
@@ -553,8 +556,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"kernel": "il_prefill_attn (attention; the suffix K/V written into the pages by the QKV-"
                                "projection stand-in's epilogue)" if not args.no_fused_kv else
                                "il_prefill_attn (K/V append + attention)", "bound": bound, "achieved": achieved,
-                     "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": ncu_traffic()[0],
-                     "traffic_src": ncu_traffic()[1],
+                     "peak": peak, "unit": unitr, "frac": achieved / peak, "traffic": ncu_traffic(args)[0],
+                     "traffic_src": ncu_traffic(args)[1],
                      "peak_src": pk["src"] + (" burst bf16" if bound == "tensor" else ""),
                      "flops_per_step": float(fl.mean()), "bytes_per_step": float(by.mean()),
                      "t_star_ms": float(np.maximum(t_tc, t_hbm).mean() * 1e3)},
