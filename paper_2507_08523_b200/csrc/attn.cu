@@ -104,6 +104,12 @@ il_status il::attn_setup(Ctx*) {
 }
 
 #ifdef IL_ATTN_TRACE
+extern "C" il_status il_debug_trace_reset() {
+  IL_CUDA(cudaDeviceSynchronize());
+  static unsigned long long zero[16 * 4096];
+  IL_CUDA(cudaMemcpyToSymbol(il::sm100::g_trace, zero, sizeof(zero)));
+  return IL_OK;
+}
 extern "C" il_status il_debug_trace(unsigned long long* out_h) {
   IL_CUDA(cudaDeviceSynchronize());
   IL_CUDA(cudaMemcpyFromSymbol(out_h, il::sm100::g_trace, sizeof(il::sm100::g_trace)));
