@@ -152,6 +152,10 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                "r"(c2)
                : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
@@ -457,6 +461,9 @@ struct LoadSeq {
 #ifndef IL_Q_PREFETCH
 #define IL_Q_PREFETCH 1
 #endif
+#ifndef IL_KV_PREFETCH
+#define IL_KV_PREFETCH 0      // (measured: 1 / 2 / 3 items ahead = 0.966 / 0.994 / 0.999 ms vs 0.886 off)
+#endif
 #ifndef IL_STREAMS
 #define IL_STREAMS 0
 #endif
@@ -549,6 +556,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (uint32_t h = 0; h < NCB; ++h) {
             tma_prefetch_3d(&tm_q, (int)(64 * h), hqn, rown);
             if (phase == 1) tma_prefetch_3d(&tm_o, (int)(64 * h), hqn, rown);   // the next item's partial
+          }
+          // phase 2 (profiling knob, off): the K / V pages of an item IL_KV_PREFETCH items ahead into
+          // L2.  Slower at every distance: the loads are not what the MMA issuer waits for
+          if (IL_KV_PREFETCH && phase == 2) {          // (IL_KV_PREFETCH = items ahead)
+            uint32_t wp = wn;
+            Tile Tp = Tn;
+            for (int a = 1; a < IL_KV_PREFETCH && wp < n_items; ++a) { wp += gridDim.x; seek(wp, Tp); }
+            const int32_t* btn = block_table + (size_t)Tp.i * c.max_blocks;
+            const uint32_t khn = wp % Hkv;
+            if (wp < n_items)
+            for (uint32_t blk = Tp.kv0 * 8; blk < min(Tp.nblk, (Tp.kv0 + Tp.n_kv) * 8); ++blk) {
+              const int row = (int)(((uint32_t)__ldg(btn + blk) * Hkv + khn) * BS);
+#pragma unroll
+              for (uint32_t h = 0; h < NCB; ++h) {
+                tma_prefetch_2d(&tm_k, (int)(64 * h), row);
+                tma_prefetch_2d(&tm_v, (int)(64 * h), row);
+              }
+            }
           }
         }
         ++ix;
