@@ -65,9 +65,17 @@ def ncu_traffic(args=None):
 MAX_FILL = {1: 400, 2: 200, 3: 200, 4: 200, 5: 200}
 
 
+def pipelined_on(args) -> bool:
+    """The cross-batch pipelined schedule (il.h il_set_sm_split comment) is timed unless --serial,
+    --no-graph or --decode."""
+    return not (args.serial or args.no_graph or args.decode)
+
+
 def n_queries_for(cfg, args, world: int) -> int:
-    """Stream length both arms use (the same dataset instance): ramp + fill + warm-up + timed."""
-    n = (MAX_FILL[args.config] + args.warmup + 2 * args.steps + 1) * cfg.B * world + 65 * world
+    """Stream length both arms use (the same dataset instance): ramp + fill + warm-up + timed
+    (2K serial steps, + 2K pipelined ones)."""
+    n_timed = 2 * args.steps * (2 if pipelined_on(args) else 1)
+    n = (MAX_FILL[args.config] + args.warmup + n_timed + 1) * cfg.B * world + 65 * world
     return int(n * 1.25) if getattr(args, "dedup", False) else n      # (the dedup'd stream is shorter)
 
 
@@ -196,7 +204,11 @@ def run_ours(args, rank, world, local_rank):
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                   head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world, max_decode_tokens=args.decode)
     stream = torch.cuda.Stream(dev)
-    pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream, fused_kv=not args.no_fused_kv)
+    piped = pipelined_on(args)
+    # (two per-batch buffer slots for the pipelined schedule: batch b's attention reads slot b % 2
+    # while batch b+1's integer stages write the other)
+    pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream, fused_kv=not args.no_fused_kv,
+                  slots=2 if piped else 1)
     # N > 1: rank r runs the r-th slice of every global batch; the pool is
     # broadcast from rank 0; per batch one record buffer per rank (ICL records + prefix-index
     # updates) is all-gathered (NCCL) on a side stream, overlapping the next batch's selection
@@ -217,8 +229,9 @@ def run_ours(args, rank, world, local_rank):
             pl.commit()
     K, W = args.steps, args.warmup
     n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
-    plan = plan_batches(cfg, n_fill_max + W + 2 * K, rank, world)
-    n_ramp = len(plan) - (n_fill_max + W + 2 * K)
+    n_timed = 2 * K * (2 if piped else 1)
+    plan = plan_batches(cfg, n_fill_max + W + n_timed, rank, world)
+    n_ramp = len(plan) - (n_fill_max + W + n_timed)
 
     dec_tok = torch.zeros(args.decode, cfg.B, dtype=torch.int64, device=dev) if args.decode else None
 
@@ -264,9 +277,12 @@ def run_ours(args, rank, world, local_rank):
     # end (pinned host inputs copied in, refined DS / info / hits copied out inside the timed
     # region), so both see the same part of the stream.
     warm_in = [to_dev(bt) for bt in batches[:W]]
-    timed = batches[W:]
+    timed = batches[W:W + 2 * K]
     dev_in = [to_dev(bt) if j % 2 == 0 else None for j, bt in enumerate(timed)]
     host_in = [to_pinned(bt) if j % 2 == 1 else None for j, bt in enumerate(timed)]
+    # the pipelined schedule's batches: K device-resident, then K from pinned host memory
+    piped_dev = [to_dev(bt) for bt in batches[W + 2 * K:W + 3 * K]] if piped else []
+    piped_host = [to_pinned(bt) for bt in batches[W + 3 * K:W + 4 * K]] if piped else []
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     out_fin = torch.empty(cfg.B, cfg.k, dtype=torch.int32).pin_memory()
@@ -315,19 +331,23 @@ def run_ours(args, rank, world, local_rank):
         l0 = pl.launches()
         pl.B = cfg.B
         graphs = {}
-        for name in stage_names:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                stage_fns[name]()
-            graphs[name] = g
-        per_step_launches = pl.launches() - l0
+        for slot in range(2 if piped else 1):          # one set of stage graphs per buffer slot
+            pl.use(slot)
+            for name in stage_names:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    stage_fns[name]()
+                graphs[slot, name] = g
+            if slot == 0:
+                per_step_launches = pl.launches() - l0
+        pl.use(0)
         stream.synchronize()
 
     def run_stage(name):
         if dp is not None and name == "refine":
             dp.wait_gathered()                         # (eager: an event wait, never captured)
         if graphs is not None:
-            graphs[name].replay()
+            graphs[pl.slot, name].replay()
         else:
             stage_fns[name]()
         if dp is not None and name == "commit":
@@ -385,6 +405,64 @@ def run_ours(args, rank, world, local_rank):
                 e2e_evs.append((e0, e1))
                 h2d = 4 * (qo.numel() + qt.numel() + qs.numel()) + (8 * dt.numel() if dec_tok is not None else 0)
                 d2h = 4 * B * cfg.k + 4 * B + 16 * B
+    torch.cuda.synchronize()
+
+    # ---- the pipelined schedule (il.h, il_set_sm_split comment): batch j's synth + attention on
+    # stream sA overlap batch j's commit and batch j+1's select / refine / match on `stream`; buffer
+    # slot j % 2; batch j+2 reuses slot j % 2 only after batch j's attention.  The L2 flush runs on
+    # sA before every batch's synth.  Device-resident inputs (value), then pinned host inputs with
+    # the integer results copied back (e2e).  Timed from before the first batch to after the last.
+    sA = torch.cuda.Stream(dev)
+    pipe = {}
+
+    def run_pipelined(inputs, host):
+        n = len(inputs)
+        ev_m = [torch.cuda.Event() for _ in range(n)]
+        ev_a = [torch.cuda.Event() for _ in range(n)]
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        sA.wait_stream(stream)
+        for j, x in enumerate(inputs):
+            with torch.cuda.stream(stream):
+                if j >= 2:
+                    stream.wait_event(ev_a[j - 2])     # slot j % 2 is free again
+                pl.use(j % 2)
+                if host:
+                    qo, qt, qs, B = x[:4]
+                    pl.q_off[:B + 1].copy_(qo, non_blocking=True)
+                    pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
+                    pl.q_src[:B].copy_(qs, non_blocking=True)
+                    pl.B = B
+                else:
+                    set_inputs(x)
+                for name in stage_names[:-3]:          # select, refine, match
+                    run_stage(name)
+                ev_m[j].record(stream)
+                if host:
+                    out_fin[:x[3]].copy_(pl.final_ds[:x[3]], non_blocking=True)
+                    out_hit[:x[3]].copy_(pl.hit[:x[3]], non_blocking=True)
+                    out_info[:x[3]].copy_(pl.info[:x[3]], non_blocking=True)
+            with torch.cuda.stream(sA):
+                sA.wait_event(ev_m[j])
+                flush.zero_()
+                for name in ("synth", "attn"):
+                    graphs[j % 2, name].replay()
+                ev_a[j].record(sA)
+            with torch.cuda.stream(stream):
+                run_stage("commit")                    # after match(j) on `stream`, beside the attention
+        stream.wait_stream(sA)
+        e1.record(stream)
+        return e0, e1
+
+    if piped:
+        assert stage_names[-3:] == ["synth", "attn", "commit"], stage_names
+        for key, inputs, host in (("device", piped_dev, False), ("e2e", piped_host, True)):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            pipe[key] = run_pipelined(inputs, host)
+            torch.cuda.synchronize()
+        pl.use(0)
     if dp is not None:
         with torch.cuda.stream(stream):
             dp.flush()                                 # the last batch's records (after the timed region)
@@ -402,7 +480,7 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     launches = pl.launches() - launches0 - 2 * K      # minus the per-step k_stats (accounting, not the path)
     if graphs is not None:                             # replays do not pass through the host counter
-        launches += per_step_launches * 2 * K
+        launches += per_step_launches * (2 * K + (2 * K if piped else 0))
     st_steps = [pl.ctx.stats_from_bytes(r) for r in rec_stats.cpu().numpy()]
     evicted = [s_["evicted_blocks"] for s_ in st_steps]
     # hit accounting of every timed step (device counters), summed over ranks: rank-local hits and
@@ -447,10 +525,17 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- reduce over ranks (max time)
     ms = float(np.mean(step_ms)); e2e = float(np.mean(e2e_ms))
+    pms = pe2e = 0.0
+    if piped:
+        pms = pipe["device"][0].elapsed_time(pipe["device"][1]) / K
+        pe2e = pipe["e2e"][0].elapsed_time(pipe["e2e"][1]) / K
     if world > 1:
-        t = torch.tensor([ms, e2e], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, e2e, pms, pe2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e = float(t[0]), float(t[1])
+        ms, e2e, pms, pe2e = (float(x) for x in t)
+    serial_ms, serial_e2e = ms, e2e
+    if piped:                                          # the headline is the pipelined schedule
+        ms, e2e = pms, pe2e
     if rank != 0:
         return
     pk = peaks()
@@ -563,8 +648,20 @@ def run_ours(args, rank, world, local_rank):
                      "t_star_ms": float(np.maximum(t_tc, t_hbm).mean() * 1e3)},
         "e2e": {"value": B_all / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
+        "schedule": {
+            "kind": "pipelined" if piped else "serial",
+            "note": ("value / e2e: batch b's QKV stand-in + attention (one stream) overlap batch b's commit and batch "
+                     "b+1's select / refine / match (another stream), two per-batch buffer slots, the attention on "
+                     "every SM (il_set_sm_split measured slower: the latency-bound integer stages need the whole "
+                     "GPU); stage_ms, roofline and the per-step accounting come from the serial steps"
+                     if piped else "one batch at a time on one stream"),
+            "serial": {"value": B_all / (serial_ms * 1e-3), "ms_per_step": serial_ms,
+                       "e2e_value": B_all / (serial_e2e * 1e-3), "e2e_ms_per_step": serial_e2e},
+            **({"pipelined": {"value": B_all / (pms * 1e-3), "ms_per_step": pms,
+                              "e2e_value": B_all / (pe2e * 1e-3), "e2e_ms_per_step": pe2e}} if piped else {})},
         "gpu_launches": int(launches),
-        "timed_steps": {"device": K, "e2e": K, "order": "alternating",
+        "timed_steps": {"serial_device": K, "serial_e2e": K, "serial_order": "alternating",
+                        **({"pipelined_device": K, "pipelined_e2e": K} if piped else {}),
                         "launch": "eager" if graphs is None else "per-stage CUDA graphs"},
         "clocks": clk,
         "wall_s_timed": wall,
@@ -740,8 +837,9 @@ def run_reference(args, rank, world):
         flags |= O.F_DEDUP
     K, W = args.steps, args.warmup
     n_fill_max = 0 if args.no_fill else MAX_FILL[args.config]
-    plans = [plan_batches(cfg, n_fill_max + W + 2 * K, r, world) for r in range(world)]
-    n_ramp = len(plans[0]) - (n_fill_max + W + 2 * K)
+    n_timed = 2 * K * (2 if pipelined_on(args) else 1)
+    plans = [plan_batches(cfg, n_fill_max + W + n_timed, r, world) for r in range(world)]
+    n_ramp = len(plans[0]) - (n_fill_max + W + n_timed)
     cores = len(os.sched_getaffinity(0))
     # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; only rank 0 runs the oracle);
     # set before the oracle library and its OpenMP runtime are first loaded
@@ -774,16 +872,22 @@ def run_reference(args, rank, world):
         if j > n_ramp and len(r.evicted) > 0:
             break
     n_fill = j - n_ramp if n_fill_max else 0
-    order = list(range(n_ramp + n_fill_max, n_ramp + n_fill_max + W + 2 * K))
+    order = list(range(n_ramp + n_fill_max, n_ramp + n_fill_max + W + n_timed))
     for jj in order[:W]:
         run(jj)
+    # the GPU arm's headline steps: with the pipelined schedule, the K device-resident batches after
+    # its 2K serial ones (replayed here untimed, integer path only); else its alternating serial steps
+    timed_ix = list(range(2 * K, 3 * K)) if pipelined_on(args) else list(range(0, 2 * K, 2))
+    for step in range(timed_ix[0]):
+        if step not in timed_ix:
+            run(order[W + step])
     t_prep = time.perf_counter() - t_prep
     rng = np.random.default_rng(0)
     steps_ms, per_req = [], []
     n_att_tot = 0
-    for step in range(2 * K):
+    for step in range(timed_ix[0], timed_ix[-1] + 1):
         jj = order[W + step]
-        if step % 2 == 1:                                 # the GPU arm's e2e steps: keep the state in step
+        if step not in timed_ix:                          # the GPU arm's serial e2e steps: keep the state in step
             run(jj)
             continue
         t0 = time.perf_counter()
@@ -834,6 +938,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of per-stage CUDA graphs")
     ap.add_argument("--no-fill", action="store_true", help="time right after the ramp (cache not yet full)")
+    ap.add_argument("--serial", action="store_true",
+                    help="time one batch at a time only (no cross-batch pipelining of attention vs integer stages)")
     ap.add_argument("--decode", type=int, default=0, help="decode tokens per request after the prefill (NEXT-4)")
     ap.add_argument("--no-fused-kv", action="store_true",
                     help="K / V to k_new / v_new and il_prefill_attn's append pass (instead of the projection "

@@ -138,6 +138,20 @@ il_status il_stats_sync(il_ctx* ctx, il_stream s, il_stats* out_h);
  * `launches` holds the host counter at the time of the call (at capture, for a graph). */
 il_status il_stats_async(il_ctx* ctx, il_stats* out_d, il_stream s);
 const char* il_last_error(void);                          /* thread-local */
+/* Cross-batch pipelining (a serving schedule, not a change of what is computed): the attention
+ * of batch b (il_synth_qkv* + il_prefill_attn on one stream) may run CONCURRENTLY with
+ * il_commit of batch b and il_select_batch / il_refine_batch / il_prefix_match of batch b+1 on a
+ * second stream, provided (1) the two batches use different per-batch buffers (prompts, block
+ * tables, cu_q, prefix_len, Q, out, ...), (2) calls that read or write KV page CONTENTS for batch
+ * b+1 (il_synth_qkv_paged, il_prefill_attn) are ordered after batch b's il_prefill_attn, and (3)
+ * il_commit of batch b is ordered after its il_prefix_match.  Pages batch b reads may be freed or
+ * evicted (metadata) by those calls, but only batch b+1's page writes reuse them.  For the two
+ * streams to overlap on the device, il_set_sm_split(ctx, n) gives il_prefill_attn's persistent
+ * grid n CTAs (one per SM) and sizes the cooperative integer kernels (LRU eviction, index
+ * compaction, residency-map compaction) to fit on the remaining SMs; n = 0 restores the default
+ * (attention on every SM).  IL_ERR_ARG if n >= the SM count.  Host-side only; takes effect for
+ * later calls (and captures). */
+il_status il_set_sm_split(il_ctx* ctx, uint32_t attn_ctas);
 
 /* ---- il_pool_load: the candidate set ("samples 200 logs ... to construct the
  * candidate set").  CSR device arrays of n_demos demos: log tokens, template tokens,

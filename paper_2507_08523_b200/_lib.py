@@ -25,7 +25,7 @@ EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "i
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
            "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
            "il_table_dump", "il_evicted_dump", "il_record_bytes", "il_commit_export", "il_commit_apply",
-           "il_box_hit_dump", "il_select_batch", "il_synth_qkv_paged"]
+           "il_box_hit_dump", "il_select_batch", "il_synth_qkv_paged", "il_set_sm_split"]
 
 
 class ILError(RuntimeError):
@@ -98,6 +98,7 @@ def load():
         "il_commit_apply": [P, P, U32, P, P],
         "il_box_hit_dump": [P, P, P, U32],
         "il_select_batch": [P, U32, P, P, P, P, P],
+        "il_set_sm_split": [P, U32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

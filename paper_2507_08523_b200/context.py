@@ -162,6 +162,11 @@ class Context:
         L.check(self.lib.il_stats_sync(self.h, _stream(stream), C.byref(st)), "il_stats_sync")
         return {f: getattr(st, f) for f, _ in L.il_stats._fields_}
 
+    def set_sm_split(self, attn_ctas: int) -> None:
+        """il_set_sm_split: the attention's persistent grid on attn_ctas SMs, the cooperative
+        integer kernels sized for the rest (cross-batch pipelining); 0 = default."""
+        L.check(self.lib.il_set_sm_split(self.h, attn_ctas), "il_set_sm_split")
+
     def stats_async(self, out: torch.Tensor, stream=None):
         """il_stats written by a kernel into `out` (a device tensor of >= 48 bytes; no sync)."""
         L.check(self.lib.il_stats_async(self.h, _p(out), _stream(stream)), "il_stats_async")

@@ -1011,13 +1011,14 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
   k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
+  const int grid = c->attn_ctas ? c->attn_ctas : c->num_sms;   // (il_set_sm_split)
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
     if (phase == 1 && !cascade) break;
     if (D == 128)
-      k_attn_sm100<128><<<c->num_sms, THREADS, smem_bytes(128), st>>>(*c, B, cu_q, prefix_len, block_table,
+      k_attn_sm100<128><<<grid, THREADS, smem_bytes(128), st>>>(*c, B, cu_q, prefix_len, block_table,
           (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     else
-      k_attn_sm100<64><<<c->num_sms, THREADS, smem_bytes(64), st>>>(*c, B, cu_q, prefix_len, block_table,
+      k_attn_sm100<64><<<grid, THREADS, smem_bytes(64), st>>>(*c, B, cu_q, prefix_len, block_table,
           (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");
   }

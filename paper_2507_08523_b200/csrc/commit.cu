@@ -400,7 +400,8 @@ il_status il::commit_setup(Ctx* c) {
   IL_CUDA(cudaFuncSetAttribute(k_tab_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
   int per_sm = 0;
   IL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild, 512, 0));
-  c->rb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+  c->rb_per_sm = std::max(1, std::min(per_sm, 2));
+  c->rb_blocks = c->rb_per_sm * c->num_sms;
   return IL_OK;
 }
 

@@ -379,6 +379,16 @@ static __global__ void k_stats(Ctx c, il_stats* out, uint64_t launches) {
   out->dedup_blocks = h.dedup_sum;
 }
 
+il_status il_set_sm_split(il_ctx* c, uint32_t attn_ctas) {
+  if (attn_ctas >= (uint32_t)c->num_sms) { set_error("il_set_sm_split: attn_ctas >= SM count"); return IL_ERR_ARG; }
+  const int aux = attn_ctas ? c->num_sms - (int)attn_ctas : c->num_sms;
+  c->attn_ctas = (int)attn_ctas;
+  c->ev_blocks = c->ev_per_sm * aux;
+  c->rb_blocks = c->rb_per_sm * aux;
+  c->mb_blocks = c->mb_per_sm * aux;
+  return IL_OK;
+}
+
 il_status il_stats_async(il_ctx* c, il_stats* out, il_stream s) {
   if (!out || ((uintptr_t)out & 7)) { set_error("il_stats_async: null or misaligned output"); return IL_ERR_ARG; }
   k_stats<<<1, 1, 0, (cudaStream_t)s>>>(*c, out, c->launches);

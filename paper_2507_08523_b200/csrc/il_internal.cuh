@@ -151,6 +151,8 @@ struct Ctx {
   int num_sms = 148;
   int ev_blocks = 0, rb_blocks = 0, mb_blocks = 0;   // cooperative grid sizes (k_evict, k_rebuild,
                                                      // k_map_rebuild), set per context
+  int ev_per_sm = 1, rb_per_sm = 1, mb_per_sm = 1;   // their CTAs per SM
+  int attn_ctas = 0;                                 // il_set_sm_split: attention grid (0 = every SM)
   uint64_t launches = 0;     // kernels launched by this context (host counter)
 };
 

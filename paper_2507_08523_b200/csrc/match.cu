@@ -399,7 +399,8 @@ il_status il::match_setup(Ctx* c) {
   IL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_evict, EV_THREADS, 0));
   // one CTA per SM: each of the five passes over the pages is short, the grid syncs dominate
   // (148 CTAs: 25 us per evicting c3 step; 296: 28; 74: 27; 37: 38)
-  c->ev_blocks = std::max(1, std::min(per_sm, 1)) * c->num_sms;
+  c->ev_per_sm = std::max(1, std::min(per_sm, 1));
+  c->ev_blocks = c->ev_per_sm * c->num_sms;
   return IL_OK;
 }
 

@@ -161,7 +161,8 @@ il_status il::records_setup(Ctx* c) {
   if (!c->map_slots) return IL_OK;
   int per_sm = 0;
   IL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_rebuild, 512, 0));
-  c->mb_blocks = std::max(1, std::min(per_sm, 2)) * c->num_sms;
+  c->mb_per_sm = std::max(1, std::min(per_sm, 2));
+  c->mb_blocks = c->mb_per_sm * c->num_sms;
   return IL_OK;
 }
 

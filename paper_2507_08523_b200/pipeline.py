@@ -22,7 +22,7 @@ def _dev_u32(a, device) -> torch.Tensor:
 class Pipeline:
     def __init__(self, cfg: Config, device="cuda", qkv_seed: int = 3000, q_scale: float = 1.0,
                  max_query_tokens: int | None = None, stream: torch.cuda.Stream | None = None,
-                 fused_kv: bool = False):
+                 fused_kv: bool = False, slots: int = 1):
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream
@@ -33,32 +33,55 @@ class Pipeline:
         self.fused_kv = fused_kv
         B, S, MB, k = cfg.max_batch, cfg.max_prompt_tokens, cfg.max_blocks, cfg.k
         dev, i32 = self.device, torch.int32
-        self.topk = torch.zeros(B, k, dtype=i32, device=dev)
-        self.final_ds = torch.zeros(B, k, dtype=i32, device=dev)
-        self.info = torch.zeros(B, 16, dtype=torch.uint8, device=dev)
-        self.prompt_tok = torch.zeros(B, S, dtype=i32, device=dev)
-        self.prompt_len = torch.zeros(B, dtype=i32, device=dev)
-        self.block_hash = torch.zeros(B, MB, dtype=torch.int64, device=dev)
-        self.hit = torch.zeros(B, dtype=i32, device=dev)
-        self.block_table = torch.zeros(B, MB, dtype=i32, device=dev)
-        self.prefix_len = torch.zeros(B, dtype=i32, device=dev)
-        self.cu_q = torch.zeros(B + 1, dtype=i32, device=dev)
         rows = cfg.max_suffix_tokens or B * S
         Hq, Hkv, d = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
         bf = torch.bfloat16
-        self.q = torch.empty(rows, Hq, d, dtype=bf, device=dev)
-        self.k_new = torch.empty(rows, Hkv, d, dtype=bf, device=dev)
-        self.v_new = torch.empty(rows, Hkv, d, dtype=bf, device=dev)
-        self.out = torch.empty(rows, Hq, d, dtype=bf, device=dev)
-        self.lse = torch.empty(rows, Hq, dtype=torch.float32, device=dev)
+        mq = max_query_tokens or B * cfg.max_log_tokens
+        self._rows = rows
+        # per-batch buffers; `slots` > 1 gives every slot its own set, so that the attention of one
+        # batch can run while the integer stages of the next use the other slot (il.h: cross-batch
+        # pipelining; `use(slot)` selects the set the calls below read and write)
+        self._slots = []
+        for _ in range(slots):
+            self._slots.append(dict(
+                topk=torch.zeros(B, k, dtype=i32, device=dev),
+                final_ds=torch.zeros(B, k, dtype=i32, device=dev),
+                info=torch.zeros(B, 16, dtype=torch.uint8, device=dev),
+                prompt_tok=torch.zeros(B, S, dtype=i32, device=dev),
+                prompt_len=torch.zeros(B, dtype=i32, device=dev),
+                block_hash=torch.zeros(B, MB, dtype=torch.int64, device=dev),
+                hit=torch.zeros(B, dtype=i32, device=dev),
+                block_table=torch.zeros(B, MB, dtype=i32, device=dev),
+                prefix_len=torch.zeros(B, dtype=i32, device=dev),
+                cu_q=torch.zeros(B + 1, dtype=i32, device=dev),
+                q=torch.empty(rows, Hq, d, dtype=bf, device=dev),
+                # (the append path's K / V buffers only when the projection does not write the pages)
+                k_new=None if fused_kv else torch.empty(rows, Hkv, d, dtype=bf, device=dev),
+                v_new=None if fused_kv else torch.empty(rows, Hkv, d, dtype=bf, device=dev),
+                out=torch.empty(rows, Hq, d, dtype=bf, device=dev),
+                lse=torch.empty(rows, Hq, dtype=torch.float32, device=dev),
+                q_off=torch.zeros(B + 1, dtype=i32, device=dev),
+                q_tok=torch.zeros(mq, dtype=i32, device=dev),
+                q_src=torch.zeros(B, dtype=i32, device=dev)))
+        self.use(0)
         self.k_pages = torch.zeros(cfg.kv_pages, Hkv, 16, d, dtype=bf, device=dev)
         self.v_pages = torch.zeros(cfg.kv_pages, Hkv, 16, d, dtype=bf, device=dev)
-        mq = max_query_tokens or B * cfg.max_log_tokens
-        self.q_off = torch.zeros(B + 1, dtype=i32, device=dev)
-        self.q_tok = torch.zeros(mq, dtype=i32, device=dev)
-        self.q_src = torch.zeros(B, dtype=i32, device=dev)
         self.scale = d ** -0.5
         self.B = 0
+
+    def use(self, slot: int) -> None:
+        """Select the per-batch buffer set the following calls use."""
+        for name, t in self._slots[slot].items():
+            setattr(self, name, t)
+        self.slot = slot
+
+    def _append_buffers(self) -> None:
+        if self.k_new is None:                          # (fused_kv switched off after construction)
+            cfg, sl = self.cfg, self._slots[self.slot]
+            for name in ("k_new", "v_new"):
+                sl[name] = torch.empty(self._rows, cfg.n_kv_heads, cfg.head_dim, dtype=torch.bfloat16,
+                                       device=self.device)
+            self.use(self.slot)
 
     # -------------------------------------------------------------- inputs
     def load_pool(self, pool, instr) -> None:
@@ -100,11 +123,14 @@ class Pipeline:
             self.ctx.synth_qkv_paged(B, self.prompt_tok, self.cu_q, self.prefix_len, self.block_table, self.qkv_seed,
                                      self.q_scale, self.q, self.k_pages, self.v_pages, stream=self.stream)
             return
+        self._append_buffers()
         self.ctx.synth_qkv(B, self.prompt_tok, self.cu_q, self.prefix_len, self.qkv_seed, self.q_scale,
                            self.q, self.k_new, self.v_new, stream=self.stream)
 
     def attn(self, B=None, lse: bool = True) -> None:
         B = self.B if B is None else B
+        if not self.fused_kv:
+            self._append_buffers()
         kn, vn = (None, None) if self.fused_kv else (self.k_new, self.v_new)
         self.ctx.prefill_attn(B, self.cu_q, self.prefix_len, self.block_table, self.q, kn, vn,
                               self.k_pages, self.v_pages, self.out, self.lse if lse else None, self.scale,

@@ -51,14 +51,19 @@ def make_stream(sp: StreamSpec):
     return ds, pool, instr
 
 
+def gpu_config(sp: StreamSpec, pool, max_suffix_tokens: int = 0):
+    from paper_2507_08523_b200 import Config
+    return Config(k=sp.k, table_capacity=sp.T, kv_pages=sp.C, max_batch=sp.B,
+                  max_prompt_tokens=sp.max_prompt_tokens, max_pool=sp.M,
+                  max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16,
+                  max_log_tokens=255, max_suffix_tokens=max_suffix_tokens,
+                  n_q_heads=sp.Hq, n_kv_heads=sp.Hkv, head_dim=sp.d,
+                  metric=sp.metric, flags=sp.flags, hash_seed=sp.hash_seed)
+
+
 def gpu_pipeline(sp: StreamSpec, pool, instr, max_suffix_tokens: int = 0):
-    from paper_2507_08523_b200 import Config, Pipeline
-    cfg = Config(k=sp.k, table_capacity=sp.T, kv_pages=sp.C, max_batch=sp.B,
-                 max_prompt_tokens=sp.max_prompt_tokens, max_pool=sp.M,
-                 max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16,
-                 max_log_tokens=255, max_suffix_tokens=max_suffix_tokens,
-                 n_q_heads=sp.Hq, n_kv_heads=sp.Hkv, head_dim=sp.d,
-                 metric=sp.metric, flags=sp.flags, hash_seed=sp.hash_seed)
+    from paper_2507_08523_b200 import Pipeline
+    cfg = gpu_config(sp, pool, max_suffix_tokens)
     pl = Pipeline(cfg, "cuda")
     pl.load_pool(pool, instr)
     return pl

@@ -93,6 +93,9 @@ def _zipf_probs(n: int, s: float) -> np.ndarray:
     return w / w.sum()
 
 
+LOG_CHUNK = 4096
+
+
 def make_dataset(name: str, n_logs: int, n_templates: int, zipf_s: float, seed: int,
                  vocab: int = 2000, len_range=(4, 20), p_const: float = 0.75,
                  value_pool_range=(1, 1000), value_base: int = VALUE_BASE,
@@ -124,9 +127,22 @@ def make_dataset(name: str, n_logs: int, n_templates: int, zipf_s: float, seed: 
         templates.append(tpl)
         slot_pools.append(pools)
     pop = _zipf_probs(n_templates, zipf_s)
-    log_tpl = rng.choice(n_templates, size=n_logs, p=pop).astype(np.uint32)
-    log_off, log_tok = _assemble_logs(rng, templates, slot_pools, log_tpl)
-    return Dataset(name, templates, log_off, log_tok, log_tpl)
+    # Logs come in chunks of doubling size (4,096, 4,096, 8,192, 16,384, ...), each drawn whole from
+    # its own generator (seed, chunk): the first m logs are the same for every n_logs >= m, so a
+    # longer run (more bench steps) replays the same stream prefix.
+    offs, toks, tpls, base, c0, k = [], [], [], 0, 0, 0
+    while c0 < n_logs:
+        size = LOG_CHUNK if k == 0 else LOG_CHUNK << (k - 1)
+        crng = np.random.default_rng([seed, k])
+        lt = crng.choice(n_templates, size=size, p=pop).astype(np.uint32)
+        lo, lk = _assemble_logs(crng, templates, slot_pools, lt)
+        m = min(size, n_logs - c0)
+        offs.append(lo[:m].astype(np.int64) + base)
+        toks.append(lk[:int(lo[m])])
+        tpls.append(lt[:m])
+        base += int(lo[m]); c0 += size; k += 1
+    log_off = np.concatenate(offs + [np.array([base], np.int64)]).astype(np.uint32)
+    return Dataset(name, templates, log_off, np.concatenate(toks), np.concatenate(tpls))
 
 
 def _ragged_arange(lens: np.ndarray) -> np.ndarray:
