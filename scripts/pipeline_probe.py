@@ -71,7 +71,7 @@ def main():
         torch.cuda.synchronize()
     capture()
 
-    def serial(n):
+    def serial(n, fl=True):
         nonlocal pos
         ins = [dev_in(pos + j) for j in range(n)]
         pos += n
@@ -81,7 +81,8 @@ def main():
         e0.record(sB)
         with torch.cuda.stream(sB):
             for x in ins:
-                flush.zero_()
+                if fl:
+                    flush.zero_()
                 pl.load_inputs(*x)
                 for name in ("select", "refine", "match"):
                     graphs[0, name].replay()
@@ -94,7 +95,7 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / n
 
-    def pipelined(n):
+    def pipelined(n, fl="A"):
         nonlocal pos
         ins = [dev_in(pos + j) for j in range(n)]
         pos += n
@@ -110,6 +111,8 @@ def main():
                 if j >= 2:
                     sB.wait_event(ev_a[j - 2])            # slot s: batch j-2's attention is done
                 pl.use(s)
+                if fl == "B":
+                    flush.zero_()
                 pl.load_inputs(*x)
                 for name in ("select", "refine", "match"):
                     graphs[s, name].replay()
@@ -117,7 +120,8 @@ def main():
                 graphs[s, "commit"].replay()
             with torch.cuda.stream(sA):
                 sA.wait_event(ev_m[j])
-                flush.zero_()
+                if fl == "A":
+                    flush.zero_()
                 graphs[s, "synth"].replay(); graphs[s, "attn"].replay()
                 ev_a[j].record(sA)
         sB.wait_stream(sA)
@@ -128,6 +132,11 @@ def main():
     for _ in range(2):
         serial(W)
     print(f"serial: {serial(K):.4f} ms/step", flush=True)
+    for fl in ("A", "B", "none"):
+        pipelined(W, fl)
+        t = pipelined(K, fl)
+        print(f"pipelined, flush on {fl}: {t:.4f} ms/step", flush=True)
+    print(f"serial without flush: {serial(K, False):.4f} ms/step", flush=True)
     for R in splits:
         pl.ctx.set_sm_split(148 - R if R else 0)
         capture()

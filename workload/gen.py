@@ -198,9 +198,10 @@ def _assemble_logs(rng, templates, slot_pools, log_tpl):
     return log_off.astype(np.uint32), log_tok
 
 
-def sample_pool(ds: Dataset, M: int, seed: int) -> Pool:
+def sample_pool(ds: Dataset, M: int, seed: int, n_rows: int | None = None) -> Pool:
+    """M distinct logs of the first n_rows (default: all) rows, seeded."""
     rng = np.random.default_rng(seed)
-    rows = np.sort(rng.choice(ds.n, size=M, replace=False)).astype(np.uint32)
+    rows = np.sort(rng.choice(min(n_rows or ds.n, ds.n), size=M, replace=False)).astype(np.uint32)
     log_lens = np.array([ds.log_off[r + 1] - ds.log_off[r] for r in rows], dtype=np.int64)
     tpls = [ds.templates[ds.log_tpl[r]] for r in rows]
     log_off = np.zeros(M + 1, dtype=np.int64); np.cumsum(log_lens, out=log_off[1:])
