@@ -223,6 +223,25 @@ il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const in
                           il_bf16* k_pages, il_bf16* v_pages, il_bf16* out, float* lse,
                           float softmax_scale, il_stream s);
 
+/* ---- il_decode_attn: paged decode attention (decode is the part of request
+ * latency that is not prefill): ONE query row per request at absolute position pos[i]
+ * (attending keys 0..pos[i], the prompt and the decode tokens before it), after il_prefix_match
+ * reserved the pages for position pos[i] (il_config.max_decode_tokens).  Same page layout and
+ * numerics as il_prefill_attn.
+ *   pos          [B] int32   position of request i's row (= its prefix length)
+ *   block_table  [B][max_blocks] as from il_prefix_match
+ *   q            [B][Hq][d] bf16;  k_new, v_new [B][Hkv][d] bf16, appended at pos[i], or both NULL
+ *                (the projection already wrote them into the pages)
+ *   out          [B][Hq][d] bf16;  lse [B][Hq] fp32 natural-log LSE, or NULL
+ * The keys below the batch-shared prefix run on the tensor kernel's dense phase (rows of all
+ * requests stacked), each request's own keys on a CUDA-core kernel (one warp per request and kv
+ * head: a one-row M-tile would be 97% padding).  IL_ERR_STATE before il_prefix_match; IL_ERR_ARG
+ * for B > max_batch or one of k_new / v_new NULL. */
+il_status il_decode_attn(il_ctx* ctx, uint32_t B, const int32_t* pos, const int32_t* block_table,
+                         const il_bf16* q, const il_bf16* k_new, const il_bf16* v_new,
+                         il_bf16* k_pages, il_bf16* v_pages, il_bf16* out, float* lse,
+                         float softmax_scale, il_stream s);
+
 /* ---- il_commit: end of batch ("update the elements in the ICL Table after processing
  * the request").  Inserts the batch's new full blocks into the prefix index (first request in
  * admission order owns the page; duplicates and partial-block pages are freed, Z22-Z23) and

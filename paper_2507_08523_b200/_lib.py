@@ -25,7 +25,8 @@ EXPORTS = ["il_workspace_bytes", "il_create", "il_destroy", "il_status_sync", "i
            "il_last_error", "il_pool_load", "il_refine_batch", "il_prefix_match", "il_prefill_attn",
            "il_commit", "il_commit_index", "il_commit_records", "il_synth_qkv", "il_index_dump",
            "il_table_dump", "il_evicted_dump", "il_record_bytes", "il_commit_export", "il_commit_apply",
-           "il_box_hit_dump", "il_select_batch", "il_synth_qkv_paged", "il_set_sm_split"]
+           "il_box_hit_dump", "il_select_batch", "il_synth_qkv_paged", "il_set_sm_split",
+           "il_decode_attn"]
 
 
 class ILError(RuntimeError):
@@ -85,6 +86,7 @@ def load():
         "il_refine_batch": [P, U32, P, P, P, P, P, P, P, P, P],
         "il_prefix_match": [P, U32, P, P, P, P, P, P, P, P],
         "il_prefill_attn": [P, U32, P, P, P, P, P, P, P, P, P, P, F32, P],
+        "il_decode_attn": [P, U32, P, P, P, P, P, P, P, P, P, F32, P],
         "il_commit": [P, P],
         "il_commit_index": [P, P],
         "il_commit_records": [P, U32, P, P, P],

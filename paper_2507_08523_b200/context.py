@@ -115,6 +115,11 @@ class Context:
                                          _p(k_new), _p(v_new), _p(k_pages), _p(v_pages), _p(out), _p(lse),
                                          float(scale), _stream(stream)), "il_prefill_attn")
 
+    def decode_attn(self, B, pos, block_table, q, k_new, v_new, k_pages, v_pages, out, lse, scale, stream=None):
+        L.check(self.lib.il_decode_attn(self.h, B, _p(pos), _p(block_table), _p(q), _p(k_new), _p(v_new),
+                                        _p(k_pages), _p(v_pages), _p(out), _p(lse), float(scale), _stream(stream)),
+                "il_decode_attn")
+
     def commit(self, stream=None):
         L.check(self.lib.il_commit(self.h, _stream(stream)), "il_commit")
 

@@ -73,6 +73,7 @@ __device__ __forceinline__ uint32_t tile_owner(const uint32_t* __restrict__ tile
 
 }  // namespace il
 
+#include "decode_dev.cuh"
 #include "attn_sm100.cuh"
 
 using namespace il;
@@ -92,6 +93,24 @@ extern "C" il_status il_prefill_attn(il_ctx* c, uint32_t B, const int32_t* cu_q,
     c->launches += 1;
   }
   return attn_sm100_launch(c, B, cu_q, prefix_len, block_table, q, k_pages, v_pages, out, lse, scale, st);
+}
+
+extern "C" il_status il_decode_attn(il_ctx* c, uint32_t B, const int32_t* pos, const int32_t* block_table,
+                                    const il_bf16* q, const il_bf16* k_new, const il_bf16* v_new, il_bf16* k_pages,
+                                    il_bf16* v_pages, il_bf16* out, float* lse, float scale, il_stream s) {
+  if (!c->matched) { set_error("il_decode_attn before il_prefix_match"); return IL_ERR_STATE; }
+  if (B > c->cfg.max_batch) { set_error("B > max_batch"); return IL_ERR_ARG; }
+  if (B == 0) return IL_OK;
+  cudaStream_t st = (cudaStream_t)s;
+  const int32_t* cu = reinterpret_cast<const int32_t*>(c->dec_cu);    // 0, 1, .., max_batch
+  if (k_new || v_new) {
+    if (!k_new || !v_new) { set_error("k_new and v_new: both or neither"); return IL_ERR_ARG; }
+    k_kv_append<<<c->num_sms * 8, 256, 0, st>>>(*c, B, cu, pos, block_table, (const uint4*)k_new,
+                                                (const uint4*)v_new, (uint4*)k_pages, (uint4*)v_pages);
+    IL_LAUNCH_CHECK("k_kv_append");
+    c->launches += 1;
+  }
+  return attn_sm100_launch(c, B, cu, pos, block_table, q, k_pages, v_pages, out, lse, scale, st, true);
 }
 
 // one-time per-context setup of the attention kernels (il_create, current device)

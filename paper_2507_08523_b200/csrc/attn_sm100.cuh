@@ -978,16 +978,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// decode: one row per request (cu_q = 0, 1, .., B; il_decode_attn): each request's own keys run on
+// CUDA cores (k_decode_own, decode_dev.cuh) instead of tensor phase 2; phase 1 is unchanged.
 static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
                                           const int32_t* block_table, const il_bf16* q, il_bf16* k_pages,
-                                          il_bf16* v_pages, il_bf16* out, float* lse, float scale, cudaStream_t st) {
+                                          il_bf16* v_pages, il_bf16* out, float* lse, float scale, cudaStream_t st,
+                                          bool decode = false) {
   using namespace sm100;
   const uint32_t Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads, g = Hq / Hkv, TQ = BM / g, D = c->cfg.head_dim;
   auto enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return IL_ERR_CUDA; }
   CUtensorMap tq, to, tk, tv;
   for (int which = 0; which < 2; ++which) {            // Q, and `out` (same geometry: L2 prefetch only)
-    cuuint64_t dims[3] = {D, Hq, c->cfg.max_suffix_tokens};
+    cuuint64_t dims[3] = {D, Hq, decode ? (cuuint64_t)B : (cuuint64_t)c->cfg.max_suffix_tokens};
     cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)Hq * D * 2};
     cuuint32_t box[3] = {64, g, TQ};
     cuuint32_t es[3] = {1, 1, 1};
@@ -1010,9 +1013,26 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   const bool cascade = !(ce && ce[0] == '0');
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
-  k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
+  if (!decode) k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
   const int grid = c->attn_ctas ? c->attn_ctas : c->num_sms;   // (il_set_sm_split)
+  if (decode) {
+    const uint32_t G2 = g <= 1 ? 1 : g <= 2 ? 2 : g <= 4 ? 4 : 8;
+    const dim3 dg(B * Hkv), db(DEC_WARPS * 32);
+    const float sl2 = scale * 1.4426950408889634f;
+    const __nv_bfloat16 *qq = (const __nv_bfloat16*)q, *kp = (const __nv_bfloat16*)k_pages,
+                        *vp = (const __nv_bfloat16*)v_pages;
+    __nv_bfloat16* oo = (__nv_bfloat16*)out;
+#define IL_DEC(DD, GG) k_decode_own<DD, GG><<<dg, db, 0, st>>>(*c, B, prefix_len, block_table, qq, kp, vp, oo, lse, sl2)
+    if (D == 128) {
+      if (G2 == 1) IL_DEC(128, 1); else if (G2 == 2) IL_DEC(128, 2); else if (G2 == 4) IL_DEC(128, 4); else IL_DEC(128, 8);
+    } else {
+      if (G2 == 1) IL_DEC(64, 1); else if (G2 == 2) IL_DEC(64, 2); else if (G2 == 4) IL_DEC(64, 4); else IL_DEC(64, 8);
+    }
+#undef IL_DEC
+    IL_LAUNCH_CHECK("k_decode_own");
+  }
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
+    if (phase == 2 && decode) continue;
     if (phase == 1 && !cascade) break;
     if (D == 128)
       k_attn_sm100<128><<<grid, THREADS, smem_bytes(128), st>>>(*c, B, cu_q, prefix_len, block_table,
@@ -1022,7 +1042,7 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
           (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");
   }
-  c->launches += cascade ? (B > 1 ? 5 : 4) : 3;
+  c->launches += cascade ? (B > 1 ? 5 : 4) : 3;         // (decode: k_decode_own instead of k_pair_scan)
   return IL_OK;
 }
 

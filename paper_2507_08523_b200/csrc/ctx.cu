@@ -77,6 +77,7 @@ static size_t carve(Ctx* c, void* ws) {
   c->attn_ml = w.take<float>((size_t)g.max_suffix_tokens * g.n_q_heads);
   c->evicted_list = w.take<uint64_t>(C);
   c->hit_local = w.take<uint32_t>(B);
+  c->dec_cu = w.take<uint32_t>(B + 1);
   if (g.flags & IL_F_DEDUP) {                          // every full block of the batch, half full
     uint32_t n = 1024;
     while (n < 2ull * B * MB) n <<= 1;
@@ -166,6 +167,7 @@ __global__ void k_reset_index(Ctx c) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.dd_mask; t += stride) { c.dd_key[t] = 0; c.dd_max[t] = 0; }
   if (c.bd_key)
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.bd_mask; t += stride) { c.bd_key[t] = 0; c.bd_owner[t] = 0; }
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= c.cfg.max_batch; t += stride) c.dec_cu[t] = t;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevScalars z;
     memset(&z, 0, sizeof(z));

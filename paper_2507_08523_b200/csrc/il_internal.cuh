@@ -129,6 +129,7 @@ struct Ctx {
   uint32_t *box_hit;         // per request: box-level hit count of the last prefix match
   // in-batch dedup (IL_F_DEDUP, match.cu): snapshot hits before dedup, and the batch's table
   // hash -> lowest admission index presenting it as a block it computes
+  uint32_t *dec_cu;          // 0, 1, .., max_batch (il_decode_attn's row offsets)
   uint32_t *hit_local;
   uint64_t *bd_key;          // 0 = empty (chain hashes are never 0, Z18)
   uint32_t *bd_owner;        // ~(lowest admission index); 0 = none

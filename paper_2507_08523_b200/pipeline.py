@@ -174,7 +174,7 @@ class Pipeline:
     def decode_step(self, t: int, tokens: torch.Tensor, B=None, lse: bool = True) -> None:
         """Decode token t of every request (after il_prefill_attn, before il_commit; needs
         Config.max_decode_tokens > t): tokens[i] is written at position L_i + t of the prompt
-        row, its Q / K / V come from il_synth_qkv (the QKV-projection stand-in) and il_prefill_attn
+        row, its Q / K / V come from il_synth_qkv (the QKV-projection stand-in) and il_decode_attn
         runs ONE row per request at position L_i + t: its K / V go into the reserved decode page,
         attention covers the prompt and the t decode tokens before it.  Output: dec_out[:B]."""
         B = self.B if B is None else B
@@ -196,9 +196,9 @@ class Pipeline:
             self.prompt_tok.view(-1)[torch.arange(B, device=dev) * self.prompt_tok.shape[1] + pos] = tokens[:B].to(torch.int32)
         self.ctx.synth_qkv(B, self.prompt_tok, self.dec_cu, self.dec_pos, self.qkv_seed, self.q_scale,
                            self.dec_q, self.dec_k, self.dec_v, stream=self.stream)
-        self.ctx.prefill_attn(B, self.dec_cu, self.dec_pos, self.block_table, self.dec_q, self.dec_k, self.dec_v,
-                              self.k_pages, self.v_pages, self.dec_out, self.dec_lse if lse else None, self.scale,
-                              stream=self.stream)
+        self.ctx.decode_attn(B, self.dec_pos, self.block_table, self.dec_q, self.dec_k, self.dec_v,
+                             self.k_pages, self.v_pages, self.dec_out, self.dec_lse if lse else None, self.scale,
+                             stream=self.stream)
 
     def launches(self) -> int:
         """Kernels this context has launched so far (host-side counter in the library)."""

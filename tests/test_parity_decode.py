@@ -26,8 +26,15 @@ def _pipeline(sp, pool, instr, D):
     return pl
 
 
-@pytest.mark.parametrize("Hq,Hkv,d,D", [(4, 4, 64, 6), (32, 8, 128, 20)])
-def test_decode_steps_after_cached_prefill(Hq, Hkv, d, D):
+@pytest.mark.parametrize("Hq,Hkv,d,D,cascade", [(4, 4, 64, 6, True), (32, 8, 128, 20, True),
+                                                (12, 4, 128, 5, True), (64, 8, 128, 4, True),
+                                                (16, 8, 64, 5, False), (32, 8, 128, 4, False)])
+def test_decode_steps_after_cached_prefill(Hq, Hkv, d, D, cascade, monkeypatch):
+    # il_decode_attn: the shared prefix on the tensor kernel's dense phase, each request's own keys
+    # on the CUDA-core kernel (g = 1, 2, 3 (padded to 4), 4, 8); without the cascade the CUDA-core
+    # kernel covers every key and writes the final rows and LSE
+    if not cascade:
+        monkeypatch.setenv("IL_CASCADE", "0")
     sp = StreamSpec(B=24, C=200, n_logs=2000, Hq=Hq, Hkv=Hkv, d=d,
                     flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4,), n_batches=8)
     ds, pool, instr = make_stream(sp)
@@ -50,6 +57,7 @@ def test_decode_steps_after_cached_prefill(Hq, Hkv, d, D):
             pl.decode_step(t, torch.from_numpy(dec[:, t].astype(np.int64)).to("cuda"))
             pl.ctx.status_sync()
             got = pl.dec_out[:B].float().cpu().numpy().astype(np.float64)
+            glse = pl.dec_lse[:B].cpu().numpy().astype(np.float64)
             for i in range(B):
                 L = int(r.prompt_len[i])
                 toks = np.concatenate([r.prompt(i), dec[i, :t + 1]]).astype(np.uint32)
@@ -57,9 +65,11 @@ def test_decode_steps_after_cached_prefill(Hq, Hkv, d, D):
                 q = gen.bf16_bits_to_f64(gen.synth_bf16_bits(pl.qkv_seed, "q", toks[-1:], pos[-1:], Hq, d))
                 k = gen.bf16_bits_to_f64(gen.synth_bf16_bits(pl.qkv_seed, "k", toks, pos, Hkv, d))
                 v = gen.bf16_bits_to_f64(gen.synth_bf16_bits(pl.qkv_seed, "v", toks, pos, Hkv, d))
-                ref = O.attention_np(q, k, v, P=L + t, scale=d ** -0.5)[0]
+                ref, rl = O.attention(q, k, v, P=L + t, scale=d ** -0.5, want_lse=True)
+                ref, rl = ref[0], rl[0]
                 err = np.abs(got[i] - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
                 assert err.max() <= 1e-2, (b, t, i, float(err.max()))
+                assert np.abs(glse[i] - rl).max() <= 1e-3 * max(1.0, np.abs(rl).max()), (b, t, i)
                 worst = max(worst, float(err.max()))
         pl.commit()
         pl.ctx.status_sync()
