@@ -22,6 +22,9 @@ namespace il {
 // shared prefix (NC > 0) the phase-2 partial (out = O / l, attn_ml = m + log2 l) that phase 1
 // merges; without, the final row and its natural-log LSE.
 constexpr uint32_t DEC_WARPS = 4;
+#ifndef DEC_KEYS_IN_FLIGHT
+#define DEC_KEYS_IN_FLIGHT 8      // (16: 5.94 ms per 16 c3 decode steps vs 5.11: registers cost more occupancy than the loads gain)
+#endif
 
 __device__ __forceinline__ void bf16x4(const uint2 u, float* f) {
   f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
@@ -71,23 +74,35 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode_own(Ctx c, uint32_t B
   const uint32_t my_h = lane % G2;
   float m = -INFINITY, l = 0.f;                          // running max / sum of head my_h (replicated)
   const size_t head_off = (size_t)kh * BS * D + lane * DPL;
-  for (int32_t kb = k0 + (int32_t)(warp * KC); kb <= p; kb += (int32_t)(DEC_WARPS * KC)) {
-    // the chunk's K and V rows (this lane's dims), all loads in flight together
-    uint32_t kraw[KC][DPL / 2], vraw[KC][DPL / 2];
+  // NSUB chunks per iteration: their K and V rows (this lane's dims) are all loaded first, so
+  // 2 x NSUB x KC loads per lane are in flight together (the kernel is bound by HBM latency x
+  // bytes in flight), then the chunks are processed one by one
+  constexpr uint32_t NSUB = KC >= DEC_KEYS_IN_FLIGHT ? 1 : DEC_KEYS_IN_FLIGHT / KC;
+  for (int32_t kb0 = k0 + (int32_t)(warp * NSUB * KC); kb0 <= p; kb0 += (int32_t)(DEC_WARPS * NSUB * KC)) {
+    uint32_t kraw_all[NSUB][KC][DPL / 2], vraw_all[NSUB][KC][DPL / 2];
+#pragma unroll
+    for (uint32_t sub = 0; sub < NSUB; ++sub)
 #pragma unroll
     for (uint32_t kk = 0; kk < KC; ++kk) {
-      const int32_t key = min(kb + (int32_t)kk, p);      // (past p: a duplicate load, masked below)
+      const int32_t key = min(kb0 + (int32_t)(sub * KC + kk), p);   // (past p: a duplicate load, masked)
       const uint32_t page = (uint32_t)__ldg(bt + key / BS);
       const size_t off = (size_t)page * Hkv * BS * D + head_off + (size_t)(key % BS) * D;
       if (DPL == 4) {
         const uint2 a = __ldg(reinterpret_cast<const uint2*>(k_pages + off));
         const uint2 b = __ldg(reinterpret_cast<const uint2*>(v_pages + off));
-        kraw[kk][0] = a.x; kraw[kk][DPL / 2 - 1] = a.y; vraw[kk][0] = b.x; vraw[kk][DPL / 2 - 1] = b.y;
+        kraw_all[sub][kk][0] = a.x; kraw_all[sub][kk][DPL / 2 - 1] = a.y;
+        vraw_all[sub][kk][0] = b.x; vraw_all[sub][kk][DPL / 2 - 1] = b.y;
       } else {
-        kraw[kk][0] = __ldg(reinterpret_cast<const uint32_t*>(k_pages + off));
-        vraw[kk][0] = __ldg(reinterpret_cast<const uint32_t*>(v_pages + off));
+        kraw_all[sub][kk][0] = __ldg(reinterpret_cast<const uint32_t*>(k_pages + off));
+        vraw_all[sub][kk][0] = __ldg(reinterpret_cast<const uint32_t*>(v_pages + off));
       }
     }
+#pragma unroll
+    for (uint32_t sub = 0; sub < NSUB; ++sub) {
+    const int32_t kb = kb0 + (int32_t)(sub * KC);
+    if (kb > p) break;
+    const auto& kraw = kraw_all[sub];
+    const auto& vraw = vraw_all[sub];
     // partial dots: vals[kk * G2 + h] over this lane's dims
     float vals[32];
 #pragma unroll
@@ -145,6 +160,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode_own(Ctx c, uint32_t B
 #pragma unroll
         for (uint32_t e = 0; e < DPL; ++e) acc[h][e] = fmaf(ph, vf[e], acc[h][e]);
       }
+    }
     }
   }
   // merge the warps' states: M = max_w m_w, L = sum_w l_w 2^(m_w - M), O = sum_w O_w 2^(m_w - M)
