@@ -209,6 +209,9 @@ def run_ours(args, rank, world, local_rank):
                   head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world, max_decode_tokens=args.decode)
     stream = torch.cuda.Stream(dev)
     piped = pipelined_on(args)
+    # (IL_SPLIT_SYNTH=1: batch j+1's Q on the integer stream, its K / V after batch j's attention --
+    # measured slower, 1.10-1.11 vs 1.06 ms per step: the integer stream only has the attention's gaps)
+    split_synth = piped and not args.no_fused_kv and bool(os.environ.get("IL_SPLIT_SYNTH"))
     # (two per-batch buffer slots for the pipelined schedule: batch b's attention reads slot b % 2
     # while batch b+1's integer stages write the other)
     pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream, fused_kv=not args.no_fused_kv,
@@ -342,8 +345,15 @@ def run_ours(args, rank, world, local_rank):
                 with torch.cuda.graph(g, stream=stream):
                     stage_fns[name]()
                 graphs[slot, name] = g
-            if slot == 0:
-                per_step_launches = pl.launches() - l0
+                if slot == 0 and name == "commit":
+                    per_step_launches = pl.launches() - l0
+                if piped and name == "synth" and split_synth:
+                    for part in ("q", "kv"):           # the pipelined schedule's split of the stand-in
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, stream=stream):
+                            pl.synth(part=part)
+                        graphs[slot, "synth_" + part] = g
+                    l0 += 2                           # (not extra launches of a step)
         pl.use(0)
         stream.synchronize()
 
@@ -443,6 +453,8 @@ def run_ours(args, rank, world, local_rank):
                     set_inputs(x)
                 for name in stage_names[:-3]:          # select, refine, match
                     run_stage(name)
+                if split_synth:
+                    graphs[j % 2, "synth_q"].replay()  # Q of batch j: no page writes
                 ev_m[j].record(stream)
                 if host:
                     out_fin[:x[3]].copy_(pl.final_ds[:x[3]], non_blocking=True)
@@ -450,7 +462,7 @@ def run_ours(args, rank, world, local_rank):
                     out_info[:x[3]].copy_(pl.info[:x[3]], non_blocking=True)
             with torch.cuda.stream(sA):
                 sA.wait_event(ev_m[j])
-                for name in ("synth", "attn"):
+                for name in (("synth_kv" if split_synth else "synth"), "attn"):
                     graphs[j % 2, name].replay()
                 ev_a[j].record(sA)
             with torch.cuda.stream(stream):
@@ -485,7 +497,7 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     launches = pl.launches() - launches0 - 2 * K      # minus the per-step k_stats (accounting, not the path)
     if graphs is not None:                             # replays do not pass through the host counter
-        launches += per_step_launches * (2 * K + (2 * K if piped else 0))
+        launches += per_step_launches * (2 * K + (2 * K if piped else 0)) + (2 * K if split_synth else 0)
     st_steps = [pl.ctx.stats_from_bytes(r) for r in rec_stats.cpu().numpy()]
     evicted = [s_["evicted_blocks"] for s_ in st_steps]
     # hit accounting of every timed step (device counters), summed over ranks: rank-local hits and

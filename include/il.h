@@ -311,7 +311,9 @@ il_status il_select_batch(il_ctx* ctx, uint32_t B, const uint32_t* q_off, const 
  * generator of DESIGN.md Z28, so cached pages equal recomputation.  q_scale scales Q.
  * il_synth_qkv_paged writes K and V straight into the request's KV pages (block_table of the
  * preceding il_prefix_match), as a model's QKV-projection epilogue writes the paged cache; the
- * following il_prefill_attn then gets k_new = v_new = NULL and skips its append pass. */
+ * following il_prefill_attn then gets k_new = v_new = NULL and skips its append pass.  A NULL q
+ * skips the Q heads, NULL k / v (both) the K and V heads: under cross-batch pipelining the next
+ * batch's Q can be written while this batch's attention runs, its K / V only after. */
 il_status il_synth_qkv(il_ctx* ctx, uint32_t B, const uint32_t* prompt_tok, const int32_t* cu_q,
                        const int32_t* prefix_len, uint64_t seed, float q_scale,
                        il_bf16* q, il_bf16* k_new, il_bf16* v_new, il_stream s);

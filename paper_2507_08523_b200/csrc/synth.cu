@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
                                                const int32_t* __restrict__ block_table,
                                                uint64_t sq, uint64_t sk, uint64_t sv, float qmul, float kvmul,
                                                __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ kn,
-                                               __nv_bfloat16* __restrict__ vn) {
+                                               __nv_bfloat16* __restrict__ vn, uint32_t h_begin, uint32_t h_end) {
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
   const uint32_t total = (uint32_t)cu_q[B];
   const uint32_t lane = threadIdx.x & 31;
@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
     const uint64_t kq = mix64(mix64(sq ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint64_t kk = mix64(mix64(sk ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint64_t kv = mix64(mix64(sv ^ (uint64_t)tok) ^ (uint64_t)pos);
-    const uint32_t nvec = (Hq + 2 * Hkv) * VPH;
+    const uint32_t nvec = h_end * VPH;                  // head rows [h_begin, h_end) of Q | K | V
     const size_t page_row = PAGED ? (size_t)(uint32_t)block_table[(size_t)i * c.max_blocks + pos / BS] * Hkv : 0;
-    for (uint32_t e = lane; e < nvec; e += 32) {
+    for (uint32_t e = h_begin * VPH + lane; e < nvec; e += 32) {
       const uint32_t h = e / VPH, x0 = (e % VPH) * 8;
       uint64_t key;
       float mul;
@@ -88,17 +88,22 @@ static il_status synth_launch(il_ctx* c, uint32_t B, const uint32_t* prompt_tok,
                               const int32_t* prefix_len, const int32_t* block_table, uint64_t seed, float q_scale,
                               il_bf16* q, il_bf16* kd, il_bf16* vd, il_stream s) {
   if (B == 0) return IL_OK;
+  if (!kd != !vd) { set_error("k and v: both or neither"); return IL_ERR_ARG; }
+  if (!q && !kd) return IL_OK;
   auto tseed = [&](uint64_t salt) { return mix64((seed << 8) ^ salt); };
   const float unit = 2.0f;                             // x = (f - 1.5) * 2 * scale
-  const uint32_t d = c->cfg.head_dim;
+  const uint32_t d = c->cfg.head_dim, Hq = c->cfg.n_q_heads, Hkv = c->cfg.n_kv_heads;
+  // a NULL q skips the Q heads, NULL k / v the K and V heads (Q of the next batch may be written
+  // while this batch's attention still reads the pages the next batch's K / V will overwrite)
+  const uint32_t h0 = q ? 0u : Hq, h1 = kd ? Hq + 2 * Hkv : Hq;
   if (d == 128)
     k_synth<128, PAGED><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, block_table,
         tseed(0x51), tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)kd,
-        (__nv_bfloat16*)vd);
+        (__nv_bfloat16*)vd, h0, h1);
   else
     k_synth<64, PAGED><<<c->num_sms * 8, 256, 0, (cudaStream_t)s>>>(*c, B, prompt_tok, cu_q, prefix_len, block_table,
         tseed(0x51), tseed(0x4B), tseed(0x56), q_scale * unit, unit, (__nv_bfloat16*)q, (__nv_bfloat16*)kd,
-        (__nv_bfloat16*)vd);
+        (__nv_bfloat16*)vd, h0, h1);
   IL_LAUNCH_CHECK("k_synth");
   c->launches += 1;
   return IL_OK;

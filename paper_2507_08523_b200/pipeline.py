@@ -117,12 +117,17 @@ class Pipeline:
         self.ctx.prefix_match(B, self.prompt_tok, self.prompt_len, self.block_hash, self.hit,
                               self.block_table, self.prefix_len, self.cu_q, stream=self.stream)
 
-    def synth(self, B=None) -> None:
+    def synth(self, B=None, part: str = "qkv") -> None:
+        """The QKV-projection stand-in; part = "q" / "kv" writes only Q / only K and V (fused_kv:
+        the pipelined schedule writes the next batch's Q before this batch's attention ends)."""
         B = self.B if B is None else B
         if self.fused_kv:
+            q = None if part == "kv" else self.q
+            kp, vp = (None, None) if part == "q" else (self.k_pages, self.v_pages)
             self.ctx.synth_qkv_paged(B, self.prompt_tok, self.cu_q, self.prefix_len, self.block_table, self.qkv_seed,
-                                     self.q_scale, self.q, self.k_pages, self.v_pages, stream=self.stream)
+                                     self.q_scale, q, kp, vp, stream=self.stream)
             return
+        assert part == "qkv", "split synth needs fused_kv"
         self._append_buffers()
         self.ctx.synth_qkv(B, self.prompt_tok, self.cu_q, self.prefix_len, self.qkv_seed, self.q_scale,
                            self.q, self.k_new, self.v_new, stream=self.stream)

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-2
 
 
-def _run(sp: StreamSpec, n_batches: int, split: int = 0):
+def _run(sp: StreamSpec, n_batches: int, split: int = 0, split_synth: bool = False):
     from paper_2507_08523_b200 import Pipeline
     ds, pool, instr = make_stream(sp)
     o = oracle_for(sp, pool, instr)
@@ -45,6 +45,8 @@ def _run(sp: StreamSpec, n_batches: int, split: int = 0):
             pl.use(j % 2)
             pl.stage_batch(gen.make_batch(ds, s, B))
             pl.select(); pl.refine(); pl.match()
+            if split_synth:
+                pl.synth(part="q")                     # batch j's Q beside batch j-1's attention
             ev_m[j].record(sB)
             ints = {n: getattr(pl, n)[:B].clone() for n in ("topk", "final_ds", "info", "prompt_len", "hit",
                                                           "prefix_len", "block_hash")}
@@ -52,7 +54,7 @@ def _run(sp: StreamSpec, n_batches: int, split: int = 0):
         with torch.cuda.stream(sA):                    # (host order: il.h's call order; device order: streams)
             sA.wait_event(ev_m[j])
             pl.stream = sA
-            pl.synth(); pl.attn()
+            pl.synth(part="kv" if split_synth else "qkv"); pl.attn()
             pl.stream = sB
             att = {"out": pl.out.clone(), "lse": pl.lse.clone()}
             ev_a[j].record(sA)
@@ -96,11 +98,12 @@ def _run(sp: StreamSpec, n_batches: int, split: int = 0):
     return worst
 
 
-def test_pipelined_stream_eviction_pressure():
+@pytest.mark.parametrize("split_synth", [False, True])
+def test_pipelined_stream_eviction_pressure(split_synth):
     # most batches evict: pages of batch b are evicted / freed by batch b+1's match while b's
-    # attention may still run
+    # attention may still run; split_synth: batch b+1's Q is written then too (its K / V after)
     sp = StreamSpec(C=700, B=32, T=64, flags=O.F_PAIR | O.F_VERIFY | O.F_GUARD, ramp=(4, 16))
-    assert _run(sp, 60) <= TOL
+    assert _run(sp, 60, split_synth=split_synth) <= TOL
 
 
 def test_pipelined_c1_stream_and_sm_split():
