@@ -43,6 +43,38 @@ def test_host_detected_argument_errors():
     assert e.value.status == L.IL_ERR_ARG
 
 
+def test_round2_call_argument_errors():
+    """il_set_sm_split, il_decode_attn, il_synth_qkv_paged: host-detected misuse."""
+    sp = StreamSpec(B=8, C=512)
+    ds, pool, instr = make_stream(sp)
+    pl = gpu_pipeline(sp, pool, instr)
+    with pytest.raises(L.ILError) as e:                    # the attention grid must leave an SM
+        pl.ctx.set_sm_split(10_000)
+    assert e.value.status == L.IL_ERR_ARG
+    pl.ctx.set_sm_split(0)
+    B = sp.B
+    with pytest.raises(L.ILError) as e:                    # decode before il_prefix_match
+        pl.ctx.decode_attn(B, pl.prefix_len, pl.block_table, pl.q, None, None, pl.k_pages, pl.v_pages,
+                           pl.out, None, 0.125)
+    assert e.value.status == L.IL_ERR_STATE
+    pl.stage_batch(gen.make_batch(ds, 0, B))
+    pl.refine(); pl.match()
+    with pytest.raises(L.ILError) as e:                    # k_new without v_new
+        pl.ctx.decode_attn(B, pl.prefix_len, pl.block_table, pl.q, pl.k_new, None, pl.k_pages, pl.v_pages,
+                           pl.out, None, 0.125)
+    assert e.value.status == L.IL_ERR_ARG
+    with pytest.raises(L.ILError) as e:                    # B > max_batch
+        pl.ctx.decode_attn(B + 1, pl.prefix_len, pl.block_table, pl.q, None, None, pl.k_pages, pl.v_pages,
+                           pl.out, None, 0.125)
+    assert e.value.status == L.IL_ERR_ARG
+    with pytest.raises(L.ILError) as e:                    # k pages without v pages
+        pl.ctx.synth_qkv_paged(B, pl.prompt_tok, pl.cu_q, pl.prefix_len, pl.block_table, 1, 1.0, pl.q,
+                               pl.k_pages, None)
+    assert e.value.status == L.IL_ERR_ARG
+    pl.commit()
+    pl.ctx.status_sync()
+
+
 def test_device_latched_capacity_error():
     # a cold batch needs more pages than the cache has: il_prefix_match latches IL_ERR_CAPACITY
     sp = StreamSpec(B=32, C=40)
