@@ -50,7 +50,8 @@ def ncu_traffic(args=None):
     """dram read+write bytes per launch of the attention kernel from the committed ncu summary
     (profiles/attn_ncu_summary.json, written from one `ncu --set full` capture of the DEFAULT
     run: c3, PAIR, fused K/V, no decode), or None for any other workload."""
-    if args is not None and (args.config != 3 or args.naive or args.no_fused_kv or args.decode):
+    if args is not None and (args.config != 3 or args.naive or args.no_fused_kv or args.decode or args.dedup
+                             or args.batch_dedup):
         return None, "no ncu capture of this workload (profiles/attn_ncu_summary.json is the default c3 run's)"
     p = os.path.join(ROOT, "profiles", "attn_ncu_summary.json")
     if os.path.exists(p):
