@@ -49,8 +49,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(Ctx c, uint32_t B, const int
   uint32_t acc = block_scan(n, s_w, &total);
   for (uint32_t i = tid * per; i < min(B, (tid + 1) * per); ++i) {
     c.tile_off[i] = acc;
-    const uint32_t nt = cdiv((uint32_t)(cu_q[i + 1] - cu_q[i]), tq);
-    for (uint32_t t = 0; t < nt; ++t) c.tile_req[acc + t] = i;
+    const uint32_t S = (uint32_t)(cu_q[i + 1] - cu_q[i]), nt = cdiv(S, tq);
+    const uint32_t P = (uint32_t)prefix_len[i], r0 = (uint32_t)cu_q[i], nblk = cdiv(P + S, BS);
+    for (uint32_t t = 0; t < nt; ++t) {
+      c.tile_req[acc + t] = i;
+      // (one 16-byte load decodes a tile in the phase-2 kernel: no dependent loads at item switches)
+      c.tile_desc[acc + t] = make_uint4(i, P + t * tq, r0 + t * tq, min(tq, S - t * tq) | (nblk << 8));
+    }
     acc += nt;
   }
   if (tid == 1023) {
@@ -119,6 +124,10 @@ il_status il::attn_setup(Ctx*) {
                                sm100::smem_bytes(128)));
   IL_CUDA(cudaFuncSetAttribute(sm100::k_attn_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                sm100::smem_bytes(64)));
+  IL_CUDA(cudaFuncSetAttribute(sm100::p2::k_attn_p2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               sm100::p2::smem_bytes2<128>));
+  IL_CUDA(cudaFuncSetAttribute(sm100::p2::k_attn_p2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               sm100::p2::smem_bytes2<64>));
   return IL_OK;
 }
 

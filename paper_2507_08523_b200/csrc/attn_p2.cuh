@@ -1,0 +1,401 @@
+// attn_p2.cuh — cascade phase 2 of the prefill attention (each request's own KV range past the
+// batch-shared prefix: its cached demonstrations, then its own suffix keys under the causal
+// mask) on 64-key KV steps with a DOUBLE-BUFFERED S per Q tile.
+//
+// Why a kernel of its own.  Phase 2 items are short (~2.4 128-key tiles per
+// M-tile at c3), so the per-tile chain of the shared kernel -- QK -> softmax -> (P aliases S)
+// PV -> next QK -> ... -- is the whole story there: with one S buffer per tile the next QK can
+// only be issued after the softmax has released P, and the tensor pipe idles (~20% busy).  Here
+// each Q tile owns two 64-column S buffers (TMEM: S0, S1, O per tile = 64 + 64 + 128 columns,
+// two tiles = 512), so QK of step n+1 runs while the softmax of step n does; P of step n is
+// written over the first 32 columns of its buffer and PV(n) must be issued before QK(n+2)
+// overwrites that buffer (tcgen05 ops of one thread execute in order).  64-key steps also halve
+// the keys computed past the causal diagonal.  (The QK MMA at N = 64 runs at 2/3 of the N = 128
+// rate -- SS mode reads Q's 4 KB per MMA from smem either way -- which phase 1, tensor bound,
+// could not afford; phase 2 is chain bound.)
+//
+// Work: the two Q tiles of a CTA are two independent PIPELINES (streams) x = 0 / 1, each with
+// its own Q buffer, K / V rings, TMA producer warp and MMA issuer warp; they share only the tensor
+// pipe and the SM's issue slots.  Stream x takes items w = blockIdx.x + k gridDim.x while M-tile
+// 2 (w / Hkv) + x exists; item w = that phase-2 M-tile (decode: one 16-byte k_tile_scan
+// descriptor, read one item ahead) with kv head w % Hkv.  Warp roles: warp 2x = producer of
+// stream x (Q, K and V TMAs; warp 2 also allocates TMEM), warp 2x + 1 = MMA issuer of stream x,
+// warps 4-7 / 8-11 = softmax + epilogue of stream 0 / 1.  The issuer's order per step s of an
+// item is QK(s), then PV(s - 1) (so the softmax of step s - 1 overlaps QK(s)), and PV(last) right
+// after the item's last QK; QK(s) overwrites the S buffer of step s - 2, whose PV precedes it.
+#pragma once
+// (included from attn_sm100.cuh after namespace sm100: uses its PTX wrappers, Tile and decode_tile)
+
+namespace il {
+namespace sm100 {
+namespace p2 {
+
+constexpr uint32_t BN2 = 64;                      // keys per KV step
+constexpr uint32_t KCB2 = BN2 * 128;              // one 64-column block of a 64-key K / V tile (8 KB)
+// per-stream K / V ring depths (64-key tiles): head dim 128 fills 224 KB with (2, 3)
+#ifndef IL_P2_NSTK
+#define IL_P2_NSTK 2
+#endif
+#ifndef IL_P2_NSTV
+#define IL_P2_NSTV 3
+#endif
+template <uint32_t DH> constexpr uint32_t NK2 = DH == 128 ? IL_P2_NSTK : 2 * IL_P2_NSTK;
+template <uint32_t DH> constexpr uint32_t NV2 = DH == 128 ? IL_P2_NSTV : 2 * IL_P2_NSTV;
+// smem per stream (NCB = DH / 64): Q NCB x 16 KB | K ring | V ring (NCB x 8 KB per 64-key tile); barriers after both
+template <uint32_t DH> constexpr uint32_t stream_bytes2 = (CB + (NK2<DH> + NV2<DH>) * KCB2) * (DH / 64);
+// per stream: Q_FULL, Q_FREE, S_FULL x 2, P_FULL x 2, PV_DONE, O_FULL, O_FREE, K_FULL / K_FREE, V_FULL / V_FREE
+enum Bar2 : uint32_t { Q_FULL2 = 0, Q_FREE2, S_FULL2, P_FULL2 = S_FULL2 + 2, PV_DONE2 = P_FULL2 + 2, O_FULL2, O_FREE2, K_RING2 };
+template <uint32_t DH> constexpr uint32_t nbar2 = K_RING2 + 2 * (NK2<DH> + NV2<DH>);
+template <uint32_t DH> constexpr uint32_t smem_bytes2 = 2 * stream_bytes2<DH> + 2 * nbar2<DH> * 8 + 64;
+
+// S = Q K^T at N = 64 keys; O += P V as in k_attn_sm100 (K = 16 keys per MMA, 4 per step)
+constexpr uint32_t IDESC_QK2 = (1u << 4) | (1u << 7) | (1u << 10) | ((BN2 >> 3) << 17) | ((BM >> 4) << 24);
+
+// A phase-2 M-tile from its k_tile_scan descriptor {request, position of its first suffix token,
+// its first suffix row, ntok | nblk << 8}: one 16-byte load, no dependent loads.
+struct TD {
+  uint32_t i, pos0, row0, ntok, nblk;
+};
+__device__ __forceinline__ TD unpack(uint4 d) { return TD{d.x, d.y, d.z, d.w & 0xFFu, d.w >> 8}; }
+// 64-key steps of a tile: key tiles 2 NC .. (position of its last row) / 64
+__device__ __forceinline__ uint32_t n_steps(uint4 d, uint32_t NC) { return (d.y + (d.w & 0xFFu) - 1) / BN2 + 1 - 2 * NC; }
+
+// (no setmaxnreg here: a 64-key row needs far fewer registers than k_attn_sm100's 128-key row,
+// and the producers keep two loads of lookahead)
+template <uint32_t DH>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_attn_p2(Ctx c, uint32_t B, const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out,
+              float* __restrict__ lse, float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
+              const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+  constexpr uint32_t D = DH, NCB = DH / 64, NK = NK2<DH>, NV = NV2<DH>, NB = nbar2<DH>;
+  constexpr uint32_t QTILE = NCB * CB, KVT = NCB * KCB2, SB = stream_bytes2<DH>;
+  constexpr uint32_t OFF_K = QTILE, OFF_V = OFF_K + NK * KVT;      // within a stream's region
+  static_assert(DH == 64 || DH == 128, "head dim");
+  static_assert(OFF_V + NV * KVT == SB && smem_bytes2<DH> <= 232448, "smem map");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + 2 * SB;
+  // barrier idx of stream x
+  auto bar = [&](uint32_t x, uint32_t idx) { return bar0 + 8 * (x * NB + idx); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * SB + 2 * NB * 8);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
+  const uint32_t NC = c.sc->shared_blk / 8;             // 128-key tiles of the batch-shared prefix
+  const uint32_t ntl = c.sc->n_tiles;
+  const uint32_t n_items = cdiv(ntl, 2) * Hkv;
+  const uint4* desc = c.tile_desc;
+  const bool cascade = NC > 0;                          // leave a partial for phase 1
+  constexpr uint32_t phase = 2;                         // (IL_TRACE: trace builds with IL_TRACE_PHASE=2)
+  (void)phase;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t x = 0; x < 2; ++x) {
+      mbar_init(bar(x, Q_FULL2), 1); mbar_init(bar(x, Q_FREE2), 1);
+      mbar_init(bar(x, PV_DONE2), 1); mbar_init(bar(x, O_FULL2), 1); mbar_init(bar(x, O_FREE2), 128);
+      for (uint32_t b = 0; b < 2; ++b) { mbar_init(bar(x, S_FULL2 + b), 1); mbar_init(bar(x, P_FULL2 + b), 128); }
+      for (uint32_t i = 0; i < 2 * (NK + NV); ++i) mbar_init(bar(x, K_RING2 + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_k) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_v) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns of stream x: S0 [256x, +64), S1 [256x + 64, +64), O [256x + 128, +128)
+
+  if (warp < 4) {
+    const uint32_t x = warp >> 1;                       // this warp's stream
+    const uint32_t sx = sbase + x * SB;                 // its smem region
+    // ring barriers of stream x: K_FULL [0, NK), K_FREE [NK, 2NK), V_FULL, V_FREE
+    auto kfull = [&](uint32_t i) { return bar(x, K_RING2 + i); };
+    auto kfree = [&](uint32_t i) { return bar(x, K_RING2 + NK + i); };
+    auto vfull = [&](uint32_t i) { return bar(x, K_RING2 + 2 * NK + i); };
+    auto vfree = [&](uint32_t i) { return bar(x, K_RING2 + 2 * NK + NV + i); };
+    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + x < ntl; };
+    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + x); };
+    uint32_t w = blockIdx.x;
+    uint4 d = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
+    if ((warp & 1) == 0) {
+      // ============ producer of stream x: Q of each item, then its K / V tiles (64 keys = 4 pages).
+      // The page ids of an item's first 8 steps are read one item ahead, lane l holding step
+      // l / 4's page l % 4 (the block tables are written by il_prefix_match and are usually out of
+      // L2 by now: a per-step read sat on the critical path); descriptors are read two items ahead.
+      const uint32_t qbytes = 2 * D * g * TQ;
+      auto page_at = [&](const uint4& dd, uint32_t kt, uint32_t p) -> int32_t {
+        const uint32_t blk = kt * 4 + p;
+#ifdef IL_P2_SAME_PAGES
+        return __ldg(block_table + (blk < (dd.w >> 8) ? blk : 0u));   // profiling variant: every tile reads request 0's pages
+#else
+        return __ldg(block_table + (size_t)dd.x * c.max_blocks + (blk < (dd.w >> 8) ? blk : 0u));
+#endif
+      };
+      auto pages_of = [&](const uint4& dd) -> int32_t {
+        return (lane >> 2) < n_steps(dd, NC) ? page_at(dd, 2 * NC + (lane >> 2), lane & 3) : 0;
+      };
+      uint32_t s = 0, ix = 0;
+      uint4 dn = ok(w + gridDim.x) ? ld(w + gridDim.x) : d;
+      int32_t pg = ok(w) ? pages_of(d) : 0;
+      while (ok(w)) {
+        const uint32_t wn = w + gridDim.x;
+        const uint4 dnn = ok(wn + gridDim.x) ? ld(wn + gridDim.x) : dn;
+        const int32_t pgn = ok(wn) ? pages_of(dn) : 0;
+        const uint32_t kh = w % Hkv, nst = n_steps(d, NC);
+        if (lane == 0) {
+          if (ix >= 1) mbar_wait(bar(x, Q_FREE2), (ix - 1) & 1);
+          mbar_expect_tx(bar(x, Q_FULL2), qbytes);
+          IL_TRACE(12 + x, ix & 4095);
+#pragma unroll
+          for (uint32_t h = 0; h < NCB; ++h)
+            tma_load_3d(sx + h * CB, &tm_q, (int)(64 * h), (int)(kh * g), (int)d.z, bar(x, Q_FULL2));
+          if (ok(wn)) {
+#pragma unroll
+            for (uint32_t h = 0; h < NCB; ++h) tma_prefetch_3d(&tm_q, (int)(64 * h), (int)((wn % Hkv) * g), (int)dn.z);
+          }
+        }
+        for (uint32_t j = 0; j < nst; ++j, ++s) {
+          const int32_t page = j < 8 ? __shfl_sync(~0u, pg, 4 * j + (lane & 3)) : page_at(d, 2 * NC + j, lane & 3);
+          const int row = (int)(((uint32_t)page * Hkv + kh) * BS);
+          const uint32_t ks = s % NK, vs = s % NV;
+          if (lane == 0) {
+            if (s >= NK) mbar_wait(kfree(ks), (s / NK - 1) & 1);
+            IL_TRACE(2 * x, s & 4095);
+#ifdef IL_P2_NO_KV
+            mbar_arrive(kfull(ks));                    // profiling variant: no K / V loads
+#else
+            mbar_expect_tx(kfull(ks), KVT);
+#endif
+          }
+          __syncwarp();
+#ifndef IL_P2_NO_KV
+          if (lane < 4 * NCB)                          // lane = (page, 64-column block)
+            tma_load_2d(sx + OFF_K + ks * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_k, (int)(64 * (lane >> 2)), row,
+                        kfull(ks));
+#endif
+          if (lane == 0) {
+            if (s >= NV) mbar_wait(vfree(vs), (s / NV - 1) & 1);
+            IL_TRACE(2 * x + 1, s & 4095);
+#ifdef IL_P2_NO_KV
+            mbar_arrive(vfull(vs));
+#else
+            mbar_expect_tx(vfull(vs), KVT);
+#endif
+          }
+          __syncwarp();
+#ifndef IL_P2_NO_KV
+          if (lane < 4 * NCB)
+            tma_load_2d(sx + OFF_V + vs * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_v, (int)(64 * (lane >> 2)), row,
+                        vfull(vs));
+#endif
+        }
+        ++ix;
+        w = wn;
+        d = dn;
+        dn = dnn;
+        pg = pgn;
+      }
+    } else {
+      // ================= MMA issuer of stream x (warp-uniform, one elected lane issues) ==========
+      const uint64_t dq = sdesc(sx, 16, 1024);
+      const uint64_t dk0 = sdesc(sx + OFF_K, 16, 1024), dv0 = sdesc(sx + OFF_V, KCB2, 1024);
+      const uint32_t o_tmem = tmem + 256 * x + 128;
+      uint32_t s = 0, it = 0;
+      // PV of step p (first / last: its item's first / last step; the item's index it_p)
+      auto pv = [&](uint32_t p, bool first, bool last, uint32_t it_p) {
+        const uint32_t vs = p % NV;
+        if (first && it_p > 0) mbar_wait(bar(x, O_FREE2), (it_p - 1) & 1);   // previous epilogue read O
+        mbar_wait(bar(x, P_FULL2 + (p & 1)), (p >> 1) & 1);
+        mbar_wait(vfull(vs), (p / NV) & 1);
+        tc_fence_after();
+        if (lane == 0) IL_TRACE(8 + x, p & 4095);
+        const uint64_t dv = dv0 + (uint64_t)((vs * KVT) >> 4);
+        const uint32_t p_tmem = tmem + 256 * x + 64 * (p & 1);
+#pragma unroll
+        for (uint32_t k = 0; k < BN2 / 16; ++k)
+          mma_ts_w<IDESC_PV_T<DH>>(o_tmem, p_tmem + 8 * k, dv + (uint64_t)((k * 2048) >> 4), (first && k == 0) ? 0u : 1u);
+        commit_w(bar(x, PV_DONE2));
+        if (last) commit_w(bar(x, O_FULL2));
+        commit_w(vfree(vs));
+      };
+      while (ok(w)) {
+        const uint32_t wn = w + gridDim.x;
+        const uint4 dn = ok(wn) ? ld(wn) : d;
+        const uint32_t nst = n_steps(d, NC);
+        for (uint32_t j = 0; j < nst; ++j, ++s) {
+          if (j == 0) mbar_wait(bar(x, Q_FULL2), it & 1);
+          const uint32_t ks = s % NK, b = s & 1;
+          mbar_wait(kfull(ks), (s / NK) & 1);
+          tc_fence_after();
+          if (lane == 0) IL_TRACE(6 + x, s & 4095);
+          const uint64_t dk = dk0 + (uint64_t)((ks * KVT) >> 4);
+#pragma unroll
+          for (uint32_t k = 0; k < D / 16; ++k)
+            mma_ss_w<IDESC_QK2>(tmem + 256 * x + 64 * b, dq + (uint64_t)(((k >> 2) * CB + (k & 3) * 32) >> 4),
+                                dk + (uint64_t)(((k >> 2) * KCB2 + (k & 3) * 32) >> 4), k ? 1u : 0u);
+          commit_w(bar(x, S_FULL2 + b));
+          commit_w(kfree(ks));
+          if (j + 1 == nst) commit_w(bar(x, Q_FREE2));  // the item's last QK has read Q
+          if (j >= 1) pv(s - 1, j == 1, false, it);      // the softmax of step s - 1 overlapped QK(s)
+          if (j + 1 == nst) pv(s, nst == 1, true, it);   // the item's last PV: its epilogue may start
+        }
+        ++it;
+        w = wn;
+        d = dn;
+      }
+    }
+  } else {
+    // ====== softmax + epilogue, one warpgroup per stream: thread = row r of its Q tile ======
+    const uint32_t sm_t = threadIdx.x - 128, xo = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
+    const uint32_t lane_addr = (32 * q4) << 16;
+    const uint32_t s_tmem = tmem + lane_addr + 256 * xo, o_tmem = s_tmem + 128;
+    const uint32_t t = r / g, hh = r % g;
+    uint32_t it = 0, cs = 0;
+    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xo < ntl; };
+    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + xo); };
+    uint32_t w = blockIdx.x;
+    uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
+    while (ok(w)) {
+      const uint32_t wn = w + gridDim.x;
+      const uint4 dn = ok(wn) ? ld(wn) : dcur;         // (used at the next item: the load runs meanwhile)
+      const TD T = unpack(dcur);
+      const uint32_t kh = w % Hkv;
+      const bool valid = (r < g * TQ) && (t < T.ntok);
+      const uint32_t pos_q = T.pos0 + min(t, T.ntok - 1);
+      const size_t orow = (size_t)(T.row0 + t) * Hq + kh * g + hh;
+      const uint32_t nst = n_steps(dcur, NC);
+      float m_used = -INFINITY, l = 0.f;
+      for (uint32_t n = 0; n < nst; ++n, ++cs) {
+        const uint32_t b = cs & 1u, sb = s_tmem + 64 * b;
+        mbar_wait(bar(xo, S_FULL2 + b), (cs >> 1) & 1);
+        tc_fence_after();
+        if (r == 0) IL_TRACE(4 + xo, cs & 4095);
+#ifdef IL_P2_NO_SM
+        {   // profiling variant: P = 0 without touching S
+          uint32_t z[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) z[j] = 0u;
+          tmem_st32u(sb, z);
+          tmem_wait_st();
+          tc_fence_before();
+          if (r == 0) IL_TRACE(10 + xo, cs & 4095);
+          mbar_arrive(bar(xo, P_FULL2 + b));
+          l = 1.f; m_used = 0.f;
+          continue;
+        }
+#endif
+        float a[64];
+        tmem_ld32(sb, *reinterpret_cast<float(*)[32]>(&a[0]));
+        tmem_ld32(sb + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
+        tmem_wait_ld();
+        // causal mask: keys key0 + j with j >= nv lie in this row's future (32-key chunks valid
+        // for the whole warp need no select)
+        const int nv = (int)pos_q - (int)((2 * NC + n) * BN2) + 1;
+        if (__any_sync(~0u, nv < (int)BN2)) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (__all_sync(~0u, 32 * q + 32 <= nv)) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[32 * q + j] = 32 * q + j < nv ? a[32 * q + j] : -INFINITY;
+          }
+        }
+        float mxa[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mxa[q] = a[q];
+#pragma unroll
+        for (int j = 8; j < 64; ++j) mxa[j & 7] = fmaxf(mxa[j & 7], a[j]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float mx2 = mx * scale_log2;
+        bool need = false;
+        float factor = 1.f;
+        if (m_used == -INFINITY) {
+          m_used = mx2;
+        } else if (mx2 > m_used + 8.f) {
+          need = true;
+          factor = ex2(m_used - mx2);
+          m_used = mx2;
+          l *= factor;
+        }
+        if (__any_sync(~0u, need)) {
+          // lazy rescale of O once PV(cs - 1) has landed (PV(cs - 2) was issued before QK(cs), so
+          // it completed before S(cs) was signalled)
+          mbar_wait(bar(xo, PV_DONE2), (cs - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int q = 0; q < (int)(D / 32); ++q) {
+            float ov[32];
+            tmem_ld32(o_tmem + 32 * q, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] *= factor;
+            tmem_st32(o_tmem + 32 * q, ov);
+          }
+          tmem_wait_st();
+        }
+        const float negm = m_used == -INFINITY ? 0.f : -m_used;
+        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          float x0, x1;
+          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+          const float p0 = ex2(x0), p1 = ex2(x1);
+          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+          pk[j >> 1] = pack_bf16(p0, p1);
+        }
+        tmem_st32u(sb, pk);                            // P (bf16 pairs) over the first 32 columns of S
+        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        tmem_wait_st();
+        tc_fence_before();
+        if (r == 0) IL_TRACE(10 + xo, cs & 4095);
+        mbar_arrive(bar(xo, P_FULL2 + b));
+      }
+      // epilogue: O / l -> bf16 row of `out`; the partial's m + log2 l (cascade) or the LSE
+      mbar_wait(bar(xo, O_FULL2), it & 1);
+      tc_fence_after();
+      {
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int q = 0; q < (int)(D / 32); ++q) {
+          float ov[32];
+          tmem_ld32(o_tmem + 32 * q, ov);
+          tmem_wait_ld();
+#ifdef IL_P2_NO_EPI
+          if (valid && ov[0] == 12345.f)               // profiling variant: no output stores
+#else
+          if (valid)
+#endif
+            store_row32(out + orow * D + 32 * q, ov, inv);
+        }
+        if (valid) {
+          if (cascade) c.attn_ml[orow] = m_used + __log2f(l);
+          else if (lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
+        }
+      }
+      tc_fence_before();
+      if (r == 0) IL_TRACE(14 + xo, it & 4095);
+      mbar_arrive(bar(xo, O_FREE2));
+      ++it;
+      w = wn;
+      dcur = dn;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+}  // namespace p2
+}  // namespace sm100
+}  // namespace il

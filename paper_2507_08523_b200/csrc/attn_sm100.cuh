@@ -288,6 +288,30 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return r;
 }
 
+// 256-bit global load / store (LDG.256 / STG.256 on sm_100a): a thread's 256-byte output row in
+// 8 accesses instead of 16 -- the rows of a warp lie in 8-32 different lines, so every access is
+// one L1 wavefront per lane group and halving their number halves the epilogue's LSU time
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]),
+               "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void ld_v8(const void* p, uint32_t (&v)[8]) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+// 32 fp32 values x inv -> 32 bf16 at p (64 bytes: two 256-bit stores)
+__device__ __forceinline__ void store_row32(__nv_bfloat16* p, const float (&ov)[32], float inv) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e] = pack_bf16(ov[16 * h + 2 * e] * inv, ov[16 * h + 2 * e + 1] * inv);
+    st_v8(p + 16 * h, w);
+  }
+}
+
 // UMMA shared-memory descriptor (sm100): start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46),
 // version 1 [46,48), layout SWIZZLE_128B = 2 [61,64).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -727,22 +751,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (r == 0 && xo == 0) IL_TRACE(12, it & 4095);
         // (the rows were prefetched into L2 by the Q producer one item ahead)
         if (valid) { m_used = c.attn_ml[orow]; l = 1.f; }
-        const uint4* src = reinterpret_cast<const uint4*>(out + orow * D);
-        uint4 raw[D / 8];
+        uint32_t raw[D / 16][8];
 #pragma unroll
-        for (int j = 0; j < (int)(D / 8); ++j) raw[j] = valid ? src[j] : make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < (int)(D / 16); ++j) {
+          if (valid) ld_v8(out + orow * D + 16 * j, raw[j]);
+          else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) raw[j][e] = 0u;
+          }
+        }
 #pragma unroll
         for (int q = 0; q < (int)(D / 32); ++q) {
           float ov[32];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 u = raw[4 * q + j];
-            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              ov[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
-              ov[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
-            }
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t u = raw[2 * q + (j >> 3)][j & 7];
+            ov[2 * j] = __uint_as_float(u << 16);
+            ov[2 * j + 1] = __uint_as_float(u & 0xFFFF0000u);
           }
           tmem_st32(o_tmem + 32 * q, ov);
         }
@@ -875,18 +900,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           float ov[32];
           tmem_ld32(o_tmem + 32 * q, ov);
           tmem_wait_ld();
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(out + orow * D + 32 * q);
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-              uint4 v;
-              v.x = pack_bf16(ov[8 * ch + 0] * inv, ov[8 * ch + 1] * inv);
-              v.y = pack_bf16(ov[8 * ch + 2] * inv, ov[8 * ch + 3] * inv);
-              v.z = pack_bf16(ov[8 * ch + 4] * inv, ov[8 * ch + 5] * inv);
-              v.w = pack_bf16(ov[8 * ch + 6] * inv, ov[8 * ch + 7] * inv);
-              dst[ch] = v;
-            }
-          }
+          if (valid) store_row32(out + orow * D + 32 * q, ov, inv);
         }
         if (valid) {
           if (phase == 2 && cascade) c.attn_ml[orow] = m_used + __log2f(l);
@@ -965,6 +979,11 @@ __global__ void __launch_bounds__(256) k_shared_scan(Ctx c, uint32_t B, const in
 }
 
 }  // namespace sm100
+}  // namespace il
+
+#include "attn_p2.cuh"
+
+namespace il {
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1011,9 +1030,13 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   }
   const char* ce = getenv("IL_CASCADE");
   const bool cascade = !(ce && ce[0] == '0');
+  // phase 2 on the 64-key double-buffered-S kernel (attn_p2.cuh); IL_P2=0 keeps it on
+  // k_attn_sm100 (the round-2 path, A / B comparisons)
+  const char* pe = getenv("IL_P2");
+  const bool p2 = !(pe && pe[0] == '0');
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
-  if (!decode) k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
+  if (!decode && !p2) k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
   const int grid = c->attn_ctas ? c->attn_ctas : c->num_sms;   // (il_set_sm_split)
   if (decode) {
     const uint32_t G2 = g <= 1 ? 1 : g <= 2 ? 2 : g <= 4 ? 4 : 8;
@@ -1034,6 +1057,16 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
     if (phase == 2 && decode) continue;
     if (phase == 1 && !cascade) break;
+    if (phase == 2 && p2) {
+      if (D == 128)
+        p2::k_attn_p2<128><<<grid, THREADS, p2::smem_bytes2<128>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
+            scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+      else
+        p2::k_attn_p2<64><<<grid, THREADS, p2::smem_bytes2<64>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
+            scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+      IL_LAUNCH_CHECK("k_attn_p2");
+      continue;
+    }
     if (D == 128)
       k_attn_sm100<128><<<grid, THREADS, smem_bytes(128), st>>>(*c, B, cu_q, prefix_len, block_table,
           (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
@@ -1042,7 +1075,8 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
           (__nv_bfloat16*)out, lse, scale * 1.4426950408889634f, g, TQ, phase, tq, to, tk, tv);
     IL_LAUNCH_CHECK("k_attn_sm100");
   }
-  c->launches += cascade ? (B > 1 ? 5 : 4) : 3;         // (decode: k_decode_own instead of k_pair_scan)
+  // k_tile_scan, k_shared_scan (cascade, B > 1), k_pair_scan (old phase 2) or k_decode_own, the two phases
+  c->launches += 1 + (cascade && B > 1 ? 1 : 0) + (decode || !p2 ? 1 : 0) + (decode ? 0u : 1u) + (cascade ? 1 : 0);
   return IL_OK;
 }
 

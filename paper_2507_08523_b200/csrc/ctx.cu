@@ -73,6 +73,7 @@ static size_t carve(Ctx* c, void* ws) {
   }
   c->tile_off = w.take<uint32_t>(B + 1);
   c->tile_req = w.take<uint32_t>((size_t)g.max_suffix_tokens / 16 + B + 1);
+  c->tile_desc = w.take<uint4>((size_t)g.max_suffix_tokens / 16 + B + 1);
   c->pair_nsh = w.take<uint32_t>((size_t)g.max_suffix_tokens / 32 + B + 1);
   c->attn_ml = w.take<float>((size_t)g.max_suffix_tokens * g.n_q_heads);
   c->evicted_list = w.take<uint64_t>(C);

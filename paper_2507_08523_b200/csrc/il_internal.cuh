@@ -105,6 +105,7 @@ struct Ctx {
   uint32_t dd_mask = 0;
   uint32_t *tile_off;        // attention work decomposition
   uint32_t *tile_req;        // attention M-tile -> request
+  uint4 *tile_desc;          // attention M-tile -> {request, first position, first suffix row, ntok | nblk << 8}
   uint32_t *pair_nsh;        // attention M-tile pair -> leading shared KV tiles
   float *attn_ml;            // cascade: per row log2 softmax mass of the shared-prefix partial
   uint64_t *evicted_list;
