@@ -128,6 +128,16 @@ il_status il::attn_setup(Ctx*) {
                                sm100::p2::smem_bytes2<128>));
   IL_CUDA(cudaFuncSetAttribute(sm100::p2::k_attn_p2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                sm100::p2::smem_bytes2<64>));
+  // the phase-2 kernel's setmaxnreg split assumes the launch register count (a smaller pool
+  // would leave setmaxnreg.inc waiting forever): refuse to run otherwise
+  for (const void* f : {(const void*)sm100::p2::k_attn_p2<128>, (const void*)sm100::p2::k_attn_p2<64>}) {
+    cudaFuncAttributes a;
+    IL_CUDA(cudaFuncGetAttributes(&a, f));
+    if (a.numRegs != sm100::p2::REGS2_LAUNCH) {
+      set_error("k_attn_p2 compiled with an unexpected register count (setmaxnreg pool)");
+      return IL_ERR_CUDA;
+    }
+  }
   return IL_OK;
 }
 

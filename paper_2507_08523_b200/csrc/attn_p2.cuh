@@ -39,14 +39,29 @@ constexpr uint32_t KCB2 = BN2 * 128;              // one 64-column block of a 64
 #ifndef IL_P2_NSTV
 #define IL_P2_NSTV 3
 #endif
+// bit (j / 2) % 8 set: exponential pair j of a row computed by the cubic on the FMA pipe (the two
+// streams' softmax warps share each SMSP's MUFU)
+#ifndef IL_P2_EMU
+#define IL_P2_EMU 0
+#endif
 template <uint32_t DH> constexpr uint32_t NK2 = DH == 128 ? IL_P2_NSTK : 2 * IL_P2_NSTK;
 template <uint32_t DH> constexpr uint32_t NV2 = DH == 128 ? IL_P2_NSTV : 2 * IL_P2_NSTV;
 // smem per stream (NCB = DH / 64): Q NCB x 16 KB | K ring | V ring (NCB x 8 KB per 64-key tile); barriers after both
 template <uint32_t DH> constexpr uint32_t stream_bytes2 = (CB + (NK2<DH> + NV2<DH>) * KCB2) * (DH / 64);
 // per stream: Q_FULL, Q_FREE, S_FULL x 2, P_FULL x 2, PV_DONE, O_FULL, O_FREE, K_FULL / K_FREE, V_FULL / V_FREE
-enum Bar2 : uint32_t { Q_FULL2 = 0, Q_FREE2, S_FULL2, P_FULL2 = S_FULL2 + 2, PV_DONE2 = P_FULL2 + 2, O_FULL2, O_FREE2, K_RING2 };
+enum Bar2 : uint32_t { Q_FULL2 = 0, Q_FREE2, S_FULL2, P_FULL2 = S_FULL2 + 2, PV_DONE2 = P_FULL2 + 2, O_FULL2, O_FREE2, L_READY2,
+                       K_RING2 };
 template <uint32_t DH> constexpr uint32_t nbar2 = K_RING2 + 2 * (NK2<DH> + NV2<DH>);
-template <uint32_t DH> constexpr uint32_t smem_bytes2 = 2 * stream_bytes2<DH> + 2 * nbar2<DH> * 8 + 64;
+// + the row sums / maxima the softmax warps hand to the epilogue warps (2 streams x 128 float2)
+template <uint32_t DH> constexpr uint32_t smem_bytes2 = 2 * stream_bytes2<DH> + 2 * nbar2<DH> * 8 + 64 + 2048;
+// warps 0-3 producers / issuers, 4-11 softmax, 12-19 epilogue (stream x: 12 + 4x .. 15 + 4x)
+constexpr int THREADS2 = 640;
+// register split (setmaxnreg, per warpgroup): the launch gives every thread REGS2_LAUNCH (ptxas'
+// cap for 640 threads; attn_setup checks the compiled count, since setmaxnreg.inc waits for the
+// CTA's pool to hold the request), producers / issuers and epilogue warps give some back, the
+// softmax warps (a 64-key row + its P) take it
+constexpr int REGS2_LAUNCH = 96, REGS2_PROD = 64, REGS2_EPI = 72, REGS2_SM = 136;
+static_assert(4 * REGS2_PROD + 8 * REGS2_EPI + 8 * REGS2_SM <= 20 * REGS2_LAUNCH, "register split exceeds the pool");
 
 // S = Q K^T at N = 64 keys; O += P V as in k_attn_sm100 (K = 16 keys per MMA, 4 per step)
 constexpr uint32_t IDESC_QK2 = (1u << 4) | (1u << 7) | (1u << 10) | ((BN2 >> 3) << 17) | ((BM >> 4) << 24);
@@ -63,7 +78,7 @@ __device__ __forceinline__ uint32_t n_steps(uint4 d, uint32_t NC) { return (d.y 
 // (no setmaxnreg here: a 64-key row needs far fewer registers than k_attn_sm100's 128-key row,
 // and the producers keep two loads of lookahead)
 template <uint32_t DH>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS2, 1)
     k_attn_p2(Ctx c, uint32_t B, const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out,
               float* __restrict__ lse, float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
               const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
@@ -80,6 +95,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // barrier idx of stream x
   auto bar = [&](uint32_t x, uint32_t idx) { return bar0 + 8 * (x * NB + idx); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * SB + 2 * NB * 8);
+  float2* s_lm = reinterpret_cast<float2*>(smem + 2 * SB + 2 * NB * 8 + 64);   // [stream][row] (l, m)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
@@ -95,6 +111,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (uint32_t x = 0; x < 2; ++x) {
       mbar_init(bar(x, Q_FULL2), 1); mbar_init(bar(x, Q_FREE2), 1);
       mbar_init(bar(x, PV_DONE2), 1); mbar_init(bar(x, O_FULL2), 1); mbar_init(bar(x, O_FREE2), 128);
+      mbar_init(bar(x, L_READY2), 128);
       for (uint32_t b = 0; b < 2; ++b) { mbar_init(bar(x, S_FULL2 + b), 1); mbar_init(bar(x, P_FULL2 + b), 128); }
       for (uint32_t i = 0; i < 2 * (NK + NV); ++i) mbar_init(bar(x, K_RING2 + i), 1);
     }
@@ -115,6 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // TMEM columns of stream x: S0 [256x, +64), S1 [256x + 64, +64), O [256x + 128, +128)
 
   if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS2_PROD));
     const uint32_t x = warp >> 1;                       // this warp's stream
     const uint32_t sx = sbase + x * SB;                 // its smem region
     // ring barriers of stream x: K_FULL [0, NK), K_FREE [NK, 2NK), V_FULL, V_FREE
@@ -169,7 +187,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t ks = s % NK, vs = s % NV;
           if (lane == 0) {
             if (s >= NK) mbar_wait(kfree(ks), (s / NK - 1) & 1);
+#ifndef IL_P2_TRACE_SM
             IL_TRACE(2 * x, s & 4095);
+#endif
 #ifdef IL_P2_NO_KV
             mbar_arrive(kfull(ks));                    // profiling variant: no K / V loads
 #else
@@ -184,7 +204,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
           if (lane == 0) {
             if (s >= NV) mbar_wait(vfree(vs), (s / NV - 1) & 1);
+#ifndef IL_P2_TRACE_SM
             IL_TRACE(2 * x + 1, s & 4095);
+#endif
 #ifdef IL_P2_NO_KV
             mbar_arrive(vfull(vs));
 #else
@@ -253,12 +275,60 @@ __global__ void __launch_bounds__(THREADS, 1)
         d = dn;
       }
     }
+  } else if (warp >= 12) {
+    // ====== epilogue of stream xe (warps 12 + 4 xe .. 15 + 4 xe): thread = row r, TMEM lane r.
+    // O / l -> bf16 row of `out`; the partial's m + log2 l (cascade) or the LSE.  The softmax warps
+    // hand l and m over through smem and go on with the next item; O is released (O_FREE) for the
+    // next item's first PV once read.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS2_EPI));
+    const uint32_t xe = (warp - 12) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
+    const uint32_t o_tmem = tmem + ((32 * q4) << 16) + 256 * xe + 128;
+    const uint32_t t = r / g, hh = r % g;
+    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xe < ntl; };
+    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + xe); };
+    uint32_t w = blockIdx.x, it = 0;
+    uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
+    while (ok(w)) {
+      const uint32_t wn = w + gridDim.x;
+      const uint4 dn = ok(wn) ? ld(wn) : dcur;
+      const TD T = unpack(dcur);
+      const bool valid = (r < g * TQ) && (t < T.ntok);
+      const size_t orow = (size_t)(T.row0 + t) * Hq + (w % Hkv) * g + hh;
+      mbar_wait(bar(xe, L_READY2), it & 1);
+      const float2 lm = s_lm[128 * xe + r];
+      mbar_wait(bar(xe, O_FULL2), it & 1);
+      tc_fence_after();
+      const float inv = 1.f / lm.x;
+#pragma unroll
+      for (int q = 0; q < (int)(D / 32); ++q) {
+        float ov[32];
+        tmem_ld32(o_tmem + 32 * q, ov);
+        tmem_wait_ld();
+#ifdef IL_P2_NO_EPI
+        if (valid && ov[0] == 12345.f)                 // profiling variant: no output stores
+#else
+        if (valid)
+#endif
+          store_row32(out + orow * D + 32 * q, ov, inv);
+      }
+      if (valid) {
+        if (cascade) c.attn_ml[orow] = lm.y + __log2f(lm.x);
+        else if (lse) lse[orow] = (lm.y + __log2f(lm.x)) * 0.69314718055994531f;
+      }
+      tc_fence_before();
+      if (r == 0) IL_TRACE(14 + xe, it & 4095);
+      mbar_arrive(bar(xe, O_FREE2));
+      ++it;
+      w = wn;
+      dcur = dn;
+    }
   } else {
-    // ====== softmax + epilogue, one warpgroup per stream: thread = row r of its Q tile ======
+    // ====== softmax, one warpgroup per stream: thread = row r of its Q tile ======
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS2_SM));
     const uint32_t sm_t = threadIdx.x - 128, xo = sm_t >> 7, r = sm_t & 127, q4 = warp & 3;
     const uint32_t lane_addr = (32 * q4) << 16;
     const uint32_t s_tmem = tmem + lane_addr + 256 * xo, o_tmem = s_tmem + 128;
-    const uint32_t t = r / g, hh = r % g;
+    const uint32_t t = r / g;
     uint32_t it = 0, cs = 0;
     auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xo < ntl; };
     auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + xo); };
@@ -268,10 +338,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t wn = w + gridDim.x;
       const uint4 dn = ok(wn) ? ld(wn) : dcur;         // (used at the next item: the load runs meanwhile)
       const TD T = unpack(dcur);
-      const uint32_t kh = w % Hkv;
-      const bool valid = (r < g * TQ) && (t < T.ntok);
       const uint32_t pos_q = T.pos0 + min(t, T.ntok - 1);
-      const size_t orow = (size_t)(T.row0 + t) * Hq + kh * g + hh;
       const uint32_t nst = n_steps(dcur, NC);
       float m_used = -INFINITY, l = 0.f;
       for (uint32_t n = 0; n < nst; ++n, ++cs) {
@@ -297,6 +364,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld32(sb, *reinterpret_cast<float(*)[32]>(&a[0]));
         tmem_ld32(sb + 32, *reinterpret_cast<float(*)[32]>(&a[32]));
         tmem_wait_ld();
+#ifdef IL_P2_TRACE_SM
+        if (r == 0 && xo == 0) IL_TRACE(0, cs & 4095);
+#endif
         // causal mask: keys key0 + j with j >= nv lie in this row's future (32-key chunks valid
         // for the whole warp need no select)
         const int nv = (int)pos_q - (int)((2 * NC + n) * BN2) + 1;
@@ -316,6 +386,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float mx2 = mx * scale_log2;
+#ifdef IL_P2_TRACE_SM
+        if (r == 0 && xo == 0) IL_TRACE(1, cs & 4095);
+#endif
         bool need = false;
         float factor = 1.f;
         if (m_used == -INFINITY) {
@@ -326,6 +399,34 @@ __global__ void __launch_bounds__(THREADS, 1)
           m_used = mx2;
           l *= factor;
         }
+        const float negm = m_used == -INFINITY ? 0.f : -m_used;
+        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          float x0, x1;
+          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
+          float p0, p1;
+          if ((IL_P2_EMU >> ((j >> 1) & 7)) & 1) {
+            ex2_poly2(x0, x1, p0, p1);                 // this pair on the FMA pipe
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
+          pk[j >> 1] = pack_bf16(p0, p1);
+        }
+#ifdef IL_P2_TRACE_SM
+        if (r == 0 && xo == 0) IL_TRACE(2, cs & 4095);
+#endif
+        tmem_st32u(sb, pk);                            // P (bf16 pairs) over the first 32 columns of S
+        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        tmem_wait_st();
+#ifdef IL_P2_TRACE_SM
+        if (r == 0 && xo == 0) IL_TRACE(3, cs & 4095);
+#endif
+        // (the O rescale comes after the exponentials, when S is no longer live: fewer registers;
+        // PV(cs) is only issued after P_FULL below, so it accumulates onto the rescaled O)
         if (__any_sync(~0u, need)) {
           // lazy rescale of O once PV(cs - 1) has landed (PV(cs - 2) was issued before QK(cs), so
           // it completed before S(cs) was signalled)
@@ -342,49 +443,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           tmem_wait_st();
         }
-        const float negm = m_used == -INFINITY ? 0.f : -m_used;
-        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[32];
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          float x0, x1;
-          ffma2(x0, x1, a[j], a[j + 1], scale_log2, negm);
-          const float p0 = ex2(x0), p1 = ex2(x1);
-          fadd2(rsa[(j >> 1) & 2], rsa[((j >> 1) & 2) + 1], p0, p1);
-          pk[j >> 1] = pack_bf16(p0, p1);
-        }
-        tmem_st32u(sb, pk);                            // P (bf16 pairs) over the first 32 columns of S
-        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
-        tmem_wait_st();
+
         tc_fence_before();
         if (r == 0) IL_TRACE(10 + xo, cs & 4095);
         mbar_arrive(bar(xo, P_FULL2 + b));
       }
-      // epilogue: O / l -> bf16 row of `out`; the partial's m + log2 l (cascade) or the LSE
-      mbar_wait(bar(xo, O_FULL2), it & 1);
-      tc_fence_after();
-      {
-        const float inv = 1.f / l;
-#pragma unroll
-        for (int q = 0; q < (int)(D / 32); ++q) {
-          float ov[32];
-          tmem_ld32(o_tmem + 32 * q, ov);
-          tmem_wait_ld();
-#ifdef IL_P2_NO_EPI
-          if (valid && ov[0] == 12345.f)               // profiling variant: no output stores
-#else
-          if (valid)
-#endif
-            store_row32(out + orow * D + 32 * q, ov, inv);
-        }
-        if (valid) {
-          if (cascade) c.attn_ml[orow] = m_used + __log2f(l);
-          else if (lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
-        }
-      }
-      tc_fence_before();
-      if (r == 0) IL_TRACE(14 + xo, it & 4095);
-      mbar_arrive(bar(xo, O_FREE2));
+      // hand l and m to the epilogue warps (single buffer: the previous item's epilogue has read
+      // it once it released O)
+      if (it >= 1) mbar_wait(bar(xo, O_FREE2), (it - 1) & 1);
+      s_lm[128 * xo + r] = make_float2(l, m_used);
+      mbar_arrive(bar(xo, L_READY2));
       ++it;
       w = wn;
       dcur = dn;

@@ -1059,10 +1059,10 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
     if (phase == 1 && !cascade) break;
     if (phase == 2 && p2) {
       if (D == 128)
-        p2::k_attn_p2<128><<<grid, THREADS, p2::smem_bytes2<128>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
+        p2::k_attn_p2<128><<<grid, p2::THREADS2, p2::smem_bytes2<128>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
             scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
       else
-        p2::k_attn_p2<64><<<grid, THREADS, p2::smem_bytes2<64>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
+        p2::k_attn_p2<64><<<grid, p2::THREADS2, p2::smem_bytes2<64>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
             scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
       IL_LAUNCH_CHECK("k_attn_p2");
       continue;

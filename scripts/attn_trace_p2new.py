@@ -54,6 +54,25 @@ def main():
     span = ev[-1][0] - t0
     n_items = sum(1 for _, n, _ in ev if n == "D0")
     print(f"phase 2 (attn_p2), CTA 0: {n_items} stream-0 items; span {span} cycles, {span / max(n_items, 1):.0f} per item")
+    # per stream: softmax time (S seen -> P stored) and wait (P stored -> next S seen), epilogue
+    for x in (0, 1):
+        S = {i: t for t, n, i in ev if n == f"S{x}"}
+        P = {i: t for t, n, i in ev if n == f"P{x}"}
+        QK = {i: t for t, n, i in ev if n == f"QK{x}"}
+        ks = sorted(set(S) & set(P))
+        sm = [P[k] - S[k] for k in ks]
+        gap = [S[k + 1] - P[k] for k in ks if k + 1 in S]
+        lat = [S[k] - QK[k] for k in ks if k in QK]
+        print(f"stream {x}: steps {len(ks)}; softmax median {np.median(sm):.0f}; P -> next S median {np.median(gap):.0f} "
+              f"(mean {np.mean(gap):.0f}); QK issue -> S seen median {np.median(lat):.0f}; span per step {span / max(len(ks), 1):.0f}")
+    if os.environ.get("IL_P2_TRACE_SM"):              # softmax sub-steps of stream 0 (slots 0-3)
+        S = tr[4]
+        for nm, a, b in (("S seen -> LDTM done", S, tr[0]), ("LDTM -> max done", tr[0], tr[1]),
+                         ("max -> exps done", tr[1], tr[2]), ("exps -> STTM done", tr[2], tr[3]),
+                         ("STTM -> P arrive", tr[3], tr[10])):
+            m = (a > 0) & (b > 0)
+            print(f"  {nm:22s} median {np.median(b[m] - a[m]):7.0f}  mean {np.mean(b[m] - a[m]):7.0f}")
+        return
     # per-event-type gap statistics
     w0 = sorted(t for t, n, _ in ev if n == "Q0")
     lo = w0[min(6, len(w0) - 1)]
