@@ -1,6 +1,8 @@
 // attn_p2.cuh — cascade phase 2 of the prefill attention (each request's own KV range past the
 // batch-shared prefix: its cached demonstrations, then its own suffix keys under the causal
-// mask) on 64-key KV steps with a DOUBLE-BUFFERED S per Q tile.
+// mask) on 64-key KV steps with a DOUBLE-BUFFERED S per Q tile.  It runs
+// after the dense pass over the shared prefix (k_attn_sm100 phase 3) and merges that pass's
+// partial (O / l, m + log2 l) into each row in its epilogue, writing the result and the LSE.
 //
 // Why a kernel of its own.  Phase 2 items are short (~2.4 128-key tiles per
 // M-tile at c3), so the per-tile chain of the shared kernel -- QK -> softmax -> (P aliases S)
@@ -60,7 +62,7 @@ constexpr int THREADS2 = 640;
 // cap for 640 threads; attn_setup checks the compiled count, since setmaxnreg.inc waits for the
 // CTA's pool to hold the request), producers / issuers and epilogue warps give some back, the
 // softmax warps (a 64-key row + its P) take it
-constexpr int REGS2_LAUNCH = 96, REGS2_PROD = 64, REGS2_EPI = 72, REGS2_SM = 136;
+constexpr int REGS2_LAUNCH = 96, REGS2_PROD = 56, REGS2_EPI = 96, REGS2_SM = 112;   // (EPI = LAUNCH: no setmaxnreg)
 static_assert(4 * REGS2_PROD + 8 * REGS2_EPI + 8 * REGS2_SM <= 20 * REGS2_LAUNCH, "register split exceeds the pool");
 
 // S = Q K^T at N = 64 keys; O += P V as in k_attn_sm100 (K = 16 keys per MMA, 4 per step)
@@ -81,7 +83,8 @@ template <uint32_t DH>
 __global__ void __launch_bounds__(THREADS2, 1)
     k_attn_p2(Ctx c, uint32_t B, const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out,
               float* __restrict__ lse, float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
-              const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+              const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_k,
+              const __grid_constant__ CUtensorMap tm_v) {
   constexpr uint32_t D = DH, NCB = DH / 64, NK = NK2<DH>, NV = NV2<DH>, NB = nbar2<DH>;
   constexpr uint32_t QTILE = NCB * CB, KVT = NCB * KCB2, SB = stream_bytes2<DH>;
   constexpr uint32_t OFF_K = QTILE, OFF_V = OFF_K + NK * KVT;      // within a stream's region
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
   const uint32_t ntl = c.sc->n_tiles;
   const uint32_t n_items = cdiv(ntl, 2) * Hkv;
   const uint4* desc = c.tile_desc;
-  const bool cascade = NC > 0;                          // leave a partial for phase 1
+  const bool merge = NC > 0;                            // the dense pass (phase 3) left a partial of every row
   constexpr uint32_t phase = 2;                         // (IL_TRACE: trace builds with IL_TRACE_PHASE=2)
   (void)phase;
 
@@ -176,9 +179,12 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #pragma unroll
           for (uint32_t h = 0; h < NCB; ++h)
             tma_load_3d(sx + h * CB, &tm_q, (int)(64 * h), (int)(kh * g), (int)d.z, bar(x, Q_FULL2));
-          if (ok(wn)) {
+          if (ok(wn)) {                                 // the next item's Q (and the partial it merges) into L2
 #pragma unroll
-            for (uint32_t h = 0; h < NCB; ++h) tma_prefetch_3d(&tm_q, (int)(64 * h), (int)((wn % Hkv) * g), (int)dn.z);
+            for (uint32_t h = 0; h < NCB; ++h) {
+              tma_prefetch_3d(&tm_q, (int)(64 * h), (int)((wn % Hkv) * g), (int)dn.z);
+              if (merge) tma_prefetch_3d(&tm_o, (int)(64 * h), (int)((wn % Hkv) * g), (int)dn.z);
+            }
           }
         }
         for (uint32_t j = 0; j < nst; ++j, ++s) {
@@ -277,10 +283,9 @@ __global__ void __launch_bounds__(THREADS2, 1)
     }
   } else if (warp >= 12) {
     // ====== epilogue of stream xe (warps 12 + 4 xe .. 15 + 4 xe): thread = row r, TMEM lane r.
-    // O / l -> bf16 row of `out`; the partial's m + log2 l (cascade) or the LSE.  The softmax warps
+    // merged O / L -> bf16 row of `out` and the LSE.  The softmax warps
     // hand l and m over through smem and go on with the next item; O is released (O_FREE) for the
     // next item's first PV once read.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS2_EPI));
     const uint32_t xe = (warp - 12) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
     const uint32_t o_tmem = tmem + ((32 * q4) << 16) + 256 * xe + 128;
     const uint32_t t = r / g, hh = r % g;
@@ -295,29 +300,55 @@ __global__ void __launch_bounds__(THREADS2, 1)
       const bool valid = (r < g * TQ) && (t < T.ntok);
       const size_t orow = (size_t)(T.row0 + t) * Hq + (w % Hkv) * g + hh;
       mbar_wait(bar(xe, L_READY2), it & 1);
-      const float2 lm = s_lm[128 * xe + r];
+      const float2 lm = s_lm[128 * xe + r];             // (l, m) of this row's own part
+      // merge with the dense pass's partial (O1 / l1 in `out`, m1 + log2 l1 in attn_ml):
+      // M = max(m, ml1), O = (O2 2^(m - M) + O1n 2^(ml1 - M)) / (l 2^(m - M) + 2^(ml1 - M))
+      const float ml1 = merge && valid ? c.attn_ml[orow] : -INFINITY;
+      const float mm = fmaxf(lm.y, ml1), a2 = ex2(lm.y - mm), a1 = ex2(ml1 - mm);
+      const float L = lm.x * a2 + a1, inv = 1.f / L;
+      const __nv_bfloat16* prow = out + orow * D;
+      const bool mv = merge && valid;
+      // O (scaled, as bf16 pairs) into registers, then O is released for the next item's first PV
+      // before the partial is read and added: the merge's loads stay off the stream's chain
+      uint32_t ob[D / 2];
       mbar_wait(bar(xe, O_FULL2), it & 1);
       tc_fence_after();
-      const float inv = 1.f / lm.x;
+      const float s2 = a2 * inv, s1 = a1 * inv;
 #pragma unroll
       for (int q = 0; q < (int)(D / 32); ++q) {
         float ov[32];
         tmem_ld32(o_tmem + 32 * q, ov);
         tmem_wait_ld();
-#ifdef IL_P2_NO_EPI
-        if (valid && ov[0] == 12345.f)                 // profiling variant: no output stores
-#else
-        if (valid)
-#endif
-          store_row32(out + orow * D + 32 * q, ov, inv);
-      }
-      if (valid) {
-        if (cascade) c.attn_ml[orow] = lm.y + __log2f(lm.x);
-        else if (lse) lse[orow] = (lm.y + __log2f(lm.x)) * 0.69314718055994531f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ob[16 * q + j] = pack_bf16(ov[2 * j] * s2, ov[2 * j + 1] * s2);
       }
       tc_fence_before();
       if (r == 0) IL_TRACE(14 + xe, it & 4095);
       mbar_arrive(bar(xe, O_FREE2));
+#pragma unroll
+      for (int h = 0; h < (int)(D / 16); ++h) {         // 16 columns = one 256-bit access
+        uint32_t w8[8];
+        if (mv) {
+          uint32_t pc[8];
+          ld_v8(prow + 16 * h, pc);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t u = ob[8 * h + e];
+            w8[e] = pack_bf16(__uint_as_float(u << 16) + __uint_as_float(pc[e] << 16) * s1,
+                              __uint_as_float(u & 0xFFFF0000u) + __uint_as_float(pc[e] & 0xFFFF0000u) * s1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w8[e] = ob[8 * h + e];
+        }
+#ifdef IL_P2_NO_EPI
+        if (valid && w8[0] == 12345u)                  // profiling variant: no output stores
+#else
+        if (valid)
+#endif
+          st_v8(out + orow * D + 16 * h, w8);
+      }
+      if (valid && lse) lse[orow] = (mm + __log2f(L)) * 0.69314718055994531f;
       ++it;
       w = wn;
       dcur = dn;

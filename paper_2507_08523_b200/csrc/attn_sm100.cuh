@@ -344,7 +344,7 @@ __device__ __forceinline__ Tile decode_tile(const Ctx& c, const int32_t* __restr
                                             const int32_t* __restrict__ prefix_len, uint32_t t, uint32_t TQ,
                                             uint32_t phase, uint32_t NC) {
   Tile T;
-  if (phase == 1) {
+  if (phase != 2) {                                     // phase 1 (or 3: phase 1 running first)
     T.valid = t < c.sc->n_dense;
     const uint32_t tot = c.sc->q_total;
     T.i = 0; T.mt = t; T.P = 0; T.r0 = 0; T.S = tot;
@@ -378,7 +378,7 @@ __device__ __forceinline__ Pair decode_pair(const Ctx& c, const int32_t* __restr
   p.kh = w % Hkv;
   p.a = decode_tile(c, cu_q, prefix_len, 2 * u, TQ, phase, NC);
   p.b = decode_tile(c, cu_q, prefix_len, 2 * u + 1, TQ, phase, NC);
-  p.nsh = p.b.valid ? (phase == 1 ? NC : c.pair_nsh[u]) : 0;
+  p.nsh = p.b.valid ? (phase != 2 ? NC : c.pair_nsh[u]) : 0;
   p.nload = p.a.n_kv + (p.b.valid ? p.b.n_kv - p.nsh : 0);
   return p;
 }
@@ -516,7 +516,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
   const uint32_t NC = c.sc->shared_blk / 8;
   // (phase 1 with NC = 0 has nothing to do: every item would have zero KV tiles)
-  const uint32_t n_items = phase == 1 ? (NC ? cdiv(c.sc->n_dense, 2) * Hkv : 0u) : cdiv(c.sc->n_tiles, 2) * Hkv;
+  // phase: 2 = each request's own M-tiles over KV tiles NC.. (leaves a partial when NC > 0);
+  // 1 = dense M-tiles over the NC shared tiles, continuing phase 2's partial; 3 = the same dense
+  // pass running FIRST and leaving the partial (O / l in `out`, m + log2 l in attn_ml) that the
+  // phase-2 kernel k_attn_p2 merges in its epilogue
+  const uint32_t n_items = phase != 2 ? (NC ? cdiv(c.sc->n_dense, 2) * Hkv : 0u) : cdiv(c.sc->n_tiles, 2) * Hkv;
   const bool cascade = NC > 0;                          // phase 2 leaves a partial that phase 1 merges
   const bool streams = IL_STREAMS && phase == 2;
 
@@ -903,7 +907,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (valid) store_row32(out + orow * D + 32 * q, ov, inv);
         }
         if (valid) {
-          if (phase == 2 && cascade) c.attn_ml[orow] = m_used + __log2f(l);
+          if ((phase == 2 && cascade) || phase == 3) c.attn_ml[orow] = m_used + __log2f(l);
           else if (lse) lse[orow] = (m_used + __log2f(l)) * 0.69314718055994531f;
         }
       }
@@ -1054,16 +1058,20 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
 #undef IL_DEC
     IL_LAUNCH_CHECK("k_decode_own");
   }
-  for (uint32_t phase : {2u, 1u}) {                    // (phase 1 has no items when NC = 0)
+  // phase order: with k_attn_p2, the dense pass over the shared prefix runs first (phase 3) and
+  // k_attn_p2 merges its partial in the epilogue; otherwise (decode, IL_P2=0) each request's own
+  // part runs first and the dense pass continues it (phase 1)
+  const bool p1_first = p2 && !decode;
+  for (uint32_t phase : {p1_first ? 3u : 2u, p1_first ? 2u : 1u}) {
     if (phase == 2 && decode) continue;
-    if (phase == 1 && !cascade) break;
+    if ((phase == 1 || phase == 3) && !cascade) continue;
     if (phase == 2 && p2) {
       if (D == 128)
         p2::k_attn_p2<128><<<grid, p2::THREADS2, p2::smem_bytes2<128>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
-            scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+            scale * 1.4426950408889634f, g, TQ, tq, to, tk, tv);
       else
         p2::k_attn_p2<64><<<grid, p2::THREADS2, p2::smem_bytes2<64>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
-            scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+            scale * 1.4426950408889634f, g, TQ, tq, to, tk, tv);
       IL_LAUNCH_CHECK("k_attn_p2");
       continue;
     }
