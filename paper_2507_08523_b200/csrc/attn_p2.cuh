@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
         uint32_t w8[8];
         if (mv) {
           uint32_t pc[8];
-          ld_v8(prow + 16 * h, pc);
+          ld_v8_nv(prow + 16 * h, pc);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t u = ob[8 * h + e];

@@ -301,6 +301,13 @@ __device__ __forceinline__ void ld_v8(const void* p, uint32_t (&v)[8]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "l"(p));
 }
+// the same load as a plain (non-volatile) asm: the compiler may hoist and batch it, for data
+// written by an earlier kernel (the phase-2 epilogue's partial rows)
+__device__ __forceinline__ void ld_v8_nv(const void* p, uint32_t (&v)[8]) {
+  asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+      : "l"(p));
+}
 // 32 fp32 values x inv -> 32 bf16 at p (64 bytes: two 256-bit stores)
 __device__ __forceinline__ void store_row32(__nv_bfloat16* p, const float (&ov)[32], float inv) {
 #pragma unroll
