@@ -57,7 +57,8 @@ def main(rep, out_all, out_attn):
     launches = summarise(rep)
     json.dump({"source": f"{rep} (ncu --set full --clock-control none, one steady-state step)",
                "launches": launches}, open(out_all, "w"), indent=1)
-    parts = [x for x in launches if "k_attn_sm100" in x["kernel"] or "k_kv_append" in x["kernel"]]
+    parts = [x for x in launches if "k_attn_sm100" in x["kernel"] or "k_attn_p2" in x["kernel"]
+             or "k_kv_append" in x["kernel"]]
     attn = {"source": f"{rep} (ncu --set full; k_attn_sm100 phase 2 + phase 1 of one step, + k_kv_append when the call appends)",
             "kernels": [x["kernel"] for x in parts],
             "duration": sum(x.get("duration", 0.0) for x in parts),
