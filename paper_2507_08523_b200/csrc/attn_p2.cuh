@@ -33,6 +33,9 @@ namespace sm100 {
 namespace p2 {
 
 constexpr uint32_t BN2 = 64;                      // keys per KV step
+#ifndef IL_P2_SKIP_PAD
+#define IL_P2_SKIP_PAD 0                          // (1: measured slower, 245 -> 255 us)
+#endif
 constexpr uint32_t KCB2 = BN2 * 128;              // one 64-column block of a 64-key K / V tile (8 KB)
 // per-stream K / V ring depths (64-key tiles): head dim 128 fills 224 KB with (2, 3)
 #ifndef IL_P2_NSTK
@@ -372,11 +375,20 @@ __global__ void __launch_bounds__(THREADS2, 1)
       const uint32_t pos_q = T.pos0 + min(t, T.ntok - 1);
       const uint32_t nst = n_steps(dcur, NC);
       float m_used = -INFINITY, l = 0.f;
+      const bool pad_warp = 32 * q4 >= g * T.ntok;         // (warp-uniform)
       for (uint32_t n = 0; n < nst; ++n, ++cs) {
         const uint32_t b = cs & 1u, sb = s_tmem + 64 * b;
         mbar_wait(bar(xo, S_FULL2 + b), (cs >> 1) & 1);
         tc_fence_after();
         if (r == 0) IL_TRACE(4 + xo, cs & 4095);
+#if IL_P2_SKIP_PAD
+        if (pad_warp) {
+          // every row of this warp is padding (rows >= g ntok): its P only feeds output rows nobody
+          // writes, so the warp skips the softmax (the other stream's warps get the SMSP's MUFU)
+          mbar_arrive(bar(xo, P_FULL2 + b));
+          continue;
+        }
+#endif
 #ifdef IL_P2_NO_SM
         {   // profiling variant: P = 0 without touching S
           uint32_t z[32];
