@@ -208,7 +208,9 @@ def run_ours(args, rank, world, local_rank):
                   max_pool_tokens=int(max(pool.log_off[-1], pool.tpl_off[-1])) + 16, max_log_tokens=255,
                   max_suffix_tokens=cfg.B * cfg.max_prompt_tokens, n_q_heads=cfg.Hq, n_kv_heads=cfg.Hkv,
                   head_dim=cfg.d, flags=flags, max_global_batch=cfg.B * world, max_decode_tokens=args.decode)
-    stream = torch.cuda.Stream(dev)
+    # (IL_BENCH_PRIO=1: the integer stream at high priority, so its kernels take the SMs the
+    # attention grids free at their boundaries -- A / B knob)
+    stream = torch.cuda.Stream(dev, priority=-1) if os.environ.get("IL_BENCH_PRIO") else torch.cuda.Stream(dev)
     piped = pipelined_on(args)
     # (IL_SPLIT_SYNTH=1: batch j+1's Q on the integer stream, its K / V after batch j's attention --
     # measured slower, 1.10-1.11 vs 1.06 ms per step: the integer stream only has the attention's gaps)

@@ -124,13 +124,15 @@ il_status il::attn_setup(Ctx*) {
                                sm100::smem_bytes(128)));
   IL_CUDA(cudaFuncSetAttribute(sm100::k_attn_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                sm100::smem_bytes(64)));
-  IL_CUDA(cudaFuncSetAttribute(sm100::p2::k_attn_p2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               sm100::p2::smem_bytes2<128>));
-  IL_CUDA(cudaFuncSetAttribute(sm100::p2::k_attn_p2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               sm100::p2::smem_bytes2<64>));
+  using sm100::p2::k_attn_p2;
+  IL_CUDA(cudaFuncSetAttribute(k_attn_p2<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<128>));
+  IL_CUDA(cudaFuncSetAttribute(k_attn_p2<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<64>));
+  IL_CUDA(cudaFuncSetAttribute(k_attn_p2<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<128>));
+  IL_CUDA(cudaFuncSetAttribute(k_attn_p2<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<64>));
   // the phase-2 kernel's setmaxnreg split assumes the launch register count (a smaller pool
   // would leave setmaxnreg.inc waiting forever): refuse to run otherwise
-  for (const void* f : {(const void*)sm100::p2::k_attn_p2<128>, (const void*)sm100::p2::k_attn_p2<64>}) {
+  for (const void* f : {(const void*)k_attn_p2<128, false>, (const void*)k_attn_p2<64, false>,
+                        (const void*)k_attn_p2<128, true>, (const void*)k_attn_p2<64, true>}) {
     cudaFuncAttributes a;
     IL_CUDA(cudaFuncGetAttributes(&a, f));
     if (a.numRegs != sm100::p2::REGS2_LAUNCH) {

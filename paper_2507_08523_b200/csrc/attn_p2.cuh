@@ -80,19 +80,28 @@ __device__ __forceinline__ TD unpack(uint4 d) { return TD{d.x, d.y, d.z, d.w & 0
 // 64-key steps of a tile: key tiles 2 NC .. (position of its last row) / 64
 __device__ __forceinline__ uint32_t n_steps(uint4 d, uint32_t NC) { return (d.y + (d.w & 0xFFu) - 1) / BN2 + 1 - 2 * NC; }
 
-// (no setmaxnreg here: a 64-key row needs far fewer registers than k_attn_sm100's 128-key row,
-// and the producers keep two loads of lookahead)
-template <uint32_t DH>
+// DENSE = false: phase 2 (each request's own M-tiles over its keys past the shared prefix, merging
+// the dense pass's partial).  DENSE = true: the dense pass itself (phase 3) -- M-tiles of TQ
+// consecutive suffix rows of the batch (rows of several requests) over the batch-shared prefix
+// (request 0's pages, 2 NC 64-key steps, no causal mask: every suffix position lies past it),
+// writing the partial (O / l, m + log2 l).  There the two streams process M-tiles 2u and 2u + 1
+// of the same kv head, i.e. the SAME K / V tiles: one producer warp fills K / V rings both issuers
+// read (twice as deep; each slot is released by both), warp 2 loads both Q tiles.
+template <uint32_t DH, bool DENSE>
 __global__ void __launch_bounds__(THREADS2, 1)
     k_attn_p2(Ctx c, uint32_t B, const int32_t* __restrict__ block_table, __nv_bfloat16* __restrict__ out,
               float* __restrict__ lse, float scale_log2, uint32_t g, uint32_t TQ, const __grid_constant__ CUtensorMap tm_q,
               const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v) {
-  constexpr uint32_t D = DH, NCB = DH / 64, NK = NK2<DH>, NV = NV2<DH>, NB = nbar2<DH>;
+  constexpr uint32_t D = DH, NCB = DH / 64, NB = nbar2<DH>;
+  // ring depths: per stream, or (DENSE) one pair of rings twice as deep shared by both streams
+  constexpr uint32_t NK = DENSE ? 2 * NK2<DH> : NK2<DH>, NV = DENSE ? 2 * NV2<DH> : NV2<DH>;
+  constexpr uint32_t RB = 2 * (NK2<DH> + NV2<DH>);                // ring barriers per stream block
   constexpr uint32_t QTILE = NCB * CB, KVT = NCB * KCB2, SB = stream_bytes2<DH>;
-  constexpr uint32_t OFF_K = QTILE, OFF_V = OFF_K + NK * KVT;      // within a stream's region
+  constexpr uint32_t OFF_K = QTILE, OFF_V = OFF_K + NK2<DH> * KVT;      // within a stream's region
   static_assert(DH == 64 || DH == 128, "head dim");
-  static_assert(OFF_V + NV * KVT == SB && smem_bytes2<DH> <= 232448, "smem map");
+  static_assert(OFF_V + NV2<DH> * KVT == SB && smem_bytes2<DH> <= 232448, "smem map");
+  static_assert(!DENSE || 2 * QTILE + (NK + NV) * KVT == 2 * SB, "DENSE smem map");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023) != 0) __trap();
@@ -106,10 +115,30 @@ __global__ void __launch_bounds__(THREADS2, 1)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Hq = c.cfg.n_q_heads, Hkv = c.cfg.n_kv_heads;
   const uint32_t NC = c.sc->shared_blk / 8;             // 128-key tiles of the batch-shared prefix
-  const uint32_t ntl = c.sc->n_tiles;
-  const uint32_t n_items = cdiv(ntl, 2) * Hkv;
+  const uint32_t q_total = c.sc->q_total;
+  // M-tiles: phase-2 tiles, or (DENSE) the dense tiles rounded up to an even count (a padding tile
+  // has no rows: its outputs are never written)
+  const uint32_t ntl = DENSE ? cdiv(c.sc->n_dense, 2) * 2 : c.sc->n_tiles;
+  // (DENSE with no batch-shared prefix, NC = 0: nothing to do -- every item would have no steps)
+  const uint32_t n_items = DENSE && NC == 0 ? 0u : cdiv(ntl, 2) * Hkv;
   const uint4* desc = c.tile_desc;
-  const bool merge = NC > 0;                            // the dense pass (phase 3) left a partial of every row
+  const bool merge = !DENSE && NC > 0;                  // the dense pass (phase 3) left a partial of every row
+  const uint32_t kt0 = DENSE ? 0u : 2 * NC;             // first 64-key tile
+  // tile t's descriptor {request, first position, first suffix row, ntok | nblk << 8}; the dense
+  // tiles' rows lie past the shared prefix whatever their request (position 2^30: no mask)
+  auto tdesc = [&](uint32_t t) -> uint4 {
+    if (DENSE) {
+      const uint32_t r0 = t * TQ, nt = r0 < q_total ? min(TQ, q_total - r0) : 0u;
+      return make_uint4(0u, 1u << 30, r0, nt | ((8 * NC) << 8));
+    }
+    return __ldg(desc + t);
+  };
+  auto nsteps = [&](const uint4& dd) -> uint32_t { return DENSE ? 2 * NC : n_steps(dd, NC); };
+  // ring barrier i: the stream's own block, or (DENSE) both streams' blocks as one
+  auto rbar = [&](uint32_t x, uint32_t i) {
+    return DENSE ? (i < RB ? bar(0, K_RING2 + i) : bar(1, K_RING2 + i - RB)) : bar(x, K_RING2 + i);
+  };
+  static_assert(!DENSE || 2 * (NK + NV) == 2 * RB, "shared rings use both streams' barrier blocks");
   constexpr uint32_t phase = 2;                         // (IL_TRACE: trace builds with IL_TRACE_PHASE=2)
   (void)phase;
 
@@ -119,8 +148,14 @@ __global__ void __launch_bounds__(THREADS2, 1)
       mbar_init(bar(x, PV_DONE2), 1); mbar_init(bar(x, O_FULL2), 1); mbar_init(bar(x, O_FREE2), 128);
       mbar_init(bar(x, L_READY2), 128);
       for (uint32_t b = 0; b < 2; ++b) { mbar_init(bar(x, S_FULL2 + b), 1); mbar_init(bar(x, P_FULL2 + b), 128); }
-      for (uint32_t i = 0; i < 2 * (NK + NV); ++i) mbar_init(bar(x, K_RING2 + i), 1);
+      for (uint32_t i = 0; i < RB; ++i) mbar_init(bar(x, K_RING2 + i), 1);
     }
+    if (DENSE)                                          // shared K_FREE / V_FREE: released by both issuers
+      for (uint32_t i = 0; i < NK + NV; ++i) {
+        const uint32_t j = i < NK ? NK + i : 2 * NK + NV + (i - NK);
+        const uint32_t b = j < RB ? bar(0, K_RING2 + j) : bar(1, K_RING2 + j - RB);
+        mbar_init(b, 2);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tm_k) : "memory");
@@ -140,18 +175,44 @@ __global__ void __launch_bounds__(THREADS2, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS2_PROD));
     const uint32_t x = warp >> 1;                       // this warp's stream
-    const uint32_t sx = sbase + x * SB;                 // its smem region
-    // ring barriers of stream x: K_FULL [0, NK), K_FREE [NK, 2NK), V_FULL, V_FREE
-    auto kfull = [&](uint32_t i) { return bar(x, K_RING2 + i); };
-    auto kfree = [&](uint32_t i) { return bar(x, K_RING2 + NK + i); };
-    auto vfull = [&](uint32_t i) { return bar(x, K_RING2 + 2 * NK + i); };
-    auto vfree = [&](uint32_t i) { return bar(x, K_RING2 + 2 * NK + NV + i); };
+    // smem: Q of stream x, its K / V rings (DENSE: Q0 | Q1 | the shared K ring | the shared V ring)
+    const uint32_t sq = DENSE ? sbase + x * QTILE : sbase + x * SB;
+    const uint32_t sk = DENSE ? sbase + 2 * QTILE : sq + OFF_K, sv = DENSE ? sk + NK * KVT : sq + OFF_V;
+    // ring barriers: K_FULL [0, NK), K_FREE [NK, 2NK), V_FULL, V_FREE
+    auto kfull = [&](uint32_t i) { return rbar(x, i); };
+    auto kfree = [&](uint32_t i) { return rbar(x, NK + i); };
+    auto vfull = [&](uint32_t i) { return rbar(x, 2 * NK + i); };
+    auto vfree = [&](uint32_t i) { return rbar(x, 2 * NK + NV + i); };
     auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + x < ntl; };
-    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + x); };
+    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + x); };
     uint32_t w = blockIdx.x;
     uint4 d = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
-    if ((warp & 1) == 0) {
-      // ============ producer of stream x: Q of each item, then its K / V tiles (64 keys = 4 pages).
+    if (DENSE && warp == 2) {
+      // ============ (DENSE) Q producer: lane xq loads stream xq's Q tile of each item
+      if (lane < 2) {
+        const uint32_t xq = lane, qbytes = 2 * D * g * TQ, sqx = sbase + xq * QTILE;
+        auto okq = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xq < ntl; };
+        uint32_t ix = 0, wq = blockIdx.x;
+        uint4 dl = okq(wq) ? tdesc(2 * (wq / Hkv) + xq) : make_uint4(0, 0, 0, 0);
+        for (; okq(wq); wq += gridDim.x, ++ix) {
+          const uint32_t wn = wq + gridDim.x;
+          const uint4 dn = okq(wn) ? tdesc(2 * (wn / Hkv) + xq) : dl;
+          if (ix >= 1) mbar_wait(bar(xq, Q_FREE2), (ix - 1) & 1);
+          mbar_expect_tx(bar(xq, Q_FULL2), qbytes);
+#pragma unroll
+          for (uint32_t h = 0; h < NCB; ++h)
+            tma_load_3d(sqx + h * CB, &tm_q, (int)(64 * h), (int)((wq % Hkv) * g), (int)dl.z, bar(xq, Q_FULL2));
+          if (okq(wn)) {
+#pragma unroll
+            for (uint32_t h = 0; h < NCB; ++h) tma_prefetch_3d(&tm_q, (int)(64 * h), (int)((wn % Hkv) * g), (int)dn.z);
+          }
+          dl = dn;
+        }
+      }
+      __syncwarp();
+    } else if ((warp & 1) == 0) {
+      // ============ producer of stream x: Q of each item, then its K / V tiles (64 keys = 4 pages);
+      // (DENSE: warp 0, K / V only, for both streams -- their items share kv head and pages).
       // The page ids of an item's first 8 steps are read one item ahead, lane l holding step
       // l / 4's page l % 4 (the block tables are written by il_prefix_match and are usually out of
       // L2 by now: a per-step read sat on the critical path); descriptors are read two items ahead.
@@ -165,7 +226,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #endif
       };
       auto pages_of = [&](const uint4& dd) -> int32_t {
-        return (lane >> 2) < n_steps(dd, NC) ? page_at(dd, 2 * NC + (lane >> 2), lane & 3) : 0;
+        return (lane >> 2) < nsteps(dd) ? page_at(dd, kt0 + (lane >> 2), lane & 3) : 0;
       };
       uint32_t s = 0, ix = 0;
       uint4 dn = ok(w + gridDim.x) ? ld(w + gridDim.x) : d;
@@ -174,14 +235,14 @@ __global__ void __launch_bounds__(THREADS2, 1)
         const uint32_t wn = w + gridDim.x;
         const uint4 dnn = ok(wn + gridDim.x) ? ld(wn + gridDim.x) : dn;
         const int32_t pgn = ok(wn) ? pages_of(dn) : 0;
-        const uint32_t kh = w % Hkv, nst = n_steps(d, NC);
-        if (lane == 0) {
+        const uint32_t kh = w % Hkv, nst = nsteps(d);
+        if (!DENSE && lane == 0) {
           if (ix >= 1) mbar_wait(bar(x, Q_FREE2), (ix - 1) & 1);
           mbar_expect_tx(bar(x, Q_FULL2), qbytes);
           IL_TRACE(12 + x, ix & 4095);
 #pragma unroll
           for (uint32_t h = 0; h < NCB; ++h)
-            tma_load_3d(sx + h * CB, &tm_q, (int)(64 * h), (int)(kh * g), (int)d.z, bar(x, Q_FULL2));
+            tma_load_3d(sq + h * CB, &tm_q, (int)(64 * h), (int)(kh * g), (int)d.z, bar(x, Q_FULL2));
           if (ok(wn)) {                                 // the next item's Q (and the partial it merges) into L2
 #pragma unroll
             for (uint32_t h = 0; h < NCB; ++h) {
@@ -191,7 +252,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
           }
         }
         for (uint32_t j = 0; j < nst; ++j, ++s) {
-          const int32_t page = j < 8 ? __shfl_sync(~0u, pg, 4 * j + (lane & 3)) : page_at(d, 2 * NC + j, lane & 3);
+          const int32_t page = j < 8 ? __shfl_sync(~0u, pg, 4 * j + (lane & 3)) : page_at(d, kt0 + j, lane & 3);
           const int row = (int)(((uint32_t)page * Hkv + kh) * BS);
           const uint32_t ks = s % NK, vs = s % NV;
           if (lane == 0) {
@@ -208,7 +269,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
           __syncwarp();
 #ifndef IL_P2_NO_KV
           if (lane < 4 * NCB)                          // lane = (page, 64-column block)
-            tma_load_2d(sx + OFF_K + ks * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_k, (int)(64 * (lane >> 2)), row,
+            tma_load_2d(sk + ks * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_k, (int)(64 * (lane >> 2)), row,
                         kfull(ks));
 #endif
           if (lane == 0) {
@@ -225,7 +286,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
           __syncwarp();
 #ifndef IL_P2_NO_KV
           if (lane < 4 * NCB)
-            tma_load_2d(sx + OFF_V + vs * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_v, (int)(64 * (lane >> 2)), row,
+            tma_load_2d(sv + vs * KVT + (lane >> 2) * KCB2 + (lane & 3) * 2048, &tm_v, (int)(64 * (lane >> 2)), row,
                         vfull(vs));
 #endif
         }
@@ -237,8 +298,8 @@ __global__ void __launch_bounds__(THREADS2, 1)
       }
     } else {
       // ================= MMA issuer of stream x (warp-uniform, one elected lane issues) ==========
-      const uint64_t dq = sdesc(sx, 16, 1024);
-      const uint64_t dk0 = sdesc(sx + OFF_K, 16, 1024), dv0 = sdesc(sx + OFF_V, KCB2, 1024);
+      const uint64_t dq = sdesc(sq, 16, 1024);
+      const uint64_t dk0 = sdesc(sk, 16, 1024), dv0 = sdesc(sv, KCB2, 1024);
       const uint32_t o_tmem = tmem + 256 * x + 128;
       uint32_t s = 0, it = 0;
       // PV of step p (first / last: its item's first / last step; the item's index it_p)
@@ -261,7 +322,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
       while (ok(w)) {
         const uint32_t wn = w + gridDim.x;
         const uint4 dn = ok(wn) ? ld(wn) : d;
-        const uint32_t nst = n_steps(d, NC);
+        const uint32_t nst = nsteps(d);
         for (uint32_t j = 0; j < nst; ++j, ++s) {
           if (j == 0) mbar_wait(bar(x, Q_FULL2), it & 1);
           const uint32_t ks = s % NK, b = s & 1;
@@ -293,7 +354,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
     const uint32_t o_tmem = tmem + ((32 * q4) << 16) + 256 * xe + 128;
     const uint32_t t = r / g, hh = r % g;
     auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xe < ntl; };
-    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + xe); };
+    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + xe); };
     uint32_t w = blockIdx.x, it = 0;
     uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
     while (ok(w)) {
@@ -351,7 +412,10 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #endif
           st_v8(out + orow * D + 16 * h, w8);
       }
-      if (valid && lse) lse[orow] = (mm + __log2f(L)) * 0.69314718055994531f;
+      if (valid) {
+        if (DENSE) c.attn_ml[orow] = mm + __log2f(L);    // the partial the phase-2 kernel merges
+        else if (lse) lse[orow] = (mm + __log2f(L)) * 0.69314718055994531f;
+      }
       ++it;
       w = wn;
       dcur = dn;
@@ -365,7 +429,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
     const uint32_t t = r / g;
     uint32_t it = 0, cs = 0;
     auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xo < ntl; };
-    auto ld = [&](uint32_t ww) { return __ldg(desc + 2 * (ww / Hkv) + xo); };
+    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + xo); };
     uint32_t w = blockIdx.x;
     uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
     while (ok(w)) {
@@ -373,7 +437,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
       const uint4 dn = ok(wn) ? ld(wn) : dcur;         // (used at the next item: the load runs meanwhile)
       const TD T = unpack(dcur);
       const uint32_t pos_q = T.pos0 + min(t, T.ntok - 1);
-      const uint32_t nst = n_steps(dcur, NC);
+      const uint32_t nst = nsteps(dcur);
       float m_used = -INFINITY, l = 0.f;
       const bool pad_warp = 32 * q4 >= g * T.ntok;         // (warp-uniform)
       for (uint32_t n = 0; n < nst; ++n, ++cs) {
@@ -412,7 +476,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #endif
         // causal mask: keys key0 + j with j >= nv lie in this row's future (32-key chunks valid
         // for the whole warp need no select)
-        const int nv = (int)pos_q - (int)((2 * NC + n) * BN2) + 1;
+        const int nv = (int)pos_q - (int)((kt0 + n) * BN2) + 1;
         if (__any_sync(~0u, nv < (int)BN2)) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {

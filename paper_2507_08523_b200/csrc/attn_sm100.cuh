@@ -1045,6 +1045,10 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   // k_attn_sm100 (the round-2 path, A / B comparisons)
   const char* pe = getenv("IL_P2");
   const bool p2 = !(pe && pe[0] == '0');
+  // IL_DENSE_P2=1: the dense pass on k_attn_p2<DH, true> (64-key double-buffered S, shared K / V
+  // rings) instead of k_attn_sm100 phase 3 -- measured slower, 644 vs 512 us
+  const char* pd = getenv("IL_DENSE_P2");
+  const bool dense_old = !(pd && pd[0] == '1');
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
   if (!decode && !p2) k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
@@ -1072,13 +1076,17 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   for (uint32_t phase : {p1_first ? 3u : 2u, p1_first ? 2u : 1u}) {
     if (phase == 2 && decode) continue;
     if ((phase == 1 || phase == 3) && !cascade) continue;
-    if (phase == 2 && p2) {
-      if (D == 128)
-        p2::k_attn_p2<128><<<grid, p2::THREADS2, p2::smem_bytes2<128>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
-            scale * 1.4426950408889634f, g, TQ, tq, to, tk, tv);
-      else
-        p2::k_attn_p2<64><<<grid, p2::THREADS2, p2::smem_bytes2<64>, st>>>(*c, B, block_table, (__nv_bfloat16*)out, lse,
-            scale * 1.4426950408889634f, g, TQ, tq, to, tk, tv);
+    // phase 2, and (unless IL_DENSE_OLD=1) the dense pass too, on k_attn_p2
+    if ((phase == 2 && p2) || (phase == 3 && !dense_old)) {
+      const float sl2 = scale * 1.4426950408889634f;
+      __nv_bfloat16* o16 = (__nv_bfloat16*)out;
+      if (D == 128) {
+        if (phase == 3) p2::k_attn_p2<128, true><<<grid, p2::THREADS2, p2::smem_bytes2<128>, st>>>(*c, B, block_table, o16, lse, sl2, g, TQ, tq, to, tk, tv);
+        else p2::k_attn_p2<128, false><<<grid, p2::THREADS2, p2::smem_bytes2<128>, st>>>(*c, B, block_table, o16, lse, sl2, g, TQ, tq, to, tk, tv);
+      } else {
+        if (phase == 3) p2::k_attn_p2<64, true><<<grid, p2::THREADS2, p2::smem_bytes2<64>, st>>>(*c, B, block_table, o16, lse, sl2, g, TQ, tq, to, tk, tv);
+        else p2::k_attn_p2<64, false><<<grid, p2::THREADS2, p2::smem_bytes2<64>, st>>>(*c, B, block_table, o16, lse, sl2, g, TQ, tq, to, tk, tv);
+      }
       IL_LAUNCH_CHECK("k_attn_p2");
       continue;
     }

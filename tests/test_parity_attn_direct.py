@@ -121,7 +121,7 @@ def test_direct_many_short_requests():
     run_case(32, 8, 128, reqs, seed=3, C=8192)
 
 
-@pytest.mark.parametrize("p2", ["1", "0"])
+@pytest.mark.parametrize("p2", ["1", "0", "dense_p2"])
 @pytest.mark.parametrize("Hq,Hkv,d", [(32, 8, 128), (16, 4, 64)])
 def test_direct_phase_orders(p2, Hq, Hkv, d, monkeypatch):
     # both cascade orders (read by il_prefill_attn at each call): the default -- the dense pass over
@@ -129,6 +129,10 @@ def test_direct_phase_orders(p2, Hq, Hkv, d, monkeypatch):
     # epilogue -- and IL_P2=0, each request's own part first on k_attn_sm100 (phase 2) continued by
     # the dense pass (phase 1); a shared prefix, short and multi-tile suffixes, one request without
     # a shared block beyond the prefix
-    monkeypatch.setenv("IL_P2", p2)
+    # ("dense_p2": the A / B variant IL_DENSE_P2=1, the dense pass on k_attn_p2 as well)
+    if p2 == "dense_p2":
+        monkeypatch.setenv("IL_DENSE_P2", "1")
+    else:
+        monkeypatch.setenv("IL_P2", p2)
     reqs = [(1600, 33), (1840, 1), (2048, 200), (1600, 64), (1760, 130), (1600, 1), (1616, 97)]
-    run_case(Hq, Hkv, d, reqs, shared_blocks=100, seed=17 + int(p2))
+    run_case(Hq, Hkv, d, reqs, shared_blocks=100, seed=17 + len(p2))
