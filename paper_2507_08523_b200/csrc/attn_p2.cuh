@@ -33,6 +33,9 @@ namespace sm100 {
 namespace p2 {
 
 constexpr uint32_t BN2 = 64;                      // keys per KV step
+#ifndef IL_P2_REV
+#define IL_P2_REV 1
+#endif
 #ifndef IL_P2_SKIP_PAD
 #define IL_P2_SKIP_PAD 0                          // (1: measured slower, 245 -> 255 us)
 #endif
@@ -134,6 +137,14 @@ __global__ void __launch_bounds__(THREADS2, 1)
     return __ldg(desc + t);
   };
   auto nsteps = [&](const uint4& dd) -> uint32_t { return DENSE ? 2 * NC : n_steps(dd, NC); };
+  // item ww of stream x -> M-tile: pair ww / Hkv, walked from the LAST pair when IL_P2_REV (phase 2:
+  // the dense pass wrote its last rows' partials last, so they are still in L2 when this starts)
+  // (stream x's tiles are x, x + 2, ..: nx = (ntl + 1 - x) / 2 of them; reversed, u -> nx - 1 - u, so
+  // that the items past the end stay the last ones and the streams' loops can stop at the first)
+  auto tile_of = [&](uint32_t ww, uint32_t x) -> uint32_t {
+    const uint32_t u = ww / Hkv, nx = (ntl + 1 - x) / 2;
+    return (IL_P2_REV && !DENSE) ? (u < nx ? 2 * (nx - 1 - u) + x : ntl) : 2 * u + x;
+  };
   // ring barrier i: the stream's own block, or (DENSE) both streams' blocks as one
   auto rbar = [&](uint32_t x, uint32_t i) {
     return DENSE ? (i < RB ? bar(0, K_RING2 + i) : bar(1, K_RING2 + i - RB)) : bar(x, K_RING2 + i);
@@ -183,20 +194,20 @@ __global__ void __launch_bounds__(THREADS2, 1)
     auto kfree = [&](uint32_t i) { return rbar(x, NK + i); };
     auto vfull = [&](uint32_t i) { return rbar(x, 2 * NK + i); };
     auto vfree = [&](uint32_t i) { return rbar(x, 2 * NK + NV + i); };
-    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + x < ntl; };
-    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + x); };
+    auto ok = [&](uint32_t ww) { return ww < n_items && tile_of(ww, x) < ntl; };
+    auto ld = [&](uint32_t ww) { return tdesc(tile_of(ww, x)); };
     uint32_t w = blockIdx.x;
     uint4 d = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
     if (DENSE && warp == 2) {
       // ============ (DENSE) Q producer: lane xq loads stream xq's Q tile of each item
       if (lane < 2) {
         const uint32_t xq = lane, qbytes = 2 * D * g * TQ, sqx = sbase + xq * QTILE;
-        auto okq = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xq < ntl; };
+        auto okq = [&](uint32_t ww) { return ww < n_items && tile_of(ww, xq) < ntl; };
         uint32_t ix = 0, wq = blockIdx.x;
-        uint4 dl = okq(wq) ? tdesc(2 * (wq / Hkv) + xq) : make_uint4(0, 0, 0, 0);
+        uint4 dl = okq(wq) ? tdesc(tile_of(wq, xq)) : make_uint4(0, 0, 0, 0);
         for (; okq(wq); wq += gridDim.x, ++ix) {
           const uint32_t wn = wq + gridDim.x;
-          const uint4 dn = okq(wn) ? tdesc(2 * (wn / Hkv) + xq) : dl;
+          const uint4 dn = okq(wn) ? tdesc(tile_of(wn, xq)) : dl;
           if (ix >= 1) mbar_wait(bar(xq, Q_FREE2), (ix - 1) & 1);
           mbar_expect_tx(bar(xq, Q_FULL2), qbytes);
 #pragma unroll
@@ -353,8 +364,8 @@ __global__ void __launch_bounds__(THREADS2, 1)
     const uint32_t xe = (warp - 12) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
     const uint32_t o_tmem = tmem + ((32 * q4) << 16) + 256 * xe + 128;
     const uint32_t t = r / g, hh = r % g;
-    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xe < ntl; };
-    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + xe); };
+    auto ok = [&](uint32_t ww) { return ww < n_items && tile_of(ww, xe) < ntl; };
+    auto ld = [&](uint32_t ww) { return tdesc(tile_of(ww, xe)); };
     uint32_t w = blockIdx.x, it = 0;
     uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
     while (ok(w)) {
@@ -428,8 +439,8 @@ __global__ void __launch_bounds__(THREADS2, 1)
     const uint32_t s_tmem = tmem + lane_addr + 256 * xo, o_tmem = s_tmem + 128;
     const uint32_t t = r / g;
     uint32_t it = 0, cs = 0;
-    auto ok = [&](uint32_t ww) { return ww < n_items && 2 * (ww / Hkv) + xo < ntl; };
-    auto ld = [&](uint32_t ww) { return tdesc(2 * (ww / Hkv) + xo); };
+    auto ok = [&](uint32_t ww) { return ww < n_items && tile_of(ww, xo) < ntl; };
+    auto ld = [&](uint32_t ww) { return tdesc(tile_of(ww, xo)); };
     uint32_t w = blockIdx.x;
     uint4 dcur = ok(w) ? ld(w) : make_uint4(0, 0, 0, 0);
     while (ok(w)) {
