@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(THREADS2, 1)
       const uint32_t pos_q = T.pos0 + min(t, T.ntok - 1);
       const uint32_t nst = nsteps(dcur);
       float m_used = -INFINITY, l = 0.f;
+#if IL_P2_SKIP_PAD
       const bool pad_warp = 32 * q4 >= g * T.ntok;         // (warp-uniform)
+#endif
       for (uint32_t n = 0; n < nst; ++n, ++cs) {
         const uint32_t b = cs & 1u, sb = s_tmem + 64 * b;
         mbar_wait(bar(xo, S_FULL2 + b), (cs >> 1) & 1);
