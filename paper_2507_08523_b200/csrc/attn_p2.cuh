@@ -37,7 +37,7 @@ constexpr uint32_t BN2 = 64;                      // keys per KV step
 #define IL_P2_REV 1
 #endif
 #ifndef IL_P2_SKIP_PAD
-#define IL_P2_SKIP_PAD 0                          // (1: measured slower, 245 -> 255 us)
+#define IL_P2_SKIP_PAD 0                          // (1: measured slower, 245 -> 255 us; also with P = 0 stored)
 #endif
 constexpr uint32_t KCB2 = BN2 * 128;              // one 64-column block of a 64-key K / V tile (8 KB)
 // per-stream K / V ring depths (64-key tiles): head dim 128 fills 224 KB with (2, 3)
