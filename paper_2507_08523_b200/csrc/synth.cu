@@ -15,24 +15,29 @@ namespace il {
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; return h ^ (h >> 16);
 }
-// the four elements (dims 4e .. 4e+3) of one mix, as two packed bf16 pairs
-__device__ __forceinline__ void synth_quad(uint64_t row_key, uint32_t e, float mul, uint32_t& w0, uint32_t& w1) {
+// the four elements (dims 4e .. 4e+3) of one mix, as two packed bf16 pairs.  (u - 128) / 256 * mul
+// is formed as ((2^23 + u) - (2^23 + 128)) * (mul / 256): both differences are exact, and the one
+// rounded product equals the generator's (f - 1.5) * mul with f = 1 + u / 256 (the same real number,
+// mul / 256 exact); 2^23 + u is one byte permute of v into 0x4B0000uu.
+__device__ __forceinline__ void synth_quad(uint64_t row_key, uint32_t e, float mul256, uint32_t& w0, uint32_t& w1) {
   const uint32_t v = fmix32(((uint32_t)row_key ^ (e * 0x9E3779B9u)) + (uint32_t)(row_key >> 32));
-  float f[4], x[4];
+  uint32_t b[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) f[j] = __uint_as_float(0x3F800000u | (((v >> (8 * j)) & 0xFFu) << 15));
-  // (f - 1.5) * mul on pairs: add.rn / mul.rn f32x2 round exactly like the scalar sub / mul
+  for (int j = 0; j < 4; ++j)                           // {0x4B, 0x00, 0x00, byte j of v}
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(b[j]) : "r"(v), "r"(0x4B000000u), "r"(0x7650u | (uint32_t)j));
+  float x[4];
 #pragma unroll
   for (int j = 0; j < 4; j += 2)
     asm("{ .reg .b64 a, c, m; mov.b64 a, {%2, %3}; mov.b64 c, {%4, %4}; add.rn.f32x2 a, a, c;\n\t"
         "mov.b64 m, {%5, %5}; mul.rn.f32x2 a, a, m; mov.b64 {%0, %1}, a; }"
-        : "=f"(x[j]), "=f"(x[j + 1]) : "f"(f[j]), "f"(f[j + 1]), "f"(-1.5f), "f"(mul));
+        : "=f"(x[j]), "=f"(x[j + 1]) : "f"(__uint_as_float(b[j])), "f"(__uint_as_float(b[j + 1])), "f"(-8388736.0f),
+          "f"(mul256));
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w0) : "f"(x[1]), "f"(x[0]));   // low half = dim 4e
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w1) : "f"(x[3]), "f"(x[2]));
 }
 
 // One warp per suffix row (grid-stride): the two (token, position) mixes are computed once per
-// row and tensor; each element then costs one mix.  Lanes write 8 consecutive bf16 (16 B).
+// row and tensor; each group of 4 elements then costs one mix.  Lanes write 8 consecutive bf16 (16 B).
 // PAGED: K and V go straight into the request's KV pages ([C][Hkv][16][d], page =
 // block_table[i][pos / 16], slot pos % 16) -- the projection's epilogue writing the paged cache, so
 // il_prefill_attn needs no separate append pass.
@@ -55,26 +60,33 @@ __global__ void __launch_bounds__(256) k_synth(Ctx c, uint32_t B, const uint32_t
     const uint64_t kq = mix64(mix64(sq ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint64_t kk = mix64(mix64(sk ^ (uint64_t)tok) ^ (uint64_t)pos);
     const uint64_t kv = mix64(mix64(sv ^ (uint64_t)tok) ^ (uint64_t)pos);
-    const uint32_t nvec = h_end * VPH;                  // head rows [h_begin, h_end) of Q | K | V
+    // head rows [h_begin, h_end) of Q | K | V, one 16-byte vector (8 dims) per lane and step; the
+    // three tensors in separate loops (no per-vector branching: the destination of vector e of a
+    // tensor is its row base + e * 8, with head = e / VPH)
     const size_t page_row = PAGED ? (size_t)(uint32_t)block_table[(size_t)i * c.max_blocks + pos / BS] * Hkv : 0;
-    for (uint32_t e = h_begin * VPH + lane; e < nvec; e += 32) {
-      const uint32_t h = e / VPH, x0 = (e % VPH) * 8;
-      uint64_t key;
-      float mul;
-      __nv_bfloat16* dst;
-      uint32_t hh;
-      if (h < Hq) { key = kq; mul = qmul; hh = h; dst = q + ((size_t)r * Hq + h) * D + x0; }
-      else if (h < Hq + Hkv) {
-        key = kk; mul = kvmul; hh = h - Hq;
-        dst = kn + (PAGED ? ((page_row + hh) * BS + pos % BS) * D : ((size_t)r * Hkv + hh) * D) + x0;
-      } else {
-        key = kv; mul = kvmul; hh = h - Hq - Hkv;
-        dst = vn + (PAGED ? ((page_row + hh) * BS + pos % BS) * D : ((size_t)r * Hkv + hh) * D) + x0;
+    const size_t slot = PAGED ? (page_row * BS + pos % BS) * D : 0;
+    auto quads = [&](uint64_t key, float mul256, uint32_t e) -> uint4 {
+      const uint32_t hh = e / VPH, eg = hh * 64 + (e % VPH) * 2;   // generator index of the first 4 dims
+      uint4 w;
+      synth_quad(key, eg, mul256, w.x, w.y);
+      synth_quad(key, eg + 1, mul256, w.z, w.w);
+      return w;
+    };
+    if (h_begin < Hq) {
+      uint4* dq = reinterpret_cast<uint4*>(q + (size_t)r * Hq * D);
+      for (uint32_t e = h_begin * VPH + lane; e < min(h_end, Hq) * VPH; e += 32) dq[e] = quads(kq, qmul * (1.f / 256.f), e);
+    }
+    if (h_end > Hq) {
+      const uint32_t nkv = Hkv * VPH;
+      uint4* dk = reinterpret_cast<uint4*>(kn + (PAGED ? slot : (size_t)r * Hkv * D));
+      uint4* dv = reinterpret_cast<uint4*>(vn + (PAGED ? slot : (size_t)r * Hkv * D));
+      // paged: head hh of the row lives BS * D elements after head hh - 1 ([page][Hkv][16][d])
+      const uint32_t hstride = PAGED ? BS * VPH : VPH;
+      for (uint32_t e = lane; e < nkv; e += 32) {
+        const uint32_t at = (e / VPH) * hstride + e % VPH;
+        dk[at] = quads(kk, kvmul * (1.f / 256.f), e);
+        dv[at] = quads(kv, kvmul * (1.f / 256.f), e);
       }
-      uint32_t w[4];
-      synth_quad(key, hh * 64 + x0 / 4, mul, w[0], w[1]);
-      synth_quad(key, hh * 64 + x0 / 4 + 1, mul, w[2], w[3]);
-      *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }
