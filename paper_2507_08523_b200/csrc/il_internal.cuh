@@ -62,7 +62,8 @@ struct DevScalars {
   uint64_t ring_tail;
   uint32_t dedup_sum;        // last prefix match: blocks shared in-batch (IL_F_DEDUP)
   uint32_t bd_n;             // in-batch dedup table: slots taken this batch (cleared by k_alloc_commit)
-  uint32_t pad1[2];
+  uint32_t probe_batch;      // low bits of the batch whose instruction probe il_refine_batch ran (0 = none)
+  uint32_t pad1;
 };
 
 struct Ctx {

@@ -413,7 +413,7 @@ extern "C" il_status il_prefix_match(il_ctx* c, uint32_t B, const uint32_t* prom
   const uint64_t b_cur = c->batch + 1;
   const bool dedup = (c->cfg.flags & IL_F_DEDUP) && B > 1;
   k_match_begin<<<1, 1, 0, st>>>(*c);
-  k_instr_probe<<<1, 256, 0, st>>>(*c);
+  k_instr_probe<<<1, 256, 0, st>>>(*c, 0u);
   if (B) k_hash_match<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit, block_table,
                                                            dedup ? 1u : 0u);
   if (dedup) k_bd_resolve<<<cdiv(B * 32, 256), 256, 0, st>>>(*c, B, prompt_tok, prompt_len, block_hash, hit);

@@ -76,10 +76,18 @@ __device__ __forceinline__ uint32_t warp_hash_match(const Ctx& c, const uint32_t
 }
 
 // Once per batch: the leading run of the instruction's blocks resident (and verified) in the
-// index snapshot, and their pages.  One CTA, one thread per block.
-static __global__ void __launch_bounds__(256) k_instr_probe(Ctx c) {
+// index snapshot, and their pages.  One CTA, one thread per block.  from_refine: il_refine_batch's
+// probe (guard), which records the batch; il_prefix_match's probe then reuses it -- nothing changes
+// the index between the two -- and clears the record, so a second match of the batch probes again.
+static __global__ void __launch_bounds__(256) k_instr_probe(Ctx c, uint32_t from_refine) {
   __shared__ uint32_t s_first_bad;
   const uint32_t nI = c.n_instr_blocks;
+  const uint32_t b_cur = (uint32_t)(c.sc->batch_done + 1);
+  if (!from_refine && c.sc->probe_batch == b_cur) {    // (uniform over the CTA)
+    __syncthreads();
+    if (threadIdx.x == 0) c.sc->probe_batch = 0;
+    return;
+  }
   const bool verify = (c.cfg.flags & IL_F_VERIFY) != 0;
   if (threadIdx.x == 0) s_first_bad = nI;
   __syncthreads();
@@ -95,7 +103,10 @@ static __global__ void __launch_bounds__(256) k_instr_probe(Ctx c) {
     if (!ok) atomicMin(&s_first_bad, j);
   }
   __syncthreads();
-  if (threadIdx.x == 0) c.sc->instr_hits = s_first_bad;
+  if (threadIdx.x == 0) {
+    c.sc->instr_hits = s_first_bad;
+    c.sc->probe_batch = from_refine ? b_cur : 0u;
+  }
 }
 
 }  // namespace il

@@ -428,7 +428,7 @@ extern "C" il_status il_refine_batch(il_ctx* c, uint32_t B, const uint32_t* q_of
     il_status r = select_launch(c, B, q_off, q_tok, q_src, topk, st);
     if (r != IL_OK) return r;
   }
-  if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c);
+  if (c->cfg.flags & IL_F_GUARD) k_instr_probe<<<1, 256, 0, st>>>(*c, 1u);
   k_refine<<<B, REF_THREADS, 0, st>>>(*c, B, q_off, q_tok, topk, final_ds, info, prompt_tok, prompt_len);
   IL_LAUNCH_CHECK("il_refine_batch");
   c->launches += (c->cfg.flags & IL_F_GUARD) ? 2 : 1;
