@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(THREADS2, 1)
       const uint32_t r0 = t * TQ, nt = r0 < q_total ? min(TQ, q_total - r0) : 0u;
       return make_uint4(0u, 1u << 30, r0, nt | ((8 * NC) << 8));
     }
+    IL_CHECK(t < c.sc->n_tiles);
     return __ldg(desc + t);
   };
   auto nsteps = [&](const uint4& dd) -> uint32_t { return DENSE ? 2 * NC : n_steps(dd, NC); };
@@ -233,7 +234,10 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #ifdef IL_P2_SAME_PAGES
         return __ldg(block_table + (blk < (dd.w >> 8) ? blk : 0u));   // profiling variant: every tile reads request 0's pages
 #else
-        return __ldg(block_table + (size_t)dd.x * c.max_blocks + (blk < (dd.w >> 8) ? blk : 0u));
+        IL_CHECK(dd.x < B && (dd.w >> 8) <= c.max_blocks);
+        const int32_t pg = __ldg(block_table + (size_t)dd.x * c.max_blocks + (blk < (dd.w >> 8) ? blk : 0u));
+        IL_CHECK(pg >= 0 && (uint32_t)pg < c.cfg.kv_pages);
+        return pg;
 #endif
       };
       auto pages_of = [&](const uint4& dd) -> int32_t {
@@ -421,7 +425,10 @@ __global__ void __launch_bounds__(THREADS2, 1)
 #else
         if (valid)
 #endif
+        {
+          IL_CHECK(orow < (size_t)q_total * Hq && T.row0 + T.ntok <= q_total);
           st_v8(out + orow * D + 16 * h, w8);
+        }
       }
       if (valid) {
         if (DENSE) c.attn_ml[orow] = mm + __log2f(L);    // the partial the phase-2 kernel merges

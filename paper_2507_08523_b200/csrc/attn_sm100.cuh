@@ -28,6 +28,14 @@
 namespace il {
 namespace sm100 {
 
+// IL_CHECKS builds (scripts/gpu_checks.sh; the pool refuses compute-sanitizer): every global index
+// the attention kernels form is checked against its buffer's extent, a violation traps
+#ifdef IL_CHECKS
+#define IL_CHECK(cond) do { if (!(cond)) { printf("IL_CHECK failed %s:%d %s\n", __FILE__, __LINE__, #cond); __trap(); } } while (0)
+#else
+#define IL_CHECK(cond) do { } while (0)
+#endif
+
 #ifdef IL_ATTN_TRACE
 // debug build only (build.py --trace): per-tile clock64 stamps of each role in CTA 0
 __device__ unsigned long long g_trace[16][4096];
@@ -630,6 +638,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     Load L;
     for (uint32_t lc = 0; seq.next(L); ++lc) {
       const int32_t* bt = block_table + (size_t)L.req * c.max_blocks;
+      IL_CHECK(L.req < B && L.kvt * 8 < c.max_blocks + 8);
       const uint32_t blk = L.kvt * 8 + (lane & 7);
       const int32_t page = blk < L.nblk ? __ldg(bt + blk) : __ldg(bt);
       const uint32_t s = lc % nst, u = lc / nst;
@@ -911,7 +920,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           float ov[32];
           tmem_ld32(o_tmem + 32 * q, ov);
           tmem_wait_ld();
-          if (valid) store_row32(out + orow * D + 32 * q, ov, inv);
+          if (valid) {
+            IL_CHECK(orow < (size_t)c.sc->q_total * Hq);
+            store_row32(out + orow * D + 32 * q, ov, inv);
+          }
         }
         if (valid) {
           if ((phase == 2 && cascade) || phase == 3) c.attn_ml[orow] = m_used + __log2f(l);
