@@ -213,10 +213,13 @@ il_status il_prefix_match(il_ctx* ctx, uint32_t B,
  *                 in the pages (il_synth_qkv_paged: the projection epilogue wrote them)
  *   k_pages, v_pages  [C][Hkv][16][d] bf16, caller-owned, persistent across batches
  * bf16 in, fp32 accumulation (Z26); parity <= 1e-2 vs the fp64 oracle (Z27).
- * Runs on the tcgen05/TMA kernel (head_dim 64 or 128, Hq/Hkv in 1..8; il_create rejects any
- * other shape with IL_ERR_ARG, there is no other attention kernel).  Requires a preceding il_prefix_match of the same batch (IL_ERR_STATE otherwise);
- * out and the workspace hold the cascade's partial between its two launches, so out must not be
- * read before the call's work completes on stream s. */
+ * Runs on two tcgen05/TMA kernels (head_dim 64 or 128, Hq/Hkv in 1..8; il_create rejects any
+ * other shape with IL_ERR_ARG, there is no other attention path): the keys every request of the
+ * batch reads from the same pages (the instruction) as one dense pass over all suffix rows,
+ * then each request's own keys, merged with the dense pass's partial through log-sum-exp (the
+ * cascade).  Requires a preceding il_prefix_match of the same batch
+ * (IL_ERR_STATE otherwise); out and the workspace hold the cascade's partial between the two
+ * launches, so out must not be read before the call's work completes on stream s. */
 il_status il_prefill_attn(il_ctx* ctx, uint32_t B, const int32_t* cu_q, const int32_t* prefix_len,
                           const int32_t* block_table,
                           const il_bf16* q, const il_bf16* k_new, const il_bf16* v_new,
