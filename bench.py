@@ -215,6 +215,7 @@ def run_ours(args, rank, world, local_rank):
     # (IL_SPLIT_SYNTH=1: batch j+1's Q on the integer stream, its K / V after batch j's attention --
     # measured slower, 1.10-1.11 vs 1.06 ms per step: the integer stream only has the attention's gaps)
     split_synth = piped and not args.no_fused_kv and bool(os.environ.get("IL_SPLIT_SYNTH"))
+    select_ahead = os.environ.get("IL_SELECT_AHEAD", "1") == "1"    # (0: select in batch order)
     # (two per-batch buffer slots for the pipelined schedule: batch b's attention reads slot b % 2
     # while batch b+1's integer stages write the other)
     pl = Pipeline(ccfg, dev, qkv_seed=cfg.qkv_seed, stream=stream, fused_kv=not args.no_fused_kv,
@@ -441,21 +442,38 @@ def run_ours(args, rank, world, local_rank):
         e0, e1 = ev(), ev()
         e0.record(stream)
         sA.wait_stream(stream)
+        # select_ahead: batch j+1's a1-a2 (il_select_batch reads only the pool) is issued right after
+        # batch j's match, ahead of batch j's commit, so it runs beside batch j's QKV stand-in instead
+        # of after batch j's attention (the integer stream only gets the SMs the attention leaves)
+        ahead = select_ahead and stage_names[0] == "select"
+
+        def stage_in(jj, xx):
+            pl.use(jj % 2)
+            if host:
+                qo, qt, qs, B = xx[:4]
+                pl.q_off[:B + 1].copy_(qo, non_blocking=True)
+                pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
+                pl.q_src[:B].copy_(qs, non_blocking=True)
+                pl.B = B
+            else:
+                set_inputs(xx)
+
+        if ahead:
+            with torch.cuda.stream(stream):
+                stage_in(0, inputs[0])
+                run_stage("select")
         for j, x in enumerate(inputs):
             with torch.cuda.stream(stream):
                 if j >= 2:
                     stream.wait_event(ev_a[j - 2])     # slot j % 2 is free again
-                pl.use(j % 2)
-                if host:
-                    qo, qt, qs, B = x[:4]
-                    pl.q_off[:B + 1].copy_(qo, non_blocking=True)
-                    pl.q_tok[:qt.numel()].copy_(qt, non_blocking=True)
-                    pl.q_src[:B].copy_(qs, non_blocking=True)
-                    pl.B = B
+                if ahead:
+                    pl.use(j % 2)
+                    pl.B = x[3]
                 else:
-                    set_inputs(x)
+                    stage_in(j, x)
                 for name in stage_names[:-3]:          # select, refine, match
-                    run_stage(name)
+                    if not (ahead and name == "select"):
+                        run_stage(name)
                 if split_synth:
                     graphs[j % 2, "synth_q"].replay()  # Q of batch j: no page writes
                 ev_m[j].record(stream)
@@ -463,6 +481,11 @@ def run_ours(args, rank, world, local_rank):
                     out_fin[:x[3]].copy_(pl.final_ds[:x[3]], non_blocking=True)
                     out_hit[:x[3]].copy_(pl.hit[:x[3]], non_blocking=True)
                     out_info[:x[3]].copy_(pl.info[:x[3]], non_blocking=True)
+                if ahead and j + 1 < n:                # batch j+1's inputs + a1-a2 into slot (j+1) % 2
+                    stage_in(j + 1, inputs[j + 1])     # (batch j-1's attention reads none of them)
+                    run_stage("select")
+                    pl.use(j % 2)
+                    pl.B = x[3]
             with torch.cuda.stream(sA):
                 sA.wait_event(ev_m[j])
                 for name in (("synth_kv" if split_synth else "synth"), "attn"):

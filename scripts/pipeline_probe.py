@@ -131,6 +131,19 @@ def main():
 
     for _ in range(2):
         serial(W)
+    if os.environ.get("PROBE_TRACE"):
+        # kernel timeline of a few pipelined steps (CUPTI): which kernels of the integer stream
+        # run beside the attention and which wait for it
+        from torch.profiler import ProfilerActivity, profile
+        pipelined(W, "none")
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            pipelined(6, "none")
+        torch.cuda.synchronize()
+        evs = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+        t0 = evs[0].time_range.start
+        for e in evs[-int(os.environ.get("PROBE_TRACE_N", "80")):]:
+            print(f"{e.time_range.start - t0:10.1f} +{e.time_range.elapsed_us():8.1f} us  {e.name[:70]}", flush=True)
+        return
     print(f"serial: {serial(K):.4f} ms/step", flush=True)
     for fl in ("A", "B", "none"):
         pipelined(W, fl)
