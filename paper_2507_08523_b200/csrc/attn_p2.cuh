@@ -18,13 +18,16 @@
 //
 // Work: the two Q tiles of a CTA are two independent PIPELINES (streams) x = 0 / 1, each with
 // its own Q buffer, K / V rings, TMA producer warp and MMA issuer warp; they share only the tensor
-// pipe and the SM's issue slots.  Stream x takes items w = blockIdx.x + k gridDim.x while M-tile
-// 2 (w / Hkv) + x exists; item w = that phase-2 M-tile (decode: one 16-byte k_tile_scan
-// descriptor, read one item ahead) with kv head w % Hkv.  Warp roles: warp 2x = producer of
-// stream x (Q, K and V TMAs; warp 2 also allocates TMEM), warp 2x + 1 = MMA issuer of stream x,
-// warps 4-7 / 8-11 = softmax + epilogue of stream 0 / 1.  The issuer's order per step s of an
-// item is QK(s), then PV(s - 1) (so the softmax of step s - 1 overlaps QK(s)), and PV(last) right
-// after the item's last QK; QK(s) overwrites the S buffer of step s - 2, whose PV precedes it.
+// pipe and the SM's issue slots.  Stream x takes items w = blockIdx.x + k gridDim.x; item w = M-tile
+// tile_of(w, x) (the x-th of pair w / Hkv, pairs walked from the last one: IL_P2_REV) with kv head
+// w % Hkv; a tile is decoded from one 16-byte k_tile_scan descriptor read one item ahead.  Warp
+// roles: warp 2x = producer of stream x (Q, K and V TMAs; warp 2 also allocates TMEM), warp 2x + 1
+// = MMA issuer of stream x, warps 4-7 / 8-11 = softmax of stream 0 / 1, warps 12-15 / 16-19 =
+// epilogue of stream 0 / 1 (l and m handed over through smem; O read into registers and released
+// before the dense pass's partial is read and merged).  The issuer's order per step s of an item is
+// QK(s), then PV(s - 1) (so the softmax of step s - 1 overlaps QK(s)), and PV(last) right after the
+// item's last QK; QK(s) overwrites the S buffer of step s - 2, whose PV precedes it.
+// DENSE = true (an A / B variant, IL_DENSE_P2=1) runs the dense pass itself on this design.
 #pragma once
 // (included from attn_sm100.cuh after namespace sm100: uses its PTX wrappers, Tile and decode_tile)
 
