@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for v in default p3e01 p3e11 p3e49 default p3e11; do
+for v in default k2v3 nosplit default k2v3 nosplit; do
   unset IL_LIB_VARIANT
   if [ $v != default ]; then export IL_LIB_VARIANT=$v; fi
   IL_BENCH_PROFILE=1 IL_BENCH_PROFILE_N=60 timeout 600 python bench.py --no-cpu-baseline --steps 10 --serial > gpurun_out/p3e_$v.json 2> gpurun_out/p3e_$v.err
