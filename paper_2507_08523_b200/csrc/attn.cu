@@ -124,6 +124,7 @@ il_status il::attn_setup(Ctx*) {
                                sm100::smem_bytes(128)));
   IL_CUDA(cudaFuncSetAttribute(sm100::k_attn_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                sm100::smem_bytes(64)));
+  IL_CUDA(cudaFuncSetAttribute(sm100::d2::k_attn_dense2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::d2::SMEM));
   using sm100::p2::k_attn_p2;
   IL_CUDA(cudaFuncSetAttribute(k_attn_p2<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<128>));
   IL_CUDA(cudaFuncSetAttribute(k_attn_p2<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm100::p2::smem_bytes2<64>));

@@ -126,7 +126,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   long long t0 = 0;
   do {
     if (t0 == 0) t0 = clock64();
+#ifdef IL_CHECKS
+    else if (clock64() - t0 > (1ll << 32)) {
+      printf("mbar_wait timeout: block %d thread %d bar smem+0x%x parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
+      __trap();
+    }
+#else
     else if (clock64() - t0 > (1ll << 34)) __trap();
+#endif
 #if IL_WAIT_HINT_NS > 0
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
@@ -1005,6 +1012,7 @@ __global__ void __launch_bounds__(256) k_shared_scan(Ctx c, uint32_t B, const in
 }  // namespace il
 
 #include "attn_p2.cuh"
+#include "attn_dense2.cuh"
 
 namespace il {
 
@@ -1061,6 +1069,9 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   // rings) instead of k_attn_sm100 phase 3 -- measured slower, 644 vs 512 us
   const char* pd = getenv("IL_DENSE_P2");
   const bool dense_old = !(pd && pd[0] == '1');
+  // IL_DENSE2=1: the dense pass on the CTA-pair kernel (attn_dense2.cuh; head dim 128)
+  const char* pd2 = getenv("IL_DENSE2");
+  const bool dense2 = pd2 && pd2[0] == '1' && D == 128;
   k_tile_scan<<<1, 1024, 0, st>>>(*c, B, cu_q, prefix_len, TQ, cascade ? 1u : 0u);
   if (cascade && B > 1) k_shared_scan<<<c->num_sms * 2, 256, 0, st>>>(*c, B, prefix_len, block_table);
   if (!decode && !p2) k_pair_scan<<<c->num_sms * 4, 256, 0, st>>>(*c, cu_q, prefix_len, block_table, TQ);
@@ -1088,7 +1099,13 @@ static inline il_status attn_sm100_launch(Ctx* c, uint32_t B, const int32_t* cu_
   for (uint32_t phase : {p1_first ? 3u : 2u, p1_first ? 2u : 1u}) {
     if (phase == 2 && decode) continue;
     if ((phase == 1 || phase == 3) && !cascade) continue;
-    // phase 2, and (unless IL_DENSE_OLD=1) the dense pass too, on k_attn_p2
+    if (phase == 3 && dense2) {
+      d2::k_attn_dense2<128><<<grid & ~1, THREADS, d2::SMEM, st>>>(*c, block_table, (__nv_bfloat16*)out,
+                                                                 scale * 1.4426950408889634f, g, TQ, tq, tk, tv);
+      IL_LAUNCH_CHECK("k_attn_dense2");
+      continue;
+    }
+    // phase 2, and (IL_DENSE_P2=1) the dense pass too, on k_attn_p2
     if ((phase == 2 && p2) || (phase == 3 && !dense_old)) {
       const float sl2 = scale * 1.4426950408889634f;
       __nv_bfloat16* o16 = (__nv_bfloat16*)out;

@@ -121,7 +121,7 @@ def test_direct_many_short_requests():
     run_case(32, 8, 128, reqs, seed=3, C=8192)
 
 
-@pytest.mark.parametrize("p2", ["1", "0", "dense_p2"])
+@pytest.mark.parametrize("p2", ["1", "0", "dense_p2", "dense2"])
 @pytest.mark.parametrize("Hq,Hkv,d", [(32, 8, 128), (16, 4, 64)])
 def test_direct_phase_orders(p2, Hq, Hkv, d, monkeypatch):
     # both cascade orders (read by il_prefill_attn at each call): the default -- the dense pass over
@@ -132,7 +132,9 @@ def test_direct_phase_orders(p2, Hq, Hkv, d, monkeypatch):
     # ("dense_p2": the A / B variant IL_DENSE_P2=1, the dense pass on k_attn_p2 as well)
     if p2 == "dense_p2":
         monkeypatch.setenv("IL_DENSE_P2", "1")
+    elif p2 == "dense2":                               # the CTA-pair dense pass (head dim 128; 64 falls back)
+        monkeypatch.setenv("IL_DENSE2", "1")
     else:
         monkeypatch.setenv("IL_P2", p2)
     reqs = [(1600, 33), (1840, 1), (2048, 200), (1600, 64), (1760, 130), (1600, 1), (1616, 97)]
-    run_case(Hq, Hkv, d, reqs, shared_blocks=100, seed=17 + len(p2))
+    run_case(Hq, Hkv, d, reqs, shared_blocks=100, seed=17)      # (the same inputs for every variant)
