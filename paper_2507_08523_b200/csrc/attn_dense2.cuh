@@ -1,8 +1,8 @@
 // attn_dense2.cuh — the cascade's dense pass (every suffix row of the batch over the batch-shared
 // prefix, P:182 / P:188-198) on a CTA PAIR: tcgen05.mma.cta_group::2, M = 256.
 // A/B variant behind IL_DENSE2=1 (head dim 128); the default dense pass is k_attn_sm100 phase 3.
-// Parity green (test_parity_attn_direct), but measured SLOWER: 836 vs 512 us at c3 -- every step
-// hands off six times across the pair (S read x 2, P halves x 4 through cluster-scope mbarrier
+// Parity green (test_parity_attn_direct), but measured SLOWER: 781 vs 512 us at c3 -- every step
+// hands off four times across the pair (S read and P, per tile, through cluster-scope mbarrier
 // arrives after a named barrier) and the leader's issuer waits on each in turn.
 //
 // Why.  On one CTA the per-tile chain S -> softmax -> P (over S in TMEM) -> PV + next
@@ -214,10 +214,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (first && it > 0) mbar_wait_c(bar(O_FREE + x), (it - 1) & 1);
         mbar_wait_c(bar(V_FULL + vs), (l / NV) & 1);
         const uint32_t o_tmem = tmem + 256 + 128 * x;
+        mbar_wait_c(bar(P_FULL + 2 * x), s & 1);        // both P halves of the tile (one hand-off)
+        tc_fence_after();
 #pragma unroll
         for (uint32_t h = 0; h < 2; ++h) {
-          mbar_wait_c(bar(P_FULL + 2 * x + h), s & 1);
-          tc_fence_after();
           const uint64_t dp = dp0 + (uint64_t)(((2 * x + h) * HALF) >> 4);
           const uint64_t dv = dv0 + (uint64_t)((vs * HALF + h * 4 * 2048) >> 4);
 #pragma unroll
@@ -345,10 +345,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + ((q ^ (r & 7)) << 4)), "r"(pk[4 * q]),
                          "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                          : "memory");
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> the tensor core
-          __syncwarp(); asm volatile("barrier.sync %0, 128;" ::"r"(1 + xo) : "memory");
-          if (r == 0) arrive_cluster(to_leader(bar(P_FULL + 2 * xo + h)));
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // generic-proxy writes -> the tensor core
+        __syncwarp(); asm volatile("barrier.sync %0, 128;" ::"r"(1 + xo) : "memory");
+        if (r == 0) arrive_cluster(to_leader(bar(P_FULL + 2 * xo)));
         l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
       }
       // epilogue: O / l (bf16) and m + log2 l: the partial k_attn_p2 merges
